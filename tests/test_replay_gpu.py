@@ -1,0 +1,78 @@
+"""Golden-stream parity of the GPU engine (pytest -m gpu).
+
+* every recorded reference SimEngine run replayed through the drop-in API;
+* the cfg 4 sweeps run in one gs_sweep launch vs the reference's events;
+* 10^5 / 10^6-probe sweeps vs the (golden-pinned) C oracle.
+"""
+
+import ctypes
+
+import numpy as np
+import pytest
+
+from replay import DropinBackend, load_sim_runs, load_sweeps, replay_run
+
+pytestmark = pytest.mark.gpu
+
+RUNS = list(load_sim_runs())
+SWEEPS = load_sweeps()
+LABELS = sorted(k for k in SWEEPS if "." not in k)
+
+
+@pytest.mark.parametrize("chunk", range(8))
+def test_dropin_replays_reference_streams(chunk):
+    n = 0
+    for run in RUNS[chunk::8]:
+        n += replay_run(DropinBackend(), run)
+    assert n > 0
+
+
+def run_gpu_sweep(spec, n_dev, probes, max_res, policy):
+    from paper_2107_08538_b200 import _native as nat
+    from paper_2107_08538_b200.gpushare import DeviceState, Scheduler, parse_policy
+
+    devs = [DeviceState(spec, i) for i in range(n_dev)]
+    sched = Scheduler(devs, parse_policy(policy))
+    cap = 2 * len(probes) + 16
+    ev = np.zeros((cap, 3), dtype=np.int32)
+    ne, ms = ctypes.c_int64(), ctypes.c_float()
+    nat.check(nat.lib().gs_sweep(sched._ptr, probes.ctypes.data, len(probes), max_res, ev.ctypes.data, cap,
+                                 ctypes.byref(ne), ctypes.byref(ms)))
+    final = np.array([[d.free_mem, d.in_use_warps, d.rr_cursor, d.version,
+                       __import__("replay").sm_crc((d.sm_warps, d.sm_tbs, d.sm_regs, d.sm_smem))]
+                      for d in devs], dtype=np.int64)
+    return ev[: ne.value], final, ms.value
+
+
+def sweep_inputs(label):
+    from paper_2107_08538_b200.gpushare.device_model import DeviceSpec
+    from paper_2107_08538_b200.sweep import gen_probes
+
+    meta = SWEEPS[label + ".meta"]
+    n_dev, n, seed, max_res, pol = (int(x) for x in meta[:5])
+    spec = DeviceSpec("s", *[int(x) for x in meta[5:]])
+    return spec, n_dev, gen_probes(n, seed), max_res, ("mgb-warps" if pol == 0 else "mgb-sm")
+
+
+@pytest.mark.parametrize("label", LABELS)
+def test_gpu_sweep_matches_reference(label):
+    spec, n_dev, probes, max_res, policy = sweep_inputs(label)
+    ev, final, _ = run_gpu_sweep(spec, n_dev, probes, max_res, policy)
+    np.testing.assert_array_equal(ev, SWEEPS[label])
+    np.testing.assert_array_equal(final, SWEEPS[label + ".final"])
+
+
+@pytest.mark.parametrize("n,policy", [(100_000, "mgb-sm"), (1_000_000, "mgb-warps"),
+                                      (200_000, "mgb-sm")])
+def test_gpu_sweep_matches_oracle_at_scale(n, policy):
+    from oracle import oracle as O
+    from paper_2107_08538_b200.gpushare import device_spec
+    from paper_2107_08538_b200.sweep import gen_probes
+
+    spec = device_spec("b200")
+    probes = gen_probes(n, seed=11)
+    ev, final, ms = run_gpu_sweep(spec, 8, probes, 32, policy)
+    devs = [O.OracleDevice(spec, i) for i in range(8)]
+    oev = O.OracleScheduler(devs, 2 if policy == "mgb-sm" else 3, 6, True).sweep(probes, 32)
+    np.testing.assert_array_equal(ev, oev)
+    np.testing.assert_array_equal(final, np.array([d.snapshot() for d in devs], dtype=np.int64))
