@@ -43,6 +43,10 @@ extern "C" {
 #define GS_REJECTED 2
 #define GS_NOT_TRIED 3
 
+/* gs_probe.level flag bits */
+#define GS_PROBE_JOB 1
+#define GS_PROBE_FRESH 2
+
 /* policies — schedulers.py:26-53 PolicyConfig.kind */
 #define GS_POLICY_SA 0
 #define GS_POLICY_CG 1
@@ -85,7 +89,9 @@ typedef struct gs_probe {
     int32_t smem_per_block;
     int32_t handle;   /* task uid handle (residency row) */
     int32_t job;      /* job id handle */
-    int32_t level;    /* 0 = "task", 1 = "job" */
+    int32_t level;    /* bit 0: 1 = "job" level, 0 = "task"; bit 1 (GS_PROBE_FRESH):
+                       * the caller guarantees no device holds a residency row
+                       * for `handle`, so the decision skips reading it */
 } gs_probe;
 
 /* Per-device ledger header, in pinned host-mapped memory so the host reads
@@ -98,6 +104,14 @@ typedef struct gs_ledger {
     int64_t version;
     int64_t held_mem;     /* Σ resident mem_bytes (check_conservation) */
     int64_t held_warps;   /* Σ resident warps */
+    /* Grow epoch: bumped by every operation that can ENLARGE a device's
+     * free resources (release_task, negative reservations) and by host-side
+     * writes to the ledger.  A scheduler's FIFO re-drive only re-scores
+     * pending probes against devices whose epoch moved since its last full
+     * pass — exact, because inside and between passes resources otherwise
+     * only shrink (schedulers.py:105-112 tries every pending request). */
+    int64_t grow_epoch;
+    int64_t reserved;     /* keeps the header 64 B (arrays 16 B aligned) */
     int32_t rr_cursor;
     int32_t sm_count;
 } gs_ledger;
@@ -122,7 +136,7 @@ typedef struct gs_residency {
     int32_t present;
     int32_t has_blocks;
     int32_t warps_per_block;
-    int32_t pad;
+    int32_t thread_blocks;  /* Σ blocks_per_sm of the committed plan */
 } gs_residency;
 
 typedef struct gs_engine gs_engine;

@@ -58,7 +58,8 @@ assert PROBE_DTYPE.itemsize == ctypes.sizeof(GsProbe) == 64
 class GsLedger(ctypes.Structure):
     _fields_ = [("free_mem", c_int64), ("in_use_warps", c_int64),
                 ("version", c_int64), ("held_mem", c_int64),
-                ("held_warps", c_int64), ("rr_cursor", c_int32),
+                ("held_warps", c_int64), ("grow_epoch", c_int64),
+                ("reserved", c_int64), ("rr_cursor", c_int32),
                 ("sm_count", c_int32)]
 
 

@@ -6,23 +6,30 @@
 //   _try_mgb_sm (Alg. 2) / _try_mgb_warps (Alg. 3)    schedulers.py:137-171
 //   _try_sa / _try_cg / _impossible_everywhere        schedulers.py:173-199
 //
-// Design: one CTA of 256 threads is the single decision
-// authority.  It stages every device ledger (free HBM, in-use warps, per-SM
-// warps/TBs/regs/smem; 2.4 KB per 148-SM device) from pinned host-mapped
-// memory into shared memory, interprets a command stream in arrival order
-// (linearizable), and writes the dirty ledgers back.
-//   * mgb-warps: lane d scores device d; ballot(free_mem >= mem) +
-//     warp argmin over (in_use_warps, d).
-//   * mgb-sm: warp w scores device w in parallel (per-SM residual capacity
-//     over 148 SMs, 64-bit warp reductions); the first feasible device in
-//     index order commits using the closed-form round-robin water-fill of
-//     SURVEY.md App. A (binary search on full rounds + ballot prefix ranks
-//     in cursor order) instead of the reference's one-block-per-visit loop.
-//   * on_release: a parallel prefilter marks pending probes that cannot fit
-//     the pass-start ledgers (exact: resources only shrink inside a pass),
-//     then survivors are decided serially in FIFO order.
+// Design.  Decisions are a serial dependency chain (each
+// ASSIGN mutates the ledgers the next decision reads), so the
+// decision authority is ONE warp: no block barriers on the chain, all
+// reductions are shuffles/ballots.  The warp stages every device ledger
+// (free HBM, in-use warps, per-SM warps/TBs/regs/smem; 2.4 KB per 148-SM
+// device, 19 KB for 8 x B200) into shared memory with 16-byte loads, runs a
+// command stream in arrival order, and writes dirty ledgers back.
+//   * mgb-warps: lane d scores device d: ballot(free_mem >= mem), then a
+//     64-bit warp argmin over (in_use_warps, d).
+//   * mgb-sm: devices in index order; per device the lanes compute per-SM
+//     residual capacity over all SMs (warp-reduced); the first feasible
+//     device commits through the closed-form round-robin water-fill of
+//     SURVEY.md App. A (binary search on full rounds, ballot prefix ranks in
+//     cursor order) instead of the reference's one-block-per-visit loop.
+//   * on_release: only devices whose resources GREW since the scheduler's
+//     last full pass can admit anything (pending requests were infeasible
+//     everywhere at their last try, and resources otherwise only shrink), so
+//     each pass scores pending probes against those devices only, first
+//     with an O(1) aggregate-capacity bound (lane-parallel, 32 probes at a
+//     time), then exactly, in FIFO order; admitted entries are compacted out
+//     in place chunk by chunk.
 // Residency rows (_Residency, device_model.py:69-77) live in HBM, indexed
-// by the interned task handle.
+// by the interned task handle; the rows a decision may touch are prefetched
+// while the devices are being scored.
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <string.h>
@@ -38,9 +45,12 @@
 
 namespace {
 
-constexpr int kThreads = 256;
-constexpr int kWarps = kThreads / 32;
+constexpr int kThreads = 32;  // the decision chain runs on one warp
+constexpr unsigned kFull = 0xffffffffu;
 constexpr int kRowHdrWords = sizeof(gs_residency) / 4;  // 12
+constexpr int kLedHdrWords = sizeof(gs_ledger) / 4;     // 16
+static_assert(sizeof(gs_ledger) == 64, "ledger header must be 64 B");
+static_assert(sizeof(gs_probe) == 64, "probe record must be 64 B");
 
 enum Op : int32_t {
   OP_SUBMIT = 1,
@@ -61,32 +71,38 @@ struct Cmd {
   int64_t a, b;
   gs_probe probe;
 };
-static_assert(sizeof(gs_probe) == 64, "probe record must be 64 B");
+static_assert(sizeof(Cmd) == 96, "command record is 96 B");
 
 struct SchedState {  // pinned host-mapped
   int32_t sa_owner[GS_MAX_DEVICES];
   int32_t cg_counts[GS_MAX_DEVICES];
+  int64_t seen_epoch[GS_MAX_DEVICES];
   int32_t cg_cursor;
   int32_t pend_count;
   int32_t fifo_head, fifo_tail;
   int32_t n_tried, n_admitted;
-  int32_t pad0, pad1;
+  int32_t error, pad;
   int64_t n_events;
 };
 
 struct KDev {
-  gs_ledger *led;   // device pointer of the mapped ledger
-  int32_t *res;     // residency rows in HBM
-  int32_t stride;   // words per residency row
+  gs_ledger *led;    // device pointer of the mapped ledger
+  int32_t *res;      // residency rows in HBM
+  int32_t stride;    // words per residency row
   int32_t n_sm;
-  int32_t arr_pad;  // padded array length (ledger + smem)
-  int32_t smem_off; // int offset of this device's arrays in dynamic smem
+  int32_t arr_pad;   // padded per-SM array length
+  int32_t smem_off;  // int offset of this device's staged block in dyn smem
+  int32_t fast;      // all spec per-SM limits < 2^22 (32-bit cap arithmetic)
+  int32_t pad;
   gs_spec spec;
 };
 
 struct KParams {
   int32_t n_dev, policy, cg_ratio, skip_ahead;
   int32_t n_cmds, max_sm_pad, max_resident, sweep;
+  int32_t stage_q;   // int4 count of all staged ledger blocks
+  int32_t scratch_off;
+  int32_t fifo_off, fifo_cap, fifo_stride, pad0;
   KDev dev[GS_MAX_DEVICES];
   SchedState *st;
   const Cmd *cmds;
@@ -95,11 +111,9 @@ struct KParams {
   int32_t drain_cap;
   int32_t pend_cap;
   gs_probe *pend;
-  int32_t *pend_flag;
   int32_t *claims;
   int32_t job_cap;
-  int32_t fifo_cap;
-  int32_t *fifo;
+  int32_t pad;
   int32_t *plan_io;
   int32_t *events;
   int64_t events_cap;
@@ -107,13 +121,35 @@ struct KParams {
 };
 
 struct SLed {
-  long long free_mem, in_use_warps, version, held_mem, held_warps;
+  long long free_mem, in_use_warps, version, held_mem, held_warps, grow_epoch;
   int rr_cursor, dirty;
+};
+
+struct Smem {
+  SLed led[GS_MAX_DEVICES];
+  // Σ over SMs of the positive residual (tbs, warps, regs, smem) per device:
+  // an O(1) upper bound on the blocks a shape can still place there.
+  // Maintained exactly while every SM's usage is within its limits
+  // (agg_ok); recomputed at every launch.
+  long long agg[GS_MAX_DEVICES][4];
+  int agg_ok[GS_MAX_DEVICES];
+  gs_probe cbuf[32];
+  gs_probe cur;
+  SchedState st;
+  Cmd cmd;
 };
 
 struct Shape {
   long long mem, T, wpb, rpb, spb, tw;
+  float iw, ir, is;  // reciprocals for the exact 32-bit division fast path
+  bool fast;         // per-block amounts in [0, 2^22)
 };
+
+struct Dec {
+  int outcome, dev;
+};
+
+constexpr long long kFastLim = 1LL << 22;
 
 __device__ __forceinline__ Shape shape_of(const gs_probe &p) {
   Shape s;
@@ -123,71 +159,94 @@ __device__ __forceinline__ Shape shape_of(const gs_probe &p) {
   s.rpb = (long long)p.regs_per_thread * (long long)p.threads_per_block;
   s.spb = p.smem_per_block;
   s.tw = p.total_warps;
+  s.fast = s.wpb >= 0 && s.wpb < kFastLim && s.rpb >= 0 && s.rpb < kFastLim && s.spb >= 0 && s.spb < kFastLim;
+  s.iw = s.wpb > 0 ? 1.0f / (float)s.wpb : 0.f;
+  s.ir = s.rpb > 0 ? 1.0f / (float)s.rpb : 0.f;
+  s.is = s.spb > 0 ? 1.0f / (float)s.spb : 0.f;
   return s;
+}
+
+// floor(n / d) for 0 <= n < 2^22, 1 <= d < 2^22: float estimate (error < 1)
+// corrected by one integer step each way — exact, ~8 instructions instead of
+// an emulated 64-bit division.
+__device__ __forceinline__ int fdiv(int n, int d, float inv) {
+  int q = __float2int_rz(__int2float_rn(n) * inv);
+  if (q * d > n) --q;
+  else if ((q + 1) * d <= n) ++q;
+  return q;
 }
 
 __device__ __forceinline__ long long warp_sum64(long long v) {
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
   return v;
 }
 __device__ __forceinline__ long long warp_min64(long long v) {
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v = min(v, (long long)__shfl_xor_sync(0xffffffffu, v, o));
+  for (int o = 16; o > 0; o >>= 1) v = min(v, (long long)__shfl_xor_sync(kFull, v, o));
   return v;
 }
-__device__ __forceinline__ int warp_max32(int v) { return __reduce_max_sync(0xffffffffu, v); }
 
-// Kernel-wide shared state (static part).
-struct SmemStatic {
-  SLed led[GS_MAX_DEVICES];
-  SchedState st;
-  Cmd cmd;
-  int feas[GS_MAX_DEVICES];
-  int chosen;
-  int outcome;
-  int cursor_out;
-  int chk;
-  long long scratch64;
-};
+__device__ __forceinline__ unsigned all_mask(int n) { return n >= 32 ? kFull : ((1u << n) - 1u); }
 
-__device__ __forceinline__ int *arr_warps(int *dyn, const KDev &D) { return dyn + D.smem_off; }
-__device__ __forceinline__ int *arr_tbs(int *dyn, const KDev &D) { return dyn + D.smem_off + D.arr_pad; }
-__device__ __forceinline__ int *arr_regs(int *dyn, const KDev &D) { return dyn + D.smem_off + 2 * D.arr_pad; }
-__device__ __forceinline__ int *arr_smem(int *dyn, const KDev &D) { return dyn + D.smem_off + 3 * D.arr_pad; }
+// staged per-SM arrays: 0 warps, 1 tbs, 2 regs, 3 smem (ledger order)
+__device__ __forceinline__ int *arr(int *dyn, const KDev &D, int which) {
+  return dyn + D.smem_off + kLedHdrWords + which * D.arr_pad;
+}
 
-// Per-SM residual capacity for one more block of this shape, clamped to T.
-// Mirrors _sm_admits (device_model.py:105-118) in closed form.
+__device__ __forceinline__ int32_t *res_row(const KDev &D, int h) { return D.res + (size_t)h * D.stride; }
+
+// Per-SM residual capacity for more blocks of this shape, clamped to T.
+// _sm_admits (device_model.py:105-118) in closed form.
 __device__ __forceinline__ int sm_cap(const KDev &D, int *dyn, int s, const Shape &sh) {
-  const int *w = arr_warps(dyn, D), *t = arr_tbs(dyn, D), *r = arr_regs(dyn, D), *m = arr_smem(dyn, D);
-  long long c = D.spec.max_tbs_per_sm - (long long)t[s];
+  const int w = arr(dyn, D, 0)[s], t = arr(dyn, D, 1)[s], r = arr(dyn, D, 2)[s], m = arr(dyn, D, 3)[s];
+  if (D.fast && sh.fast && (w | t | r | m) >= 0) {
+    // all residuals are below 2^22 here (spec < 2^22, usage >= 0)
+    int c = (int)D.spec.max_tbs_per_sm - t;
+    if (sh.wpb > 0) {
+      const int num = (int)D.spec.max_warps_per_sm - w;
+      c = min(c, num < 0 ? -1 : fdiv(num, (int)sh.wpb, sh.iw));
+    } else if (w > (int)D.spec.max_warps_per_sm) {
+      c = 0;
+    }
+    if (sh.rpb > 0) {
+      const int num = (int)D.spec.regs_per_sm - r;
+      c = min(c, num < 0 ? -1 : fdiv(num, (int)sh.rpb, sh.ir));
+    }
+    if (sh.spb > 0) {
+      const int num = (int)D.spec.smem_per_sm_bytes - m;
+      c = min(c, num < 0 ? -1 : fdiv(num, (int)sh.spb, sh.is));
+    }
+    c = max(c, 0);
+    return (long long)c > sh.T ? (int)sh.T : c;
+  }
+  long long c = D.spec.max_tbs_per_sm - (long long)t;
   if (sh.wpb > 0) {
-    long long num = D.spec.max_warps_per_sm - (long long)w[s];
+    long long num = D.spec.max_warps_per_sm - (long long)w;
     c = min(c, num < 0 ? -1LL : num / sh.wpb);
-  } else if ((long long)w[s] > D.spec.max_warps_per_sm) {
+  } else if ((long long)w > D.spec.max_warps_per_sm) {
     c = 0;
   }
-  if (sh.rpb != 0) {
-    long long num = D.spec.regs_per_sm - (long long)r[s];
-    c = min(c, num < 0 ? -1LL : (sh.rpb > 0 ? num / sh.rpb : c));
+  if (sh.rpb > 0) {
+    long long num = D.spec.regs_per_sm - (long long)r;
+    c = min(c, num < 0 ? -1LL : num / sh.rpb);
   }
-  if (sh.spb != 0) {
-    long long num = D.spec.smem_per_sm_bytes - (long long)m[s];
-    c = min(c, num < 0 ? -1LL : (sh.spb > 0 ? num / sh.spb : c));
+  if (sh.spb > 0) {
+    long long num = D.spec.smem_per_sm_bytes - (long long)m;
+    c = min(c, num < 0 ? -1LL : num / sh.spb);
   }
   if (c < 0) c = 0;
   if (c > sh.T) c = sh.T;
   return (int)c;
 }
 
-// Σ cap over the device's SMs (one warp).
 __device__ __forceinline__ long long warp_total_cap(const KDev &D, int *dyn, const Shape &sh, int lane) {
   long long tot = 0;
   for (int s = lane; s < D.n_sm; s += 32) tot += sm_cap(D, dyn, s, sh);
   return warp_sum64(tot);
 }
 
-// occupancy_limit_per_sm (device_model.py:48-58) × sm_count.
+// occupancy_limit_per_sm (device_model.py:48-58) x sm_count.
 __device__ __forceinline__ long long empty_capacity_blocks(const gs_spec &S, const Shape &sh) {
   long long lim = S.max_tbs_per_sm;
   if (sh.wpb > 0) lim = min(lim, S.max_warps_per_sm / sh.wpb);
@@ -197,9 +256,7 @@ __device__ __forceinline__ long long empty_capacity_blocks(const gs_spec &S, con
   return lim * S.sm_count;
 }
 
-__device__ __forceinline__ int32_t *res_row(const KDev &D, int h) { return D.res + (size_t)h * D.stride; }
-
-// _entry (device_model.py:211-216): create an empty residency row on demand.
+// _entry (device_model.py:211-216), single thread.
 __device__ __forceinline__ gs_residency *entry(const KDev &D, int h) {
   gs_residency *row = reinterpret_cast<gs_residency *>(res_row(D, h));
   if (!row->present) {
@@ -214,12 +271,77 @@ __device__ __forceinline__ gs_residency *entry(const KDev &D, int h) {
   return row;
 }
 
-// Closed-form round-robin placement for one device, computed by one warp.
-// Writes blocks into P[0..n) and returns the final cursor (all lanes), or -1
-// when the blocks cannot fit (the reference's n-consecutive-misses None).
-// Equivalent to try_place_blocks (device_model.py:120-139); SURVEY.md App. A.
-__device__ int warp_plan(const KDev &D, int *dyn, const SLed &L, const Shape &sh, int *cap, int *P,
-                         int lane) {
+// ---- ledger staging -----------------------------------------------------
+
+__device__ __forceinline__ int dev_of_q(const KParams &p, int q) {
+  int d = 0;
+  while (d + 1 < p.n_dev && q >= (p.dev[d + 1].smem_off >> 2)) ++d;
+  return d;
+}
+
+// Copy every staged ledger block mapped->smem (in) or smem->mapped (out,
+// dirty devices only) with 16-byte accesses, 8 in flight per lane.
+__device__ void stage(const KParams &p, int *dyn, const Smem &S, bool in, int lane) {
+  int4 *sm4 = reinterpret_cast<int4 *>(dyn);
+  for (int base = 0; base < p.stage_q; base += 32 * 8) {
+    int4 r[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int q = base + k * 32 + lane;
+      if (q < p.stage_q) {
+        const int d = dev_of_q(p, q);
+        int4 *g = reinterpret_cast<int4 *>(p.dev[d].led) + (q - (p.dev[d].smem_off >> 2));
+        if (in) r[k] = *g;
+        else if (S.led[d].dirty) *g = sm4[q];
+      }
+    }
+    if (in) {
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const int q = base + k * 32 + lane;
+        if (q < p.stage_q) sm4[q] = r[k];
+      }
+    }
+  }
+}
+
+__device__ void led_from_stage(const KParams &p, int *dyn, Smem &S, int lane) {
+  if (lane < p.n_dev) {
+    const gs_ledger *g = reinterpret_cast<const gs_ledger *>(dyn + p.dev[lane].smem_off);
+    SLed &L = S.led[lane];
+    L.free_mem = g->free_mem;
+    L.in_use_warps = g->in_use_warps;
+    L.version = g->version;
+    L.held_mem = g->held_mem;
+    L.held_warps = g->held_warps;
+    L.grow_epoch = g->grow_epoch;
+    L.rr_cursor = g->rr_cursor;
+    L.dirty = 0;
+  }
+  __syncwarp();
+}
+
+__device__ void led_to_stage(const KParams &p, int *dyn, Smem &S, int lane) {
+  if (lane < p.n_dev && S.led[lane].dirty) {
+    gs_ledger *g = reinterpret_cast<gs_ledger *>(dyn + p.dev[lane].smem_off);
+    const SLed &L = S.led[lane];
+    g->free_mem = L.free_mem;
+    g->in_use_warps = L.in_use_warps;
+    g->version = L.version;
+    g->held_mem = L.held_mem;
+    g->held_warps = L.held_warps;
+    g->grow_epoch = L.grow_epoch;
+    g->rr_cursor = L.rr_cursor;
+  }
+  __syncwarp();
+}
+
+// ---- placement plan / commit / release (one warp) ------------------------
+
+// Closed-form round-robin placement == try_place_blocks
+// (device_model.py:120-139).  Writes P[0..n) and returns the final cursor,
+// or -1 when the blocks cannot fit (the reference's None).
+__device__ int warp_plan(const KDev &D, int *dyn, const SLed &L, const Shape &sh, int *cap, int *P, int lane) {
   const int n = D.n_sm;
   long long tot = 0;
   int mx = 0;
@@ -230,7 +352,7 @@ __device__ int warp_plan(const KDev &D, int *dyn, const SLed &L, const Shape &sh
     mx = max(mx, c);
   }
   tot = warp_sum64(tot);
-  mx = warp_max32(mx);
+  mx = __reduce_max_sync(kFull, mx);
   __syncwarp();
   if (tot < sh.T) return -1;
   int c0 = L.rr_cursor % n;
@@ -240,10 +362,10 @@ __device__ int warp_plan(const KDev &D, int *dyn, const SLed &L, const Shape &sh
     __syncwarp();
     return c0;
   }
-  // largest k in [0, mx] with S(k) = Σ min(cap, k) <= T  (full rounds)
+  // largest k in [0, mx] with S(k) = sum min(cap, k) <= T  (full rounds)
   int lo = 0, hi = mx;
   while (lo < hi) {
-    int mid = (lo + hi + 1) >> 1;
+    const int mid = (lo + hi + 1) >> 1;
     long long sk = 0;
     for (int s = lane; s < n; s += 32) sk += min(cap[s], mid);
     sk = warp_sum64(sk);
@@ -252,96 +374,217 @@ __device__ int warp_plan(const KDev &D, int *dyn, const SLed &L, const Shape &sh
   const int k = lo;
   long long sk = 0;
   for (int s = lane; s < n; s += 32) {
-    int v = min(cap[s], k);
+    const int v = min(cap[s], k);
     P[s] = v;
     sk += v;
   }
   sk = warp_sum64(sk);
   __syncwarp();
   const long long rem = sh.T - sk;
-  // walk the SMs in visit order from the cursor, 32 at a time
   int last = -1;
   long long run = 0;
   const unsigned lt = (1u << lane) - 1u;
   for (int base = 0; base < n; base += 32) {
-    int p = base + lane;
-    int s = p < n ? (c0 + p) % n : 0;
+    const int pos = base + lane;
+    const int s = pos < n ? (c0 + pos) % n : 0;
     bool q = false;
-    if (p < n) q = rem > 0 ? (cap[s] > k) : (cap[s] >= k);
-    unsigned b = __ballot_sync(0xffffffffu, q);
+    if (pos < n) q = rem > 0 ? (cap[s] > k) : (cap[s] >= k);
+    const unsigned b = __ballot_sync(kFull, q);
     if (rem > 0) {
-      long long rank = run + __popc(b & lt);
+      const long long rank = run + __popc(b & lt);
       if (q && rank < rem) {
         P[s] = k + 1;
         if (rank == rem - 1) last = s;
       }
       run += __popc(b);
+      if (run >= rem) break;
     } else if (b) {
-      int lp = base + 31 - __clz(b);
-      last = (c0 + lp) % n;
+      last = (c0 + base + 31 - __clz(b)) % n;
     }
   }
-  last = __reduce_max_sync(0xffffffffu, last);
+  last = __reduce_max_sync(kFull, last);
   __syncwarp();
   return (last + 1) % n;
 }
 
-// commit_placement (device_model.py:141-161), one warp.
-__device__ void warp_commit(const KDev &D, int *dyn, SLed &L, int h, const Shape &sh, const int *P,
-                            int cursor, int lane) {
-  gs_residency *row = reinterpret_cast<gs_residency *>(res_row(D, h));
-  if (lane == 0) entry(D, h);
-  __syncwarp();
+// commit_placement's SM-array and block-row part (device_model.py:141-161).
+// Also records Σ blocks in the row (for O(1) aggregate maintenance).
+__device__ void warp_commit_blocks(const KDev &D, int *dyn, SLed &L, int h, const Shape &sh, const int *P,
+                                   int cursor, int lane) {
   int32_t *blocks = res_row(D, h) + kRowHdrWords;
-  int *w = arr_warps(dyn, D), *t = arr_tbs(dyn, D), *r = arr_regs(dyn, D), *m = arr_smem(dyn, D);
+  int *w = arr(dyn, D, 0), *t = arr(dyn, D, 1), *r = arr(dyn, D, 2), *m = arr(dyn, D, 3);
+  bool neg = false;
+  int tot = 0;
   for (int s = lane; s < D.n_sm; s += 32) {
-    int c = P[s];
+    const int c = P[s];
     blocks[s] = c;
+    tot += c;
     if (c) {
+      neg |= c < 0;
       t[s] += c;
       w[s] += (int)(c * sh.wpb);
       r[s] += (int)(c * sh.rpb);
       m[s] += (int)(c * sh.spb);
     }
   }
+  neg = __any_sync(kFull, neg);
+  tot = __reduce_add_sync(kFull, tot);
   if (lane == 0) {
     L.rr_cursor = cursor;
-    row->has_blocks = 1;
-    row->regs_per_block = sh.rpb;
-    row->smem_per_block = sh.spb;
-    row->warps_per_block = (int32_t)sh.wpb;
     L.version += 1;
     L.dirty = 1;
+    if (neg) L.grow_epoch += 1;
+    reinterpret_cast<gs_residency *>(res_row(D, h))->thread_blocks = tot;
   }
   __syncwarp();
 }
 
-// reserve + assign + add_warps for an admitted task (single thread).
-__device__ void admit_accounting(const KDev &D, SLed &L, int h, const Shape &sh) {
-  L.free_mem -= sh.mem;  // reserve_memory
-  L.version += 1;
-  gs_residency *row = entry(D, h);  // assign_memory
-  row->mem_bytes += sh.mem;
-  L.held_mem += sh.mem;
-  L.version += 1;
-  row->warps += sh.tw;  // add_warps
-  L.in_use_warps += sh.tw;
-  L.held_warps += sh.tw;
-  L.version += 1;
-  L.dirty = 1;
+// commit_placement through the test API: _entry + blocks + header fields.
+__device__ void warp_commit(const KDev &D, int *dyn, SLed &L, int h, const Shape &sh, const int *P, int cursor,
+                            int lane) {
+  if (lane == 0) {
+    gs_residency *row = entry(D, h);
+    row->has_blocks = 1;
+    row->regs_per_block = sh.rpb;
+    row->smem_per_block = sh.spb;
+    row->warps_per_block = (int32_t)sh.wpb;
+  }
+  __syncwarp();
+  warp_commit_blocks(D, dyn, L, h, sh, P, cursor, lane);
 }
 
-__device__ __forceinline__ void fifo_push(const KParams &p, SchedState &st, int d, int h) {
-  if (!p.sweep) return;
-  int pos = st.fifo_tail % p.fifo_cap;
-  p.fifo[2 * pos] = d;
-  p.fifo[2 * pos + 1] = h;
-  st.fifo_tail++;
+// Residency data of a release, from HBM or from the sweep's smem cache.
+struct RelRow {
+  long long mem, warps, rpb, spb;
+  int present, has_blocks, wpb, T;
+};
+
+// Ledger side of release_task (device_model.py:192-209); c[k] holds the
+// blocks of SMs lane + 32k (k < 8), SMs >= 256 are re-read from `rowp`.
+__device__ void apply_release(const KDev &D, int *dyn, Smem &S, int d, const RelRow &rr, const int *c,
+                              const int32_t *rowp, int lane) {
+  SLed &L = S.led[d];
+  const int n = D.n_sm;
+  if (rr.has_blocks) {
+    int *w = arr(dyn, D, 0), *t = arr(dyn, D, 1), *r = arr(dyn, D, 2), *m = arr(dyn, D, 3);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int s = lane + 32 * k;
+      if (s < n && c[k]) {
+        t[s] -= c[k];
+        w[s] -= (int)((long long)c[k] * rr.wpb);
+        r[s] -= (int)(c[k] * rr.rpb);
+        m[s] -= (int)(c[k] * rr.spb);
+      }
+    }
+    for (int s = lane + 256; s < n; s += 32) {  // devices with > 256 SMs
+      const int cc = rowp[kRowHdrWords + s];
+      if (cc) {
+        t[s] -= cc;
+        w[s] -= (int)((long long)cc * rr.wpb);
+        r[s] -= (int)(cc * rr.rpb);
+        m[s] -= (int)(cc * rr.spb);
+      }
+    }
+  }
+  __syncwarp();
+  if (lane == 0) {
+    L.free_mem += rr.mem;
+    L.in_use_warps -= rr.warps;
+    L.held_mem -= rr.mem;
+    L.held_warps -= rr.warps;
+    L.version += 1;
+    L.grow_epoch += 1;
+    L.dirty = 1;
+    if (rr.has_blocks && S.agg_ok[d]) {
+      if (rr.wpb >= 0 && rr.rpb >= 0 && rr.spb >= 0) {
+        S.agg[d][0] += rr.T;
+        S.agg[d][1] += (long long)rr.T * rr.wpb;
+        S.agg[d][2] += (long long)rr.T * rr.rpb;
+        S.agg[d][3] += (long long)rr.T * rr.spb;
+      } else {
+        S.agg_ok[d] = 0;
+      }
+    }
+    reinterpret_cast<gs_residency *>(const_cast<int32_t *>(rowp))->present = 0;
+  }
+  __syncwarp();
 }
 
-__device__ __forceinline__ void log_event(const KParams &p, SchedState &st, int kind, int h, int d) {
+// release_task (device_model.py:192-209), one warp, one load round trip.
+__device__ int warp_release(const KDev &D, int *dyn, Smem &S, int d, int h, long long *freed, int lane) {
+  const int32_t *rowp = res_row(D, h);
+  const int hw = lane < kRowHdrWords ? rowp[lane] : 0;
+  int c[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const int s = lane + 32 * k;
+    c[k] = s < D.n_sm ? rowp[kRowHdrWords + s] : 0;
+  }
+  auto word = [&](int i) { return __shfl_sync(kFull, hw, i); };
+  auto dword = [&](int i) {
+    return (long long)(((unsigned long long)(unsigned)word(i + 1) << 32) | (unsigned)word(i));
+  };
+  RelRow rr;
+  rr.present = word(8);
+  rr.mem = dword(0);
+  rr.warps = dword(2);
+  rr.rpb = dword(4);
+  rr.spb = dword(6);
+  rr.has_blocks = word(9);
+  rr.wpb = word(10);
+  rr.T = word(11);
+  if (!rr.present) return GS_ERR_CONTRACT;
+  apply_release(D, dyn, S, d, rr, c, rowp, lane);
+  *freed = rr.mem;
+  return GS_OK;
+}
+
+// Σ positive residual per dimension for device d (kernel start).
+__device__ void compute_agg(const KParams &p, int *dyn, Smem &S, int d, int lane) {
+  const KDev &D = p.dev[d];
+  long long a0 = 0, a1 = 0, a2 = 0, a3 = 0;
+  bool bad = false;
+  for (int s = lane; s < D.n_sm; s += 32) {
+    const long long w = arr(dyn, D, 0)[s], t = arr(dyn, D, 1)[s], r = arr(dyn, D, 2)[s], m = arr(dyn, D, 3)[s];
+    bad |= t > D.spec.max_tbs_per_sm || w > D.spec.max_warps_per_sm || r > D.spec.regs_per_sm ||
+           m > D.spec.smem_per_sm_bytes;
+    a0 += max(0LL, D.spec.max_tbs_per_sm - t);
+    a1 += max(0LL, D.spec.max_warps_per_sm - w);
+    a2 += max(0LL, D.spec.regs_per_sm - r);
+    a3 += max(0LL, D.spec.smem_per_sm_bytes - m);
+  }
+  a0 = warp_sum64(a0);
+  a1 = warp_sum64(a1);
+  a2 = warp_sum64(a2);
+  a3 = warp_sum64(a3);
+  bad = __any_sync(kFull, bad);
+  if (lane == 0) {
+    S.agg[d][0] = a0;
+    S.agg[d][1] = a1;
+    S.agg[d][2] = a2;
+    S.agg[d][3] = a3;
+    S.agg_ok[d] = !bad;
+  }
+  __syncwarp();
+}
+
+// O(1) necessary condition for T blocks of shape sh on device d:
+// floor(A / x) >= T  <=>  A >= T * x  (no division).
+__device__ __forceinline__ bool agg_admits(const Smem &S, int d, const Shape &sh) {
+  if (!S.agg_ok[d] || sh.T <= 0) return true;
+  if (S.agg[d][0] < sh.T) return false;
+  if (sh.wpb > 0 && S.agg[d][1] < sh.T * sh.wpb) return false;
+  if (sh.rpb > 0 && S.agg[d][2] < sh.T * sh.rpb) return false;
+  if (sh.spb > 0 && S.agg[d][3] < sh.T * sh.spb) return false;
+  return true;
+}
+
+// ---- decisions -------------------------------------------------------------
+
+__device__ __forceinline__ void log_event(const KParams &p, Smem &S, int kind, int h, int d) {
   if (!p.events) return;
-  long long i = st.n_events++;
+  const long long i = S.st.n_events++;
   if (i < p.events_cap) {
     p.events[3 * i] = kind;
     p.events[3 * i + 1] = h;
@@ -349,121 +592,208 @@ __device__ __forceinline__ void log_event(const KParams &p, SchedState &st, int 
   }
 }
 
-// One admission attempt (Scheduler._try, schedulers.py:127-135).  Called by
-// all threads; returns outcome / device in S.outcome / S.chosen.
-__device__ void decide(const KParams &p, SmemStatic &S, int *dyn, int *scratch, const gs_probe &pr,
-                       int h, int job) {
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int n_dev = p.n_dev;
-  if (p.policy == GS_POLICY_MGB_WARPS) {
-    // _try_mgb_warps (schedulers.py:155-171)
-    if (warp == 0) {
-      const Shape sh = shape_of(pr);
-      bool ok = lane < n_dev && S.led[lane].free_mem >= sh.mem;
-      unsigned b = __ballot_sync(0xffffffffu, ok);
-      if (b == 0) {
-        // _impossible_everywhere(check_compute=False) (schedulers.py:191-199)
-        bool possible = lane < n_dev && !(sh.mem > p.dev[lane].spec.mem_bytes);
-        unsigned pb = __ballot_sync(0xffffffffu, possible);
-        if (lane == 0) {
-          S.outcome = pb ? GS_DEFER : GS_REJECTED;
-          S.chosen = -1;
-        }
-      } else {
-        long long key = ok ? S.led[lane].in_use_warps : LLONG_MAX;
-        long long m = warp_min64(key);
-        unsigned cand = __ballot_sync(0xffffffffu, ok && key == m);
-        int d = __ffs(cand) - 1;
-        if (lane == 0) {
-          admit_accounting(p.dev[d], S.led[d], h, sh);
-          S.outcome = GS_ASSIGN;
-          S.chosen = d;
-        }
-      }
-    }
-    __syncthreads();
+// Sweep mode: the resident FIFO lives in shared memory together with each
+// resident task's residency data, so releasing the oldest task never waits
+// on HBM.  Slot: [dev, handle, has_blocks, wpb, T, -, mem, warps, rpb, spb
+// (int64 each)] + blocks[max_sm_pad].
+constexpr int kSlotHdr = 14;
+
+__device__ void fifo_push_slot(const KParams &p, Smem &S, int *dyn, int d, int h, const Shape &sh, long long mem,
+                               long long warps, bool blocks, const int *P, int lane) {
+  if (S.st.fifo_tail - S.st.fifo_head >= p.fifo_cap) {
+    if (lane == 0) S.st.error = GS_ERR_NOMEM;
+    __syncwarp();
     return;
   }
-  if (p.policy == GS_POLICY_MGB_SM) {
-    // _try_mgb_sm (schedulers.py:137-153): devices in index order; score
-    // all devices in parallel (one warp each), commit on the first feasible.
+  int *slot = dyn + p.fifo_off + (S.st.fifo_tail % p.fifo_cap) * p.fifo_stride;
+  if (blocks)
+    for (int s = lane; s < p.dev[d].n_sm; s += 32) slot[kSlotHdr + s] = P[s];
+  if (lane == 0) {
+    slot[0] = d;
+    slot[1] = h;
+    slot[2] = blocks ? 1 : 0;
+    slot[3] = (int)sh.wpb;
+    slot[4] = (int)sh.T;
+    long long *q = reinterpret_cast<long long *>(slot + 6);
+    q[0] = mem;
+    q[1] = warps;
+    q[2] = blocks ? sh.rpb : 0;
+    q[3] = blocks ? sh.spb : 0;
+    S.st.fifo_tail++;
+  }
+  __syncwarp();
+}
+
+__device__ void fifo_pop_release(const KParams &p, Smem &S, int *dyn, int lane) {
+  const int *slot = dyn + p.fifo_off + (S.st.fifo_head % p.fifo_cap) * p.fifo_stride;
+  const int d = slot[0], h = slot[1];
+  const KDev &D = p.dev[d];
+  RelRow rr;
+  rr.present = 1;
+  rr.has_blocks = slot[2];
+  rr.wpb = slot[3];
+  rr.T = slot[4];
+  const long long *q = reinterpret_cast<const long long *>(slot + 6);
+  rr.mem = q[0];
+  rr.warps = q[1];
+  rr.rpb = q[2];
+  rr.spb = q[3];
+  int c[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const int s = lane + 32 * k;
+    c[k] = (rr.has_blocks && s < D.n_sm) ? slot[kSlotHdr + s] : 0;
+  }
+  apply_release(D, dyn, S, d, rr, c, res_row(D, h), lane);
+  if (lane == 0) S.st.fifo_head++;
+  __syncwarp();
+}
+
+// One admission attempt (Scheduler._try, schedulers.py:127-135) over the
+// devices in `mask`.  Uniform result across the warp.
+__device__ Dec decide(const KParams &p, Smem &S, int *dyn, const gs_probe &pr, unsigned mask, bool allow_reject,
+                      int lane) {
+  const int n_dev = p.n_dev;
+  Dec out{GS_DEFER, -1};
+  if (p.policy == GS_POLICY_MGB_WARPS || p.policy == GS_POLICY_MGB_SM) {
     const Shape sh = shape_of(pr);
-    for (int d = warp; d < n_dev; d += kWarps) {
-      int f = 0;
-      if (S.led[d].free_mem >= sh.mem) {
-        long long tot = warp_total_cap(p.dev[d], dyn, sh, lane);
-        f = tot >= sh.T;
-      }
-      if (lane == 0) S.feas[d] = f;
+    const int h = pr.handle;
+    const bool fresh = (pr.level & GS_PROBE_FRESH) && (allow_reject || p.sweep);
+    // prefetch the residency row this decision may accumulate into
+    int r_present = 0;
+    long long r_mem = 0, r_warps = 0;
+    if (!fresh && lane < n_dev && ((mask >> lane) & 1)) {
+      const gs_residency *row = reinterpret_cast<const gs_residency *>(res_row(p.dev[lane], h));
+      r_present = row->present;
+      r_mem = row->mem_bytes;
+      r_warps = row->warps;
     }
-    __syncthreads();
-    if (warp == 0) {
-      bool f = lane < n_dev && S.feas[lane];
-      unsigned b = __ballot_sync(0xffffffffu, f);
-      if (b) {
-        int d = __ffs(b) - 1;
-        const KDev &D = p.dev[d];
-        int *cap = scratch;
-        int *P = scratch + p.max_sm_pad;
-        int cur = warp_plan(D, dyn, S.led[d], sh, cap, P, lane);
-        warp_commit(D, dyn, S.led[d], h, sh, P, cur, lane);
-        if (lane == 0) {
-          admit_accounting(D, S.led[d], h, sh);
-          S.outcome = GS_ASSIGN;
-          S.chosen = d;
+    int chosen = -1;
+    if (p.policy == GS_POLICY_MGB_WARPS) {
+      // _try_mgb_warps (schedulers.py:155-171): feasible = free_mem >= mem,
+      // choose min((in_use_warps, idx))
+      const bool ok = lane < n_dev && ((mask >> lane) & 1) && S.led[lane].free_mem >= sh.mem;
+      if (__ballot_sync(kFull, ok)) {
+        const long long key = ok ? S.led[lane].in_use_warps : LLONG_MAX;
+        const long long m = warp_min64(key);
+        chosen = __ffs(__ballot_sync(kFull, ok && key == m)) - 1;
+      }
+    } else {
+      // _try_mgb_sm (schedulers.py:137-153): first device in index order
+      // passing memory and per-SM placement.  Memory and the O(1)
+      // aggregate bound are checked for all devices at once (lane d), the
+      // exact per-SM count only for devices that pass both.
+      const bool cand = lane < n_dev && ((mask >> lane) & 1) && S.led[lane].free_mem >= sh.mem &&
+                        agg_admits(S, lane, sh);
+      for (unsigned m = __ballot_sync(kFull, cand); m; m &= m - 1) {
+        const int d = __ffs(m) - 1;
+        if (warp_total_cap(p.dev[d], dyn, sh, lane) >= sh.T) {
+          chosen = d;
+          break;
         }
-      } else {
-        // _impossible_everywhere(check_compute=True)
+      }
+    }
+    if (chosen < 0) {
+      if (allow_reject) {
+        // _impossible_everywhere (schedulers.py:191-199)
         bool possible = false;
         if (lane < n_dev) {
           const gs_spec &sp = p.dev[lane].spec;
-          possible = !(sh.mem > sp.mem_bytes) && !(empty_capacity_blocks(sp, sh) < sh.T);
+          possible = !(sh.mem > sp.mem_bytes);
+          if (p.policy == GS_POLICY_MGB_SM) possible = possible && !(empty_capacity_blocks(sp, sh) < sh.T);
         }
-        unsigned pb = __ballot_sync(0xffffffffu, possible);
-        if (lane == 0) {
-          S.outcome = pb ? GS_DEFER : GS_REJECTED;
-          S.chosen = -1;
-        }
+        if (!__ballot_sync(kFull, possible)) out.outcome = GS_REJECTED;
       }
+      return out;
     }
-    __syncthreads();
-    return;
+    const int present = __shfl_sync(kFull, r_present, chosen);
+    const long long pm = __shfl_sync(kFull, r_mem, chosen), pw = __shfl_sync(kFull, r_warps, chosen);
+    const KDev &D = p.dev[chosen];
+    SLed &L = S.led[chosen];
+    gs_residency *row = reinterpret_cast<gs_residency *>(res_row(D, h));
+    int *P = dyn + p.scratch_off + p.max_sm_pad;
+    const bool sm_policy = p.policy == GS_POLICY_MGB_SM;
+    if (sm_policy) {
+      int *cap = dyn + p.scratch_off;
+      const int cur = warp_plan(D, dyn, L, sh, cap, P, lane);
+      warp_commit_blocks(D, dyn, L, h, sh, P, cur, lane);  // commit_placement
+    }
+    const long long new_mem = (present ? pm : 0) + sh.mem, new_warps = (present ? pw : 0) + sh.tw;
+    if (lane == 0) {
+      // commit header fields (mgb-sm), reserve_memory, assign_memory, add_warps
+      row->mem_bytes = new_mem;
+      row->warps = new_warps;
+      if (sm_policy) {
+        row->has_blocks = 1;
+        row->regs_per_block = sh.rpb;
+        row->smem_per_block = sh.spb;
+        row->warps_per_block = (int32_t)sh.wpb;
+        if (S.agg_ok[chosen]) {
+          if (sh.wpb >= 0 && sh.rpb >= 0 && sh.spb >= 0) {
+            S.agg[chosen][0] -= sh.T;
+            S.agg[chosen][1] -= sh.T * sh.wpb;
+            S.agg[chosen][2] -= sh.T * sh.rpb;
+            S.agg[chosen][3] -= sh.T * sh.spb;
+          } else {
+            S.agg_ok[chosen] = 0;
+          }
+        }
+      } else if (!present) {
+        row->has_blocks = 0;
+        row->regs_per_block = 0;
+        row->smem_per_block = 0;
+        row->warps_per_block = 0;
+        row->thread_blocks = 0;
+      }
+      row->present = 1;
+      L.free_mem -= sh.mem;
+      L.held_mem += sh.mem;
+      L.in_use_warps += sh.tw;
+      L.held_warps += sh.tw;
+      L.version += 3;
+      L.dirty = 1;
+    }
+    __syncwarp();
+    if (p.sweep) fifo_push_slot(p, S, dyn, chosen, h, sh, new_mem, new_warps, sm_policy, P, lane);
+    out.outcome = GS_ASSIGN;
+    out.dev = chosen;
+    return out;
   }
-  if (tid == 0) {
+  int oc = GS_DEFER, dv = -1;
+  if (lane == 0) {
     if (p.policy == GS_POLICY_SA) {
       // _try_sa (schedulers.py:173-178)
-      S.outcome = GS_DEFER;
-      S.chosen = -1;
       for (int d = 0; d < n_dev; ++d) {
         if (S.st.sa_owner[d] < 0) {
-          S.st.sa_owner[d] = job;
-          S.outcome = GS_ASSIGN;
-          S.chosen = d;
+          S.st.sa_owner[d] = pr.job;
+          oc = GS_ASSIGN;
+          dv = d;
           break;
         }
       }
     } else {
       // _try_cg (schedulers.py:180-189)
-      S.outcome = GS_DEFER;
-      S.chosen = -1;
       for (int step = 0; step < n_dev; ++step) {
-        int d = (S.st.cg_cursor + step) % n_dev;
+        const int d = (S.st.cg_cursor + step) % n_dev;
         if (S.st.cg_counts[d] < p.cg_ratio) {
           S.st.cg_counts[d] += 1;
-          if (job >= 0 && job < p.job_cap) p.claims[job] = d;
+          if (pr.job >= 0 && pr.job < p.job_cap) p.claims[pr.job] = d;
           S.st.cg_cursor = (d + 1) % n_dev;
-          S.outcome = GS_ASSIGN;
-          S.chosen = d;
+          oc = GS_ASSIGN;
+          dv = d;
           break;
         }
       }
     }
   }
-  __syncthreads();
+  out.outcome = __shfl_sync(kFull, oc, 0);
+  out.dev = __shfl_sync(kFull, dv, 0);
+  __syncwarp();
+  return out;
 }
 
-__device__ __forceinline__ void fill_decision(gs_decision &o, const SmemStatic &S, int outcome, int d,
-                                              int pidx, int h) {
+__device__ __forceinline__ void fill_decision(gs_decision &o, const Smem &S, int outcome, int d, int pidx,
+                                              int h) {
   o.outcome = outcome;
   o.device = d;
   o.free_mem_after = d >= 0 ? S.led[d].free_mem : 0;
@@ -472,313 +802,247 @@ __device__ __forceinline__ void fill_decision(gs_decision &o, const SmemStatic &
   o.handle = h;
 }
 
-// Parallel feasibility prefilter for one pass (exact: see header).
-__device__ void drain_prefilter(const KParams &p, SmemStatic &S, int *dyn, int P) {
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  if (p.policy == GS_POLICY_MGB_WARPS) {
-    if (warp == 0) {
-      long long f = lane < p.n_dev ? S.led[lane].free_mem : LLONG_MIN;
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) f = max(f, (long long)__shfl_xor_sync(0xffffffffu, f, o));
-      if (lane == 0) S.scratch64 = f;
-    }
-    __syncthreads();
-    const long long maxfree = S.scratch64;
-    for (int i = tid; i < P; i += kThreads) p.pend_flag[i] = p.pend[i].mem_bytes <= maxfree;
-  } else if (p.policy == GS_POLICY_MGB_SM) {
-    for (int i = warp; i < P; i += kWarps) {
-      const Shape sh = shape_of(p.pend[i]);
-      int ok = 0;
-      for (int d = 0; d < p.n_dev && !ok; ++d) {
-        if (S.led[d].free_mem < sh.mem) continue;
-        if (warp_total_cap(p.dev[d], dyn, sh, lane) >= sh.T) ok = 1;
-      }
-      if (lane == 0) p.pend_flag[i] = ok;
-    }
-  } else {
-    for (int i = tid; i < P; i += kThreads) p.pend_flag[i] = 1;
+// O(1) necessary condition for `pr` fitting one of the devices in `dirty`.
+__device__ __forceinline__ bool bound_feasible(const KParams &p, const Smem &S, const gs_probe &pr, unsigned dirty) {
+  const Shape sh = shape_of(pr);
+  for (unsigned m = dirty; m; m &= m - 1) {
+    const int d = __ffs(m) - 1;
+    if (S.led[d].free_mem < sh.mem) continue;
+    if (p.policy != GS_POLICY_MGB_SM || agg_admits(S, d, sh)) return true;
   }
-  __syncthreads();
+  return false;
+}
+
+__device__ __forceinline__ void record_admit(const KParams &p, Smem &S, bool write_out, int i, const gs_probe &pr,
+                                             Dec dc) {
+  if (write_out && i < p.drain_cap) fill_decision(p.drain_out[i], S, dc.outcome, dc.dev, i, pr.handle);
+  if (dc.outcome == GS_ASSIGN) log_event(p, S, 3, pr.handle, dc.dev);
 }
 
 // Scheduler.on_release (schedulers.py:97-113).
-__device__ void on_release(const KParams &p, SmemStatic &S, int *dyn, int *scratch, bool write_out) {
-  const int tid = threadIdx.x;
+__device__ void on_release(const KParams &p, Smem &S, int *dyn, bool write_out, int lane) {
   const int P = S.st.pend_count;
-  drain_prefilter(p, S, dyn, P);
-  int tried = 0, admitted = 0;
-  for (int i = 0; i < P; ++i) {
-    tried = i + 1;
-    int outcome, d;
-    const int h = p.pend[i].handle;
-    if (!p.pend_flag[i]) {
-      outcome = GS_DEFER;
-      d = -1;
-    } else {
-      decide(p, S, dyn, scratch, p.pend[i], h, p.pend[i].job);
-      outcome = S.outcome;
-      d = S.chosen;
-    }
-    if (tid == 0) {
-      if (write_out && i < p.drain_cap) fill_decision(p.drain_out[i], S, outcome, d, i, h);
-      if (outcome == GS_ASSIGN) {
-        fifo_push(p, S.st, d, h);
-        log_event(p, S.st, 3, h, d);
-      }
-    }
-    // pend_flag doubles as the "admitted" mark for compaction (2 = gone)
-    if (outcome == GS_ASSIGN) {
-      if (tid == 0) p.pend_flag[i] = 2;
-      admitted++;
-    } else if (!p.skip_ahead) {
+  const bool mgb = p.policy == GS_POLICY_MGB_SM || p.policy == GS_POLICY_MGB_WARPS;
+  const unsigned all = all_mask(p.n_dev);
+  unsigned dirty = all;
+  if (mgb) {
+    const bool g = lane < p.n_dev && S.led[lane].grow_epoch != S.st.seen_epoch[lane];
+    dirty = __ballot_sync(kFull, g);
+  }
+  const unsigned dmask = mgb ? dirty : all;
+  int w = 0, tried = 0, admitted = 0;
+  bool stop = false;
+  const unsigned lt = (1u << lane) - 1u;
+  for (int base = 0; base < P; base += 32) {
+    if (stop && w == base) {  // strict FIFO stopped and nothing moved: done
+      w = P;
       break;
     }
-    __syncthreads();
-  }
-  __syncthreads();
-  // stable in-place compaction of the survivors
-  __shared__ int wsum[kWarps];
-  __shared__ int base_out;
-  if (tid == 0) base_out = 0;
-  __syncthreads();
-  for (int base = 0; base < P; base += kThreads) {
-    int i = base + tid;
+    const int i = base + lane;
+    const bool valid = i < P;
+    const int cnt = min(32, P - base);
     gs_probe mine;
-    bool keep = false;
-    if (i < P) {
-      keep = !(i < tried && p.pend_flag[i] == 2);
-      if (keep) mine = p.pend[i];
+    if (valid) mine = p.pend[i];
+    unsigned adm = 0;
+    if (!stop) {
+      const bool flag = valid && (!mgb || (dirty && bound_feasible(p, S, mine, dirty)));
+      const unsigned fb = __ballot_sync(kFull, flag);
+      if (valid) S.cbuf[lane] = mine;
+      __syncwarp();
+      if (p.skip_ahead) {
+        if (write_out && valid && !flag && i < p.drain_cap)
+          fill_decision(p.drain_out[i], S, GS_DEFER, -1, i, mine.handle);
+        for (unsigned m = fb; m; m &= m - 1) {
+          const int j = __ffs(m) - 1;
+          const Dec dc = decide(p, S, dyn, S.cbuf[j], dmask, false, lane);
+          if (lane == 0) record_admit(p, S, write_out, base + j, S.cbuf[j], dc);
+          if (dc.outcome == GS_ASSIGN) adm |= 1u << j;
+          __syncwarp();
+        }
+        tried = base + cnt;
+      } else {
+        for (int j = 0; j < cnt; ++j) {
+          Dec dc{GS_DEFER, -1};
+          if ((fb >> j) & 1) dc = decide(p, S, dyn, S.cbuf[j], dmask, false, lane);
+          if (lane == 0) record_admit(p, S, write_out, base + j, S.cbuf[j], dc);
+          __syncwarp();
+          tried = base + j + 1;
+          if (dc.outcome == GS_ASSIGN) {
+            adm |= 1u << j;
+          } else {
+            stop = true;
+            break;
+          }
+        }
+      }
     }
-    unsigned b = __ballot_sync(0xffffffffu, keep);
-    int lane = tid & 31, warp = tid >> 5;
-    if (lane == 0) wsum[warp] = __popc(b);
-    __syncthreads();
-    int off = base_out;
-    for (int w = 0; w < warp; ++w) off += wsum[w];
-    off += __popc(b & ((1u << lane) - 1u));
-    __syncthreads();
-    if (keep) p.pend[off] = mine;
-    if (tid == kThreads - 1) {
-      int tot = 0;
-      for (int w = 0; w < kWarps; ++w) tot += wsum[w];
-      base_out += tot;
-    }
-    __syncthreads();
+    // in-place stable compaction of the survivors of this chunk
+    const bool keep = valid && !((adm >> lane) & 1);
+    const unsigned kb = __ballot_sync(kFull, keep);
+    if ((w != base || adm) && keep) p.pend[w + __popc(kb & lt)] = mine;
+    w += __popc(kb);
+    admitted += __popc(adm);
+    __syncwarp();
   }
-  if (tid == 0) {
-    S.st.pend_count = base_out;
+  if (lane == 0) {
+    S.st.pend_count = w;
     S.st.n_tried = tried;
     S.st.n_admitted = admitted;
   }
-  __syncthreads();
+  if (mgb && !stop && lane < p.n_dev) S.st.seen_epoch[lane] = S.led[lane].grow_epoch;
+  __syncwarp();
 }
 
-__device__ void submit(const KParams &p, SmemStatic &S, int *dyn, int *scratch, const gs_probe &pr,
-                       gs_decision *out) {
-  const int h = pr.handle;
-  decide(p, S, dyn, scratch, pr, h, pr.job);
-  if (threadIdx.x == 0) {
-    const int oc = S.outcome, d = S.chosen;
-    if (oc == GS_DEFER) {
-      int pc = S.st.pend_count;
-      if (pc < p.pend_cap) p.pend[pc] = pr;
-      S.st.pend_count = pc + 1;
-    }
-    if (oc == GS_ASSIGN) fifo_push(p, S.st, d, h);
-    log_event(p, S.st, oc == GS_ASSIGN ? 0 : (oc == GS_DEFER ? 1 : 2), h, d);
-    if (out) fill_decision(*out, S, oc, d, -1, h);
-  }
-  __syncthreads();
-}
-
-// release_task (device_model.py:192-209), one warp.
-__device__ int warp_release(const KDev &D, int *dyn, SLed &L, int h, long long *freed, int lane) {
-  gs_residency *row = reinterpret_cast<gs_residency *>(res_row(D, h));
-  int present = row->present;
-  if (!present) return GS_ERR_CONTRACT;
-  if (row->has_blocks) {
-    const int32_t *blocks = res_row(D, h) + kRowHdrWords;
-    int *w = arr_warps(dyn, D), *t = arr_tbs(dyn, D), *r = arr_regs(dyn, D), *m = arr_smem(dyn, D);
-    for (int s = lane; s < D.n_sm; s += 32) {
-      int c = blocks[s];
-      if (c) {
-        t[s] -= c;
-        w[s] -= (int)(c * (long long)row->warps_per_block);
-        r[s] -= (int)(c * row->regs_per_block);
-        m[s] -= (int)(c * row->smem_per_block);
-      }
-    }
-  }
+__device__ Dec submit(const KParams &p, Smem &S, int *dyn, const gs_probe &pr, gs_decision *out, int lane) {
+  const Dec dc = decide(p, S, dyn, pr, all_mask(p.n_dev), true, lane);
+  const int pc = S.st.pend_count;
+  if (dc.outcome == GS_DEFER && pc < p.pend_cap && lane < 16)
+    reinterpret_cast<int32_t *>(p.pend + pc)[lane] = reinterpret_cast<const int32_t *>(&pr)[lane];
   __syncwarp();
   if (lane == 0) {
-    L.free_mem += row->mem_bytes;
-    L.in_use_warps -= row->warps;
-    L.held_mem -= row->mem_bytes;
-    L.held_warps -= row->warps;
-    L.version += 1;
-    L.dirty = 1;
-    *freed = row->mem_bytes;
-    row->present = 0;
+    if (dc.outcome == GS_DEFER) S.st.pend_count = pc + 1;
+    log_event(p, S, dc.outcome == GS_ASSIGN ? 0 : (dc.outcome == GS_DEFER ? 1 : 2), pr.handle, dc.dev);
+    if (out) fill_decision(*out, S, dc.outcome, dc.dev, -1, pr.handle);
   }
   __syncwarp();
-  return GS_OK;
+  return dc;
 }
 
 __global__ void __launch_bounds__(kThreads, 1) gs_interp_kernel(KParams p) {
-  extern __shared__ int dyn[];
-  __shared__ SmemStatic S;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  int *scratch = dyn;  // per-warp scratch lives after the device arrays
-  {
-    int tot = 0;
-    for (int d = 0; d < p.n_dev; ++d) tot = max(tot, p.dev[d].smem_off + 4 * p.dev[d].arr_pad);
-    scratch = dyn + tot + warp * 2 * p.max_sm_pad;
-  }
-  // ---- stage ledgers + scheduler state into shared memory ----
-  for (int d = 0; d < p.n_dev; ++d) {
-    const KDev &D = p.dev[d];
-    const int32_t *src = reinterpret_cast<const int32_t *>(D.led + 1);
-    int *dst = dyn + D.smem_off;
-    for (int i = tid; i < 4 * D.arr_pad; i += kThreads) dst[i] = src[i];
-  }
-  if (tid < p.n_dev) {
-    const gs_ledger *g = p.dev[tid].led;
-    SLed &L = S.led[tid];
-    L.free_mem = g->free_mem;
-    L.in_use_warps = g->in_use_warps;
-    L.version = g->version;
-    L.held_mem = g->held_mem;
-    L.held_warps = g->held_warps;
-    L.rr_cursor = g->rr_cursor;
-    L.dirty = 0;
-  }
-  if (tid == 0) S.st = *p.st;
-  __syncthreads();
+  extern __shared__ __align__(16) int dyn[];
+  __shared__ Smem S;
+  const int lane = threadIdx.x;
 
-  for (int ci = 0; ci < p.n_cmds; ++ci) {
-    if (p.sweep) {
-      // placement sweep (BASELINE cfg 4): submit probe ci, then maybe
-      // release the oldest resident task and re-drive the FIFO.
-      const gs_probe pr = p.sweep_probes[ci];
-      submit(p, S, dyn, scratch, pr, nullptr);
+  stage(p, dyn, S, true, lane);
+  __syncwarp();
+  led_from_stage(p, dyn, S, lane);
+  {
+    const int nw = sizeof(SchedState) / 4;
+    for (int i = lane; i < nw; i += 32)
+      reinterpret_cast<int32_t *>(&S.st)[i] = reinterpret_cast<const int32_t *>(p.st)[i];
+  }
+  __syncwarp();
+  for (int d = 0; d < p.n_dev; ++d) compute_agg(p, dyn, S, d, lane);
+
+  if (p.sweep) {
+    // placement sweep (BASELINE cfg 4): submit probe i; then, if more than
+    // max_resident tasks are resident or requests are queued, release the
+    // oldest resident task and re-drive the FIFO.
+    const int32_t *src = reinterpret_cast<const int32_t *>(p.sweep_probes);
+    int nextw = (lane < 16 && p.n_cmds > 0) ? src[lane] : 0;
+    for (int ci = 0; ci < p.n_cmds; ++ci) {
+      if (lane < 16) reinterpret_cast<int32_t *>(&S.cur)[lane] = nextw;
+      __syncwarp();
+      if (lane < 16 && ci + 1 < p.n_cmds) nextw = src[16 * (ci + 1) + lane];  // prefetch next probe
+      submit(p, S, dyn, S.cur, nullptr, lane);
       const int resident = S.st.fifo_tail - S.st.fifo_head;
       if (resident > p.max_resident || S.st.pend_count > 0) {
-        if (resident > 0) {
-          const int pos = S.st.fifo_head % p.fifo_cap;
-          const int d = p.fifo[2 * pos], h = p.fifo[2 * pos + 1];
-          if (warp == 0) {
-            long long freed;
-            warp_release(p.dev[d], dyn, S.led[d], h, &freed, lane);
-          }
-          __syncthreads();
-          if (tid == 0) S.st.fifo_head++;
-          __syncthreads();
-        }
-        on_release(p, S, dyn, scratch, false);
+        if (resident > 0) fifo_pop_release(p, S, dyn, lane);
+        on_release(p, S, dyn, false, lane);
       }
-      continue;
+      if (S.st.error) break;
     }
-    // copy the command into shared memory (one PCIe/L2 read per word)
-    if (tid < (int)(sizeof(Cmd) / 4))
-      reinterpret_cast<int32_t *>(&S.cmd)[tid] = reinterpret_cast<const int32_t *>(p.cmds + ci)[tid];
-    __syncthreads();
-    const Cmd &c = S.cmd;
-    gs_decision *out = p.results + ci;
-    switch (c.op) {
-      case OP_SUBMIT:
-        submit(p, S, dyn, scratch, c.probe, out);
-        break;
-      case OP_ON_RELEASE:
-        on_release(p, S, dyn, scratch, true);
-        if (tid == 0) {
-          out->outcome = GS_OK;
-          out->free_mem_after = S.st.n_tried;
-          out->in_use_warps_after = S.st.n_admitted;
-        }
-        break;
-      case OP_JOB_ENDED:
-        // job_ended (schedulers.py:115-123)
-        if (tid == 0) {
-          for (int d = 0; d < p.n_dev; ++d)
-            if (S.st.sa_owner[d] == c.job) S.st.sa_owner[d] = -1;
-          if (p.policy == GS_POLICY_CG && c.job >= 0 && c.job < p.job_cap) {
-            int d = p.claims[c.job];
-            if (d >= 0) {
-              S.st.cg_counts[d] -= 1;
-              p.claims[c.job] = -1;
-            }
+  } else {
+    for (int ci = 0; ci < p.n_cmds; ++ci) {
+      if (lane < (int)(sizeof(Cmd) / 4))
+        reinterpret_cast<int32_t *>(&S.cmd)[lane] = reinterpret_cast<const int32_t *>(p.cmds + ci)[lane];
+      __syncwarp();
+      const Cmd &c = S.cmd;
+      gs_decision *out = p.results + ci;
+      switch (c.op) {
+        case OP_SUBMIT:
+          submit(p, S, dyn, c.probe, out, lane);
+          break;
+        case OP_ON_RELEASE:
+          on_release(p, S, dyn, true, lane);
+          if (lane == 0) {
+            out->outcome = GS_OK;
+            out->free_mem_after = S.st.n_tried;
+            out->in_use_warps_after = S.st.n_admitted;
           }
-          out->outcome = GS_OK;
-        }
-        break;
-      case OP_RELEASE:
-        if (warp == 0) {
+          break;
+        case OP_JOB_ENDED:
+          // job_ended (schedulers.py:115-123)
+          if (lane == 0) {
+            for (int d = 0; d < p.n_dev; ++d)
+              if (S.st.sa_owner[d] == c.job) S.st.sa_owner[d] = -1;
+            if (p.policy == GS_POLICY_CG && c.job >= 0 && c.job < p.job_cap) {
+              const int d = p.claims[c.job];
+              if (d >= 0) {
+                S.st.cg_counts[d] -= 1;
+                p.claims[c.job] = -1;
+              }
+            }
+            out->outcome = GS_OK;
+          }
+          break;
+        case OP_RELEASE: {
           long long freed = 0;
-          int rc = warp_release(p.dev[c.dev], dyn, S.led[c.dev], c.handle, &freed, lane);
+          const int rc = warp_release(p.dev[c.dev], dyn, S, c.dev, c.handle, &freed, lane);
           if (lane == 0) {
             out->outcome = rc;
             out->free_mem_after = freed;
           }
+          break;
         }
-        break;
-      case OP_RESERVE:
-      case OP_ALLOC_RAW:
-        if (tid == 0) {
-          SLed &L = S.led[c.dev];
-          if (c.a > L.free_mem) {
-            out->outcome = GS_INFEASIBLE;
-          } else {
-            L.free_mem -= c.a;
+        case OP_RESERVE:
+        case OP_ALLOC_RAW:
+          // reserve_memory (device_model.py:169-174) / allocate_raw (:185-190)
+          if (lane == 0) {
+            SLed &L = S.led[c.dev];
+            if (c.a > L.free_mem) {
+              out->outcome = GS_INFEASIBLE;
+            } else {
+              L.free_mem -= c.a;
+              L.version += 1;
+              L.dirty = 1;
+              if (c.a < 0) L.grow_epoch += 1;
+              if (c.op == OP_ALLOC_RAW) {
+                gs_residency *row = entry(p.dev[c.dev], c.handle);
+                row->mem_bytes += c.a;
+                L.held_mem += c.a;
+                L.version += 1;
+              }
+              out->outcome = GS_OK;
+            }
+          }
+          break;
+        case OP_ASSIGN:
+          if (lane == 0) {
+            SLed &L = S.led[c.dev];
+            gs_residency *row = entry(p.dev[c.dev], c.handle);
+            row->mem_bytes += c.a;
+            L.held_mem += c.a;
             L.version += 1;
             L.dirty = 1;
-            if (c.op == OP_ALLOC_RAW) {
-              gs_residency *row = entry(p.dev[c.dev], c.handle);
-              row->mem_bytes += c.a;
-              L.held_mem += c.a;
-              L.version += 1;
-            }
             out->outcome = GS_OK;
           }
-        }
-        break;
-      case OP_ASSIGN:
-        if (tid == 0) {
-          SLed &L = S.led[c.dev];
-          gs_residency *row = entry(p.dev[c.dev], c.handle);
-          row->mem_bytes += c.a;
-          L.held_mem += c.a;
-          L.version += 1;
-          L.dirty = 1;
-          out->outcome = GS_OK;
-        }
-        break;
-      case OP_ADD_WARPS:
-        if (tid == 0) {
-          SLed &L = S.led[c.dev];
-          gs_residency *row = entry(p.dev[c.dev], c.handle);
-          row->warps += c.a;
-          L.in_use_warps += c.a;
-          L.held_warps += c.a;
-          L.version += 1;
-          L.dirty = 1;
-          out->outcome = GS_OK;
-        }
-        break;
-      case OP_TRY_PLACE:
-        if (warp == 0) {
+          break;
+        case OP_ADD_WARPS:
+          if (lane == 0) {
+            SLed &L = S.led[c.dev];
+            gs_residency *row = entry(p.dev[c.dev], c.handle);
+            row->warps += c.a;
+            L.in_use_warps += c.a;
+            L.held_warps += c.a;
+            L.version += 1;
+            L.dirty = 1;
+            out->outcome = GS_OK;
+          }
+          break;
+        case OP_TRY_PLACE: {
           const Shape sh = shape_of(c.probe);
-          int *cap = scratch, *P = scratch + p.max_sm_pad;
-          int cur = warp_plan(p.dev[c.dev], dyn, S.led[c.dev], sh, cap, P, lane);
+          int *cap = dyn + p.scratch_off, *P = cap + p.max_sm_pad;
+          const int cur = warp_plan(p.dev[c.dev], dyn, S.led[c.dev], sh, cap, P, lane);
           for (int s = lane; s < p.dev[c.dev].n_sm; s += 32) p.plan_io[s] = cur >= 0 ? P[s] : 0;
           if (lane == 0) {
             out->outcome = cur >= 0 ? GS_OK : GS_INFEASIBLE;
             out->device = cur;
             out->free_mem_after = S.led[c.dev].version;
           }
+          break;
         }
-        break;
-      case OP_COMMIT:
-        if (warp == 0) {
+        case OP_COMMIT: {
           SLed &L = S.led[c.dev];
           if (c.b != L.version) {
             if (lane == 0) {
@@ -788,79 +1052,62 @@ __global__ void __launch_bounds__(kThreads, 1) gs_interp_kernel(KParams p) {
           } else {
             const Shape sh = shape_of(c.probe);
             warp_commit(p.dev[c.dev], dyn, L, c.handle, sh, p.plan_io, (int)c.a, lane);
-            if (lane == 0) out->outcome = GS_OK;
+            if (lane == 0) {
+              out->outcome = GS_OK;
+              S.agg_ok[c.dev] = 0;  // arbitrary plans: stop trusting the bound
+            }
           }
+          break;
         }
-        break;
-      case OP_CHECK: {
-        // check_conservation (device_model.py:220-245)
-        const KDev &D = p.dev[c.dev];
-        const SLed &L = S.led[c.dev];
-        if (tid == 0) {
-          int k = GS_CHECK_OK;
+        case OP_CHECK: {
+          // check_conservation (device_model.py:220-245), first violation
+          const KDev &D = p.dev[c.dev];
+          const SLed &L = S.led[c.dev];
+          int k = GS_CHECK_OK, sm = -1;
           if (L.free_mem < 0 || L.free_mem + L.held_mem != D.spec.mem_bytes) k = GS_CHECK_MEM;
           else if (L.held_warps != L.in_use_warps) k = GS_CHECK_WARPS;
-          S.chk = k ? -k : INT_MAX;
-        }
-        __syncthreads();
-        if (S.chk == INT_MAX) {
-          int *w = arr_warps(dyn, D), *t = arr_tbs(dyn, D), *r = arr_regs(dyn, D), *m = arr_smem(dyn, D);
-          for (int s = tid; s < D.n_sm; s += kThreads) {
-            int k = 0;
-            if (!(t[s] >= 0 && t[s] <= D.spec.max_tbs_per_sm)) k = GS_CHECK_SM_TBS;
-            else if (!(w[s] >= 0 && w[s] <= D.spec.max_warps_per_sm)) k = GS_CHECK_SM_WARPS;
-            else if (!(r[s] >= 0 && r[s] <= D.spec.regs_per_sm)) k = GS_CHECK_SM_REGS;
-            else if (!(m[s] >= 0 && m[s] <= D.spec.smem_per_sm_bytes)) k = GS_CHECK_SM_SMEM;
-            if (k) atomicMin(&S.chk, s * 8 + k);
+          if (k == GS_CHECK_OK) {
+            int best = INT_MAX;
+            const int *w = arr(dyn, D, 0), *t = arr(dyn, D, 1), *r = arr(dyn, D, 2), *m = arr(dyn, D, 3);
+            for (int s = lane; s < D.n_sm && best == INT_MAX; s += 32) {
+              int kk = 0;
+              if (!(t[s] >= 0 && t[s] <= D.spec.max_tbs_per_sm)) kk = GS_CHECK_SM_TBS;
+              else if (!(w[s] >= 0 && w[s] <= D.spec.max_warps_per_sm)) kk = GS_CHECK_SM_WARPS;
+              else if (!(r[s] >= 0 && r[s] <= D.spec.regs_per_sm)) kk = GS_CHECK_SM_REGS;
+              else if (!(m[s] >= 0 && m[s] <= D.spec.smem_per_sm_bytes)) kk = GS_CHECK_SM_SMEM;
+              if (kk) best = s * 8 + kk;
+            }
+            best = __reduce_min_sync(kFull, best);
+            if (best != INT_MAX) {
+              k = best & 7;
+              sm = best >> 3;
+            }
           }
-        }
-        __syncthreads();
-        if (tid == 0) {
-          int v = S.chk;
-          if (v == INT_MAX) {
-            out->outcome = GS_OK;
-            out->device = 0;
-            out->pending_index = -1;
-          } else if (v < 0) {
-            out->outcome = GS_ERR_CONTRACT;
-            out->device = -v;
-            out->pending_index = -1;
-          } else {
-            out->outcome = GS_ERR_CONTRACT;
-            out->device = v & 7;
-            out->pending_index = v >> 3;
+          if (lane == 0) {
+            out->outcome = k == GS_CHECK_OK ? GS_OK : GS_ERR_CONTRACT;
+            out->device = k;
+            out->pending_index = sm;
+            out->free_mem_after = L.held_mem;
+            out->in_use_warps_after = L.held_warps;
           }
-          out->free_mem_after = L.held_mem;
-          out->in_use_warps_after = L.held_warps;
+          break;
         }
-        break;
+        default:
+          if (lane == 0) out->outcome = GS_ERR_CONFIG;
+          break;
       }
-      default:
-        if (tid == 0) out->outcome = GS_ERR_CONFIG;
-        break;
+      __syncwarp();
     }
-    __syncthreads();
   }
 
   // ---- write back dirty ledgers + scheduler state ----
-  for (int d = 0; d < p.n_dev; ++d) {
-    if (!S.led[d].dirty) continue;
-    const KDev &D = p.dev[d];
-    int32_t *dst = reinterpret_cast<int32_t *>(D.led + 1);
-    const int *src = dyn + D.smem_off;
-    for (int i = tid; i < 4 * D.arr_pad; i += kThreads) dst[i] = src[i];
-    if (tid == 0) {
-      gs_ledger *g = D.led;
-      const SLed &L = S.led[d];
-      g->free_mem = L.free_mem;
-      g->in_use_warps = L.in_use_warps;
-      g->version = L.version;
-      g->held_mem = L.held_mem;
-      g->held_warps = L.held_warps;
-      g->rr_cursor = L.rr_cursor;
-    }
+  led_to_stage(p, dyn, S, lane);
+  stage(p, dyn, S, false, lane);
+  {
+    const int nw = sizeof(SchedState) / 4;
+    for (int i = lane; i < nw; i += 32)
+      reinterpret_cast<int32_t *>(p.st)[i] = reinterpret_cast<const int32_t *>(&S.st)[i];
   }
-  if (tid == 0) *p.st = S.st;
   __threadfence_system();
 }
 
@@ -960,9 +1207,7 @@ struct gs_sched {
   int32_t policy = 0, cg_ratio = 6, skip_ahead = 1;
   Mapped<SchedState> st;
   DevBuf<gs_probe> pend;
-  DevBuf<int32_t> pend_flag;
   DevBuf<int32_t> claims;
-  DevBuf<int32_t> fifo;
   DevBuf<int32_t> events;
   Mapped<gs_decision> drain;
 };
@@ -996,11 +1241,22 @@ int build_params(gs_engine *eng, gs_device *const *devs, int n, Launch &L) {
     k.arr_pad = dv->arr_pad;
     k.smem_off = off;
     k.spec = dv->spec;
-    off += 4 * dv->arr_pad;
+    {
+      const gs_spec &sp = dv->spec;
+      const int64_t lim = 1LL << 22;
+      k.fast = sp.max_tbs_per_sm >= 0 && sp.max_tbs_per_sm < lim && sp.max_warps_per_sm >= 0 &&
+               sp.max_warps_per_sm < lim && sp.regs_per_sm >= 0 && sp.regs_per_sm < lim &&
+               sp.smem_per_sm_bytes >= 0 && sp.smem_per_sm_bytes < lim;
+    }
+    off += kLedHdrWords + 4 * dv->arr_pad;
     max_pad = std::max(max_pad, dv->arr_pad);
   }
   p.max_sm_pad = max_pad;
-  L.smem = (size_t)(off + kWarps * 2 * max_pad) * sizeof(int);
+  p.stage_q = off / 4;
+  p.scratch_off = off;
+  p.fifo_off = off + 2 * max_pad;
+  p.fifo_cap = 0;
+  L.smem = (size_t)(off + 2 * max_pad) * sizeof(int);
   if ((int)L.smem > eng->max_smem)
     return set_err(GS_ERR_CONFIG, "fleet ledgers exceed shared memory");
   p.st = eng->dummy_state.d;
@@ -1008,7 +1264,6 @@ int build_params(gs_engine *eng, gs_device *const *devs, int n, Launch &L) {
   p.plan_io = eng->plan_io.d;
   p.claims = nullptr;
   p.job_cap = 0;
-  p.fifo_cap = 1;
   return GS_OK;
 }
 
@@ -1064,21 +1319,16 @@ int sched_params(gs_sched *s, Launch &L) {
   p.st = s->st.d;
   p.pend = s->pend.d;
   p.pend_cap = (int32_t)s->pend.n;
-  p.pend_flag = s->pend_flag.d;
   p.claims = s->claims.d;
   p.job_cap = (int32_t)s->claims.n;
   p.drain_out = s->drain.d;
   p.drain_cap = (int32_t)s->drain.n;
-  p.fifo = s->fifo.d;
-  p.fifo_cap = std::max<int32_t>(1, (int32_t)(s->fifo.n / 2));
   return GS_OK;
 }
 
 int ensure_pending(gs_sched *s, int extra) {
   const size_t need = (size_t)s->st.h->pend_count + extra + 1;
   int rc = s->pend.ensure(need, s->eng->stream, true);
-  if (rc) return rc;
-  rc = s->pend_flag.ensure(need, s->eng->stream, false);
   if (rc) return rc;
   if (need > s->drain.n) {
     rc = s->drain.alloc(std::max(need, s->drain.n * 2));
@@ -1131,7 +1381,7 @@ int gs_engine_open(int cuda_device, gs_engine **out) {
   if (prop.major < 10) return set_err(GS_ERR_CUDA, "libgs is built for sm_100a (B200)");
   auto *eng = new gs_engine();
   eng->cuda_dev = cuda_device;
-  eng->max_smem = (int)prop.sharedMemPerBlockOptin - (int)sizeof(SmemStatic) - 2048;
+  eng->max_smem = (int)prop.sharedMemPerBlockOptin - (int)sizeof(Smem) - 1024;
   CU(cudaFuncSetAttribute(gs_interp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, eng->max_smem));
   CU(cudaStreamCreateWithFlags(&eng->stream, cudaStreamNonBlocking));
   int rc = eng->cmds.alloc(64);
@@ -1343,8 +1593,6 @@ int gs_sched_create(gs_engine *eng, gs_device *const *devices, int32_t n, int32_
   int rc = s->st.alloc(1);
   if (!rc) rc = s->drain.alloc(64);
   if (!rc) rc = s->pend.ensure(64, eng->stream, false);
-  if (!rc) rc = s->pend_flag.ensure(64, eng->stream, false);
-  if (!rc) rc = s->fifo.ensure(2, eng->stream, false);
   if (!rc) rc = ensure_jobs(s, 63);
   if (rc) {
     delete s;
@@ -1361,9 +1609,7 @@ void gs_sched_destroy(gs_sched *s) {
   s->st.release();
   s->drain.release();
   s->pend.release();
-  s->pend_flag.release();
   s->claims.release();
-  s->fifo.release();
   s->events.release();
   delete s;
 }
@@ -1474,7 +1720,6 @@ int gs_sweep(gs_sched *s, const gs_probe *probes, int32_t n, int32_t max_residen
     return set_err(GS_ERR_CONTRACT, "sweep needs a fresh scheduler");
   int rc = gs_engine_reserve_handles(eng, n);
   if (!rc) rc = ensure_pending(s, n);
-  if (!rc) rc = s->fifo.ensure(2 * (size_t)n + 2, eng->stream, false);
   if (!rc) rc = s->events.ensure(3 * (size_t)std::max<int64_t>(events_cap, 1), eng->stream, false);
   if (rc) return rc;
   gs_probe *dprobes = nullptr;
@@ -1488,11 +1733,25 @@ int gs_sweep(gs_sched *s, const gs_probe *probes, int32_t n, int32_t max_residen
   }
   L.p.sweep = 1;
   L.p.sweep_probes = dprobes;
+  {
+    // resident FIFO slots with cached residency data (kSlotHdr + blocks)
+    int stride = kSlotHdr + (s->policy == GS_POLICY_MGB_SM ? L.p.max_sm_pad : 0);
+    stride = (stride + 1) & ~1;
+    L.p.fifo_stride = stride;
+    const size_t room = (size_t)eng->max_smem > L.smem ? ((size_t)eng->max_smem - L.smem) / (stride * sizeof(int)) : 0;
+    L.p.fifo_cap = (int32_t)std::min<size_t>((size_t)n + 1, room);
+    if (L.p.fifo_cap < 64) {
+      cudaFree(dprobes);
+      return set_err(GS_ERR_NOMEM, "no shared memory left for the resident FIFO");
+    }
+    L.smem += (size_t)L.p.fifo_cap * stride * sizeof(int);
+  }
   L.p.n_cmds = n;
   L.p.max_resident = max_resident;
   L.p.events = s->events.d;
   L.p.events_cap = events_cap;
   s->st.h->n_events = 0;
+  s->st.h->error = 0;
   s->st.h->fifo_head = s->st.h->fifo_tail = 0;
   cudaEvent_t e0, e1;
   CU(cudaEventCreate(&e0));
@@ -1515,6 +1774,7 @@ int gs_sweep(gs_sched *s, const gs_probe *probes, int32_t n, int32_t max_residen
   cudaFree(dprobes);
   // the sweep's residents are bookkeeping of this run only
   s->st.h->fifo_head = s->st.h->fifo_tail = 0;
+  if (s->st.h->error) return set_err(s->st.h->error, "sweep overflowed the resident FIFO");
   return GS_OK;
 }
 

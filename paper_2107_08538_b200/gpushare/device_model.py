@@ -196,6 +196,22 @@ class _ResidentView(Mapping):
         return uid in self._dev._resident
 
 
+class LedgerArray(np.ndarray):
+    """Per-SM ledger array view over mapped memory; element writes from the
+    host bump the device's grow epoch (the reference exposes plain lists
+    that tests mutate directly, tests/test_device_model.py:168-170)."""
+
+    _ledger = None
+
+    def __array_finalize__(self, obj):
+        self._ledger = getattr(obj, "_ledger", None)
+
+    def __setitem__(self, key, value):
+        super().__setitem__(key, value)
+        if self._ledger is not None:
+            self._ledger.grow_epoch += 1
+
+
 def _destroy_device(lib, ptr) -> None:
     lib.gs_device_destroy(ptr)
 
@@ -224,21 +240,32 @@ class DeviceState:
         arrs = []
         for which in range(4):
             addr = self._lib.gs_device_sm_array(ptr, which)
-            arrs.append(np.ctypeslib.as_array((ctypes.c_int32 * n).from_address(addr)))
+            a = np.ctypeslib.as_array((ctypes.c_int32 * n).from_address(addr)).view(LedgerArray)
+            a._ledger = self._led
+            arrs.append(a)
         self._sm_warps, self._sm_tbs, self._sm_regs, self._sm_smem = arrs
         self._resident: dict[str, int] = {}
         self._finalizer = weakref.finalize(self, _destroy_device, self._lib, ptr)
 
     # -- ledger fields (mapped memory) ------------------------------------
+    # Host-side writes bump the ledger's grow epoch so the FIFO re-drive
+    # re-scores this device (see gs_ledger.grow_epoch in include/gs.h).
 
-    free_mem = property(lambda self: self._led.free_mem,
-                        lambda self, v: setattr(self._led, "free_mem", int(v)))
-    in_use_warps = property(lambda self: self._led.in_use_warps,
-                            lambda self, v: setattr(self._led, "in_use_warps", int(v)))
-    rr_cursor = property(lambda self: self._led.rr_cursor,
-                         lambda self, v: setattr(self._led, "rr_cursor", int(v)))
-    version = property(lambda self: self._led.version,
-                       lambda self, v: setattr(self._led, "version", int(v)))
+    def _field(name):  # noqa: N805
+        def get(self):
+            return getattr(self._led, name)
+
+        def set_(self, v):
+            setattr(self._led, name, int(v))
+            self._led.grow_epoch += 1
+
+        return property(get, set_)
+
+    free_mem = _field("free_mem")
+    in_use_warps = _field("in_use_warps")
+    rr_cursor = _field("rr_cursor")
+    version = _field("version")
+    del _field
 
     def _arr_prop(name):  # noqa: N805
         def get(self):

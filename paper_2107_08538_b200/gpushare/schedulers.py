@@ -156,7 +156,10 @@ class Scheduler:
         """Decide a fresh request; Defer queues it (schedulers.py:89-95)."""
         uid = req.task_uid
         h = self._handles.get(uid)
-        probe = pack_probe(req.resources, h, self._job(req.job_id), 1 if req.level == "job" else 0)
+        level = 1 if req.level == "job" else 0
+        if not any(uid in d._resident for d in self.devices):
+            level |= 2  # GS_PROBE_FRESH: no residency row to accumulate into
+        probe = pack_probe(req.resources, h, self._job(req.job_id), level)
         dec = self._dec
         rc = self._lib.gs_submit(self._ptr, ctypes.byref(probe), ctypes.byref(dec))
         if rc < 0:

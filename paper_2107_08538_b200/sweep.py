@@ -40,5 +40,5 @@ def gen_probes(n: int, seed: int = 0, mem_gib: tuple[int, int] = (1, 24),
     p["smem_per_block"] = smem
     p["handle"] = np.arange(n)
     p["job"] = -1
-    p["level"] = 0
+    p["level"] = 2  # GS_PROBE_FRESH: every probe names a new task handle
     return p

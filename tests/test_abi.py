@@ -31,7 +31,7 @@ def test_struct_layouts_match_header():
     from paper_2107_08538_b200 import _native as nat
 
     assert ctypes.sizeof(nat.GsProbe) == 64
-    assert ctypes.sizeof(nat.GsLedger) == 48
+    assert ctypes.sizeof(nat.GsLedger) == 64
     assert ctypes.sizeof(nat.GsDecision) == 32
     assert ctypes.sizeof(nat.GsResidency) == 48
     assert ctypes.sizeof(nat.GsSpec) == 48
