@@ -1,0 +1,204 @@
+/*
+ * gs_work.h — workload jobs (Rodinia-class + Darknet-style) and the
+ * executor that runs them under the placement engine.
+ *
+ * The reference models every job as a catalog entry with a footprint and a
+ * duration (gpushare/data/catalog.json, sim_engine.py:191-218 `_Pool`);
+ * there is no kernel code to bind.  These entry points are the B200-native
+ * replacement of that simulated execution: each job
+ * allocates its buffers on the device the engine chose, runs hand-written
+ * sm_100a kernels on its own stream, and releases its ledger entry.
+ *
+ * Synthetic inputs come from a counter-based hash (gs_hash64) shared with
+ * the CPU oracle (oracle/kernels_cpu.c), so both sides see identical data.
+ */
+#ifndef GS_WORK_H
+#define GS_WORK_H
+
+#include <stdint.h>
+
+#include "gs.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* job kinds */
+#define GS_JOB_BFS 0
+#define GS_JOB_HOTSPOT 1
+#define GS_JOB_SRAD 2
+#define GS_JOB_KMEANS 3
+#define GS_JOB_BACKPROP 4
+#define GS_JOB_NEEDLE 5
+#define GS_JOB_LUD 6
+#define GS_JOB_GEMM 7      /* Darknet-style connected / conv layer stack (bf16, tcgen05) */
+#define GS_JOB_KINDS 8
+
+/* executor modes */
+#define GS_MODE_DEVICE 0   /* inputs pre-staged in HBM, D2D into the job's buffers */
+#define GS_MODE_E2E 1      /* inputs in pinned host memory: H2D in, D2H of results */
+
+typedef struct gs_job_desc {
+    int32_t kind;
+    int32_t iters;        /* iterations (hotspot/srad/kmeans), layers (gemm) */
+    int64_t n;            /* problem size: nodes / grid edge / points / inputs / matrix edge */
+    int64_t m;            /* secondary size: features (kmeans), hidden (backprop), batch (gemm) */
+    uint64_t seed;
+} gs_job_desc;
+
+/* Per-job outcome (SimReport.jobs rows, sim_engine.py:597-609, on a wall clock). */
+typedef struct gs_job_record {
+    int32_t state;        /* 0 done, 1 crashed (oom), 2 rejected */
+    int32_t device;
+    double pull_ms;       /* worker picked the job */
+    double admit_ms;      /* placement decided ASSIGN */
+    double end_ms;
+    double wait_ms;       /* admit - pull */
+    double compute_ms;    /* Σ device time of the job's kernels (CUDA events) */
+    int64_t mem_bytes;    /* probe footprint */
+    int64_t h2d_bytes, d2h_bytes;
+    uint64_t checksum;    /* order-independent digest of the job's outputs */
+    int32_t n_kernels;
+    int32_t pad;
+} gs_job_record;
+
+typedef struct gs_exec_stats {
+    double makespan_ms;
+    int32_t completed, crashed, oom, rejected;
+    int64_t kernel_launches;   /* workload kernels launched */
+    int64_t decision_launches; /* placement-kernel launches */
+    double decision_ms;        /* host wall time spent in placement calls */
+} gs_exec_stats;
+
+/* Probe producer: footprint (buffers rounded to the 2 MiB allocation
+ * granule, plus the 8 MiB device heap the reference counts per task,
+ * task_builder.py:264-268) and the widest launch shape of the job, with
+ * registers and static shared memory taken from cudaFuncGetAttributes. */
+int gs_job_probe(const gs_job_desc *job, gs_probe *out);
+/* Bytes of the job's host inputs / outputs (for the e2e accounting). */
+int gs_job_io_bytes(const gs_job_desc *job, int64_t *in_bytes, int64_t *out_bytes);
+
+/* Run one job to completion on `cuda_device` (isolated), for tests and the
+ * solo baseline: writes outputs to host buffers when non-NULL. */
+int gs_job_run_solo(const gs_job_desc *job, int cuda_device, int mode, void *host_out, int64_t host_out_bytes,
+                    gs_job_record *rec);
+
+/* Executor: run `n_jobs` jobs through `workers` worker threads on
+ * `n_devices` CUDA devices under `policy` (GS_POLICY_*), like
+ * metrics.run_workload -> run_sim (metrics.py:101-119, sim_engine.py:632).
+ * ledger_bytes: per-device ledger capacity (0 = free HBM - reserve). */
+int gs_exec_run(const gs_job_desc *jobs, int32_t n_jobs, int32_t policy, int32_t cg_ratio,
+                const int32_t *cuda_devices, int32_t n_devices, int32_t workers, int32_t mode,
+                int64_t ledger_bytes, gs_job_record *records, gs_exec_stats *stats);
+
+/* Prepare (generate) the inputs of a job list ahead of gs_exec_run so the
+ * timed region starts with inputs resident (device) or pinned (e2e). */
+int gs_exec_stage(const gs_job_desc *jobs, int32_t n_jobs, const int32_t *cuda_devices, int32_t n_devices,
+                  int32_t mode);
+void gs_exec_unstage(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+/* ---- shared synthetic-input generator (host + device) ----------------- */
+#ifdef __CUDACC__
+#define GS_HD __host__ __device__ __forceinline__
+#else
+#define GS_HD static inline
+#endif
+
+GS_HD uint64_t gs_hash64(uint64_t seed, uint64_t i) {
+    uint64_t z = seed * 0x9E3779B97F4A7C15ull + i + 0x632BE59BD9B4E019ull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+
+/* uniform float in [0, 1) with 24 random bits (exactly representable) */
+GS_HD float gs_unit(uint64_t seed, uint64_t i) {
+    return (float)(gs_hash64(seed, i) >> 40) * (1.0f / 16777216.0f);
+}
+
+/* ---- per-workload synthetic inputs (public Rodinia algorithm inputs,
+ * restated with a shared generator; PAPER.md:770-771 names Rodinia v3.1) -- */
+
+#define GS_BFS_DEGREE 6
+#define GS_KMEANS_K 5
+#define GS_NW_PENALTY 10
+#define GS_BP_ETA 0.3f
+#define GS_BP_MOMENTUM 0.3f
+#define GS_BP_TARGET 0.1f
+#define GS_SRAD_LAMBDA 0.5f
+#define GS_HOTSPOT_AMB 80.0f
+#define GS_LUD_BS 32
+
+/* bfs: uniform random out-degree 6 CSR, row_ptr[v] = 6 v, source 0 */
+GS_HD int32_t gs_bfs_col(uint64_t seed, uint64_t e, int64_t n) {
+    return (int32_t)(gs_hash64(seed, e) % (uint64_t)n);
+}
+/* hotspot: temperatures around 323 K, power in [0, 0.1) */
+GS_HD float gs_hotspot_temp0(uint64_t seed, uint64_t i) { return 323.0f + 10.0f * gs_unit(seed, i); }
+GS_HD float gs_hotspot_power(uint64_t seed, uint64_t i) { return 0.1f * gs_unit(seed ^ 0xA5A5A5A5ull, i); }
+/* srad: positive image in [1, 2) (no transcendental, for exact parity) */
+GS_HD float gs_srad_j0(uint64_t seed, uint64_t i) { return 1.0f + gs_unit(seed, i); }
+/* kmeans: feature-major ("flipped") features in [0, 1) */
+GS_HD float gs_kmeans_feature(uint64_t seed, uint64_t i) { return gs_unit(seed, i); }
+/* backprop: bias input 1, inputs in [0, 1), small weights */
+GS_HD float gs_bp_input(uint64_t seed, uint64_t i) { return i == 0 ? 1.0f : gs_unit(seed, i); }
+GS_HD float gs_bp_w1(uint64_t seed, uint64_t i) { return (gs_unit(seed + 1, i) - 0.5f) * 2e-3f; }
+GS_HD float gs_bp_w2(uint64_t seed, uint64_t j) { return (gs_unit(seed + 2, j) - 0.5f) * 0.2f; }
+/* needle: residues in [1, 10] like Rodinia's rand() % 10 + 1 */
+GS_HD int32_t gs_nw_seq(uint64_t seed, uint64_t i) { return (int32_t)(gs_hash64(seed, i) % 10u) + 1; }
+/* lud: diagonally dominant matrix (no pivoting needed) */
+GS_HD float gs_lud_a(uint64_t seed, int64_t i, int64_t j, int64_t n) {
+    return gs_unit(seed, (uint64_t)(i * n + j)) + (i == j ? (float)n : 0.0f);
+}
+
+/* BLOSUM62, residue order A R N D C Q E G H I L K M F P S T W Y V B Z X * */
+#define GS_BLOSUM62_INIT {                                                                  \
+    { 4,-1,-2,-2, 0,-1,-1, 0,-2,-1,-1,-1,-1,-2,-1, 1, 0,-3,-2, 0,-2,-1, 0,-4},            \
+    {-1, 5, 0,-2,-3, 1, 0,-2, 0,-3,-2, 2,-1,-3,-2,-1,-1,-3,-2,-3,-1, 0,-1,-4},            \
+    {-2, 0, 6, 1,-3, 0, 0, 0, 1,-3,-3, 0,-2,-3,-2, 1, 0,-4,-2,-3, 3, 0,-1,-4},            \
+    {-2,-2, 1, 6,-3, 0, 2,-1,-1,-3,-4,-1,-3,-3,-1, 0,-1,-4,-3,-3, 4, 1,-1,-4},            \
+    { 0,-3,-3,-3, 9,-3,-4,-3,-3,-1,-1,-3,-1,-2,-3,-1,-1,-2,-2,-1,-3,-3,-2,-4},            \
+    {-1, 1, 0, 0,-3, 5, 2,-2, 0,-3,-2, 1, 0,-3,-1, 0,-1,-2,-1,-2, 0, 3,-1,-4},            \
+    {-1, 0, 0, 2,-4, 2, 5,-2, 0,-3,-3, 1,-2,-3,-1, 0,-1,-3,-2,-2, 1, 4,-1,-4},            \
+    { 0,-2, 0,-1,-3,-2,-2, 6,-2,-4,-4,-2,-3,-3,-2, 0,-2,-2,-3,-3,-1,-2,-1,-4},            \
+    {-2, 0, 1,-1,-3, 0, 0,-2, 8,-3,-3,-1,-2,-1,-2,-1,-2,-2, 2,-3, 0, 0,-1,-4},            \
+    {-1,-3,-3,-3,-1,-3,-3,-4,-3, 4, 2,-3, 1, 0,-3,-2,-1,-3,-1, 3,-3,-3,-1,-4},            \
+    {-1,-2,-3,-4,-1,-2,-3,-4,-3, 2, 4,-2, 2, 0,-3,-2,-1,-2,-1, 1,-4,-3,-1,-4},            \
+    {-1, 2, 0,-1,-3, 1, 1,-2,-1,-3,-2, 5,-1,-3,-1, 0,-1,-3,-2,-2, 0, 1,-1,-4},            \
+    {-1,-1,-2,-3,-1, 0,-2,-3,-2, 1, 2,-1, 5, 0,-2,-1,-1,-1,-1, 1,-3,-1,-1,-4},            \
+    {-2,-3,-3,-3,-2,-3,-3,-3,-1, 0, 0,-3, 0, 6,-4,-2,-2, 1, 3,-1,-3,-3,-1,-4},            \
+    {-1,-2,-2,-1,-3,-1,-1,-2,-2,-3,-3,-1,-2,-4, 7,-1,-1,-4,-3,-2,-2,-1,-2,-4},            \
+    { 1,-1, 1, 0,-1, 0, 0, 0,-1,-2,-2, 0,-1,-2,-1, 4, 1,-3,-2,-2, 0, 0, 0,-4},            \
+    { 0,-1, 0,-1,-1,-1,-1,-2,-2,-1,-1,-1,-1,-2,-1, 1, 5,-2,-2, 0,-1,-1, 0,-4},            \
+    {-3,-3,-4,-4,-2,-2,-3,-2,-2,-3,-2,-3,-1, 1,-4,-3,-2,11, 2,-3,-4,-3,-2,-4},            \
+    {-2,-2,-2,-3,-2,-1,-2,-3, 2,-1,-1,-2,-1, 3,-3,-2,-2, 2, 7,-1,-3,-2,-1,-4},            \
+    { 0,-3,-3,-3,-1,-2,-2,-3,-3, 3, 1,-2, 1,-1,-2,-2, 0,-3,-1, 4,-3,-2,-1,-4},            \
+    {-2,-1, 3, 4,-3, 0, 1,-1, 0,-3,-4, 0,-3,-3,-2, 0,-1,-4,-3,-3, 4, 1,-1,-4},            \
+    {-1, 0, 0, 1,-3, 3, 4,-2, 0,-3,-3, 1,-1,-3,-1, 0,-1,-3,-2,-2, 1, 4,-1,-4},            \
+    { 0,-1,-1,-1,-2,-1,-1,-1,-1,-1,-1,-1,-1,-1,-2, 0, 0,-2,-1,-1,-1,-1,-1,-4},            \
+    {-4,-4,-4,-4,-4,-4,-4,-4,-4,-4,-4,-4,-4,-4,-4,-4,-4,-4,-4,-4,-4,-4,-4, 1}}
+
+/* hotspot coefficients (Rodinia hotspot constants; the cell size is fixed
+ * at a 1024-grid of a 16 mm chip so larger grids stay numerically stable).
+ * Computed in double on the host, identically for the GPU and the oracle. */
+static inline void gs_hotspot_coeffs(float *cc, float *rx1, float *ry1, float *rz1) {
+    const double t_chip = 0.0005, chip = 0.016, factor_chip = 0.5, spec_heat_si = 1.75e6, k_si = 100.0;
+    const double precision = 0.001, max_pd = 3.0e6;
+    const double gh = chip / 1024.0, gw = chip / 1024.0;
+    const double cap = factor_chip * spec_heat_si * t_chip * gw * gh;
+    const double rx = gw / (2.0 * k_si * t_chip * gh);
+    const double ry = gh / (2.0 * k_si * t_chip * gw);
+    const double rz = t_chip / (k_si * gh * gw);
+    const double max_slope = max_pd / (factor_chip * t_chip * spec_heat_si);
+    const double step = precision / max_slope;
+    *cc = (float)(step / cap);
+    *rx1 = (float)(1.0 / rx);
+    *ry1 = (float)(1.0 / ry);
+    *rz1 = (float)(1.0 / rz);
+}
+
+#endif /* GS_WORK_H */

@@ -1,0 +1,464 @@
+// gs_exec.cu — the executor: real jobs under the placement engine.
+//
+// Replaces the reference's virtual-time runtime (sim_engine.py: worker pool
+// _on_pull :286-303, probe admission _handle_probe :393-415, processor-
+// sharing _Pool :191-218, release + FIFO re-drive :541-547 / :278-282) with
+// wall-clock execution on B200s:
+//   * W worker threads pull jobs in order (the reference's workers);
+//   * each job's probe (footprint + launch shape, gs_job_probe) is decided
+//     by the GPU decision kernel (gs_submit); DEFER parks the worker until a
+//     release re-drives the FIFO (gs_on_release) and admits it;
+//   * the job runs on its own stream of the chosen device, allocating from
+//     that device's stream-ordered pool — the ledger never promises more
+//     than the pool can give, so memory-safe policies cannot OOM; sa / cg
+//     allocate without checks and can (a failed allocation is an "oom"
+//     crash record, sim_engine.py:342-350);
+//   * completion releases the task's ledger entry and re-drives the queue.
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <string.h>
+
+#include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <condition_variable>
+#include <mutex>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "../../include/gs.h"
+#include "../../include/gs_work.h"
+#include "gs_work_internal.h"
+
+using namespace gsw;
+
+#define CUE(call)                                                                 \
+  do {                                                                            \
+    cudaError_t e_ = (call);                                                      \
+    if (e_ != cudaSuccess) return err(GS_ERR_CUDA, std::string(#call ": ") + cudaGetErrorString(e_)); \
+  } while (0)
+
+namespace {
+
+using Clock = std::chrono::steady_clock;
+
+double ms_since(Clock::time_point t0) {
+  return std::chrono::duration<double, std::milli>(Clock::now() - t0).count();
+}
+
+// Staged inputs of one job: device buffers (GS_MODE_DEVICE) or pinned host
+// buffers (GS_MODE_E2E), one per job buffer (nullptr for OUT/SCR).
+struct Staged {
+  gs_job_desc desc{};
+  int device = 0;
+  bool host = false;
+  std::vector<void *> ptr;
+};
+
+std::mutex g_stage_mu;
+std::vector<Staged> g_staged;
+
+void free_staged(Staged &s) {
+  for (void *p : s.ptr) {
+    if (!p) continue;
+    if (s.host) cudaFreeHost(p);
+    else cudaFree(p);
+  }
+  s.ptr.clear();
+}
+
+bool same_desc(const gs_job_desc &a, const gs_job_desc &b) { return memcmp(&a, &b, sizeof(a)) == 0; }
+
+const Staged *find_staged(const gs_job_desc &d) {
+  for (const Staged &s : g_staged)
+    if (same_desc(s.desc, d)) return &s;
+  return nullptr;
+}
+
+int stage_one(const gs_job_desc &j, int device, int mode, Staged &out) {
+  CUE(cudaSetDevice(device));
+  const std::vector<Buf> bufs = job_buffers(j);
+  std::vector<void *> dev(bufs.size(), nullptr);
+  out.desc = j;
+  out.device = device;
+  out.host = mode == GS_MODE_E2E;
+  out.ptr.assign(bufs.size(), nullptr);
+  cudaStream_t st;
+  CUE(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  for (size_t i = 0; i < bufs.size(); ++i)
+    if (bufs[i].role == IN || bufs[i].role == INOUT) CUE(cudaMalloc(&dev[i], bufs[i].bytes));
+  int rc = generate_inputs(j, dev, st);
+  if (rc) return rc;
+  for (size_t i = 0; i < bufs.size(); ++i) {
+    if (!dev[i]) continue;
+    if (out.host) {
+      CUE(cudaHostAlloc(&out.ptr[i], bufs[i].bytes, cudaHostAllocPortable));
+      CUE(cudaMemcpyAsync(out.ptr[i], dev[i], bufs[i].bytes, cudaMemcpyDeviceToHost, st));
+    } else {
+      out.ptr[i] = dev[i];
+      dev[i] = nullptr;
+    }
+  }
+  CUE(cudaStreamSynchronize(st));
+  for (void *p : dev)
+    if (p) cudaFree(p);
+  cudaStreamDestroy(st);
+  return GS_OK;
+}
+
+// One job, start to finish, on (device, stream).  *oom is set when the
+// device pool refused an allocation.
+int run_job(const gs_job_desc &j, const Staged *stg, int mode, cudaStream_t st, gs_job_record &rec, bool *oom,
+            void *host_out, int64_t host_out_bytes, int32_t *host_scalar, std::atomic<int64_t> *kernel_count,
+            unsigned long long *host_sum, int device) {
+  *oom = false;
+  const std::vector<Buf> bufs = job_buffers(j);
+  std::vector<void *> buf(bufs.size(), nullptr);
+  unsigned long long *dsum = nullptr;
+  auto release = [&]() {
+    for (void *p : buf)
+      if (p) cudaFreeAsync(p, st);
+    if (dsum) cudaFreeAsync(dsum, st);
+    cudaStreamSynchronize(st);
+  };
+  for (size_t i = 0; i < bufs.size(); ++i) {
+    cudaError_t e = cudaMallocAsync(&buf[i], bufs[i].bytes, st);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      buf[i] = nullptr;
+      release();
+      if (e == cudaErrorMemoryAllocation) {
+        *oom = true;
+        return GS_OK;
+      }
+      return err(GS_ERR_CUDA, std::string("cudaMallocAsync: ") + cudaGetErrorString(e));
+    }
+  }
+  if (cudaMallocAsync((void **)&dsum, 8, st) != cudaSuccess) {
+    cudaGetLastError();
+    dsum = nullptr;
+    release();
+    *oom = true;
+    return GS_OK;
+  }
+  // inputs in
+  for (size_t i = 0; i < bufs.size(); ++i) {
+    if (bufs[i].role == IN || bufs[i].role == INOUT) {
+      if (stg) {
+        if (stg->host) {
+          CUE(cudaMemcpyAsync(buf[i], stg->ptr[i], bufs[i].bytes, cudaMemcpyHostToDevice, st));
+          rec.h2d_bytes += bufs[i].bytes;
+        } else if (stg->device == device) {
+          CUE(cudaMemcpyAsync(buf[i], stg->ptr[i], bufs[i].bytes, cudaMemcpyDeviceToDevice, st));
+        } else {
+          CUE(cudaMemcpyPeerAsync(buf[i], device, stg->ptr[i], stg->device, bufs[i].bytes, st));
+        }
+      }
+    } else if (bufs[i].role == SCR) {
+      CUE(cudaMemsetAsync(buf[i], 0, bufs[i].bytes, st));
+    }
+  }
+  if (!stg) {  // unstaged: synthesize the inputs in place
+    int rc = generate_inputs(j, buf, st);
+    if (rc) return rc;
+  }
+  cudaEvent_t e0, e1;
+  CUE(cudaEventCreate(&e0));
+  CUE(cudaEventCreate(&e1));
+  CUE(cudaEventRecord(e0, st));
+  int out_idx = 0;
+  int64_t launches = 0;
+  int rc = run_kernels(j, buf, st, &out_idx, &launches, host_scalar);
+  if (rc) return rc;
+  CUE(cudaEventRecord(e1, st));
+  rec.n_kernels = (int32_t)launches;
+  kernel_count->fetch_add(launches + 1);
+  // outputs: the primary output buffer (and every OUT buffer in e2e)
+  rc = digest(buf[out_idx], bufs[out_idx].bytes, dsum, st);
+  if (rc) return rc;
+  if (mode == GS_MODE_E2E) {
+    int64_t off = 0;
+    for (size_t i = 0; i < bufs.size(); ++i) {
+      const bool is_out = bufs[i].role == OUT || (int)i == out_idx;
+      if (!is_out) continue;
+      if (host_out && off + bufs[i].bytes <= host_out_bytes) {
+        CUE(cudaMemcpyAsync((char *)host_out + off, buf[i], bufs[i].bytes, cudaMemcpyDeviceToHost, st));
+        off += bufs[i].bytes;
+        rec.d2h_bytes += bufs[i].bytes;
+      }
+    }
+  } else if (host_out && bufs[out_idx].bytes <= host_out_bytes) {
+    CUE(cudaMemcpyAsync(host_out, buf[out_idx], bufs[out_idx].bytes, cudaMemcpyDeviceToHost, st));
+  }
+  CUE(cudaMemcpyAsync(host_sum, dsum, 8, cudaMemcpyDeviceToHost, st));
+  rec.d2h_bytes += 8;
+  CUE(cudaStreamSynchronize(st));
+  float ms = 0;
+  CUE(cudaEventElapsedTime(&ms, e0, e1));
+  rec.compute_ms = ms;
+  rec.checksum = *host_sum;
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  release();
+  return GS_OK;
+}
+
+int64_t max_out_bytes(const gs_job_desc *jobs, int n) {
+  int64_t m = 0;
+  for (int i = 0; i < n; ++i) {
+    int64_t o = 0;
+    for (const Buf &b : job_buffers(jobs[i])) o += b.bytes;  // conservative: every buffer
+    m = std::max(m, o);
+  }
+  return m;
+}
+
+}  // namespace
+
+extern "C" {
+
+int gs_exec_stage(const gs_job_desc *jobs, int32_t n_jobs, const int32_t *cuda_devices, int32_t n_devices,
+                  int32_t mode) {
+  std::lock_guard<std::mutex> g(g_stage_mu);
+  for (int i = 0; i < n_jobs; ++i) {
+    int rc = validate(jobs[i]);
+    if (rc) return rc;
+    if (find_staged(jobs[i])) continue;
+    Staged s;
+    rc = stage_one(jobs[i], cuda_devices[i % n_devices], mode, s);
+    if (rc) {
+      free_staged(s);
+      return rc;
+    }
+    g_staged.push_back(std::move(s));
+  }
+  return GS_OK;
+}
+
+void gs_exec_unstage(void) {
+  std::lock_guard<std::mutex> g(g_stage_mu);
+  for (Staged &s : g_staged) free_staged(s);
+  g_staged.clear();
+}
+
+int gs_job_run_solo(const gs_job_desc *job, int cuda_device, int mode, void *host_out, int64_t host_out_bytes,
+                    gs_job_record *rec) {
+  int rc = validate(*job);
+  if (rc) return rc;
+  CUE(cudaSetDevice(cuda_device));
+  memset(rec, 0, sizeof(*rec));
+  cudaStream_t st;
+  CUE(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  int32_t *scalar;
+  unsigned long long *hsum;
+  CUE(cudaHostAlloc((void **)&scalar, 16, 0));
+  CUE(cudaHostAlloc((void **)&hsum, 16, 0));
+  std::atomic<int64_t> kc{0};
+  const Staged *stg = nullptr;
+  {
+    std::lock_guard<std::mutex> g(g_stage_mu);
+    stg = find_staged(*job);
+  }
+  bool oom = false;
+  const auto t0 = Clock::now();
+  rc = run_job(*job, stg, mode, st, *rec, &oom, host_out, host_out_bytes, scalar, &kc, hsum, cuda_device);
+  rec->end_ms = ms_since(t0);
+  rec->device = cuda_device;
+  rec->state = oom ? 1 : 0;
+  cudaFreeHost(scalar);
+  cudaFreeHost(hsum);
+  cudaStreamDestroy(st);
+  return rc;
+}
+
+int gs_exec_run(const gs_job_desc *jobs, int32_t n_jobs, int32_t policy, int32_t cg_ratio,
+                const int32_t *cuda_devices, int32_t n_devices, int32_t workers, int32_t mode, int64_t ledger_bytes,
+                gs_job_record *records, gs_exec_stats *stats) {
+  if (n_jobs <= 0) return GS_OK;
+  if (n_devices < 1 || n_devices > GS_MAX_DEVICES) return err(GS_ERR_CONFIG, "1..32 devices");
+  if (workers < 1) return err(GS_ERR_CONFIG, "need at least one worker");
+  for (int i = 0; i < n_jobs; ++i) {
+    int rc = validate(jobs[i]);
+    if (rc) return rc;
+  }
+  const bool task_level = policy == GS_POLICY_MGB_SM || policy == GS_POLICY_MGB_WARPS;
+  // decision engine on the first device; one ledger per device
+  gs_engine *eng = nullptr;
+  int rc = gs_engine_open(cuda_devices[0], &eng);
+  if (rc) return err(rc, gs_last_error());
+  std::vector<gs_device *> ledgers(n_devices, nullptr);
+  for (int d = 0; d < n_devices; ++d) {
+    cudaDeviceProp prop;
+    CUE(cudaGetDeviceProperties(&prop, cuda_devices[d]));
+    CUE(cudaSetDevice(cuda_devices[d]));
+    size_t free_b = 0, total_b = 0;
+    CUE(cudaMemGetInfo(&free_b, &total_b));
+    // keep the pool's memory (no trimming between jobs)
+    cudaMemPool_t pool;
+    CUE(cudaDeviceGetDefaultMemPool(&pool, cuda_devices[d]));
+    uint64_t thr = UINT64_MAX;
+    CUE(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+    gs_spec spec;
+    spec.sm_count = prop.multiProcessorCount;
+    spec.mem_bytes = ledger_bytes > 0 ? ledger_bytes : (int64_t)free_b - (int64_t)(6ll << 30);
+    spec.max_warps_per_sm = prop.maxThreadsPerMultiProcessor / 32;
+    spec.max_tbs_per_sm = prop.maxBlocksPerMultiProcessor;
+    spec.regs_per_sm = prop.regsPerMultiprocessor;
+    spec.smem_per_sm_bytes = (int64_t)prop.sharedMemPerMultiprocessor;
+    rc = gs_device_create(eng, &spec, d, &ledgers[d]);
+    if (rc) return err(rc, gs_last_error());
+  }
+  gs_sched *sched = nullptr;
+  rc = gs_sched_create(eng, ledgers.data(), n_devices, policy, cg_ratio, 1, &sched);
+  if (rc) return err(rc, gs_last_error());
+  rc = gs_engine_reserve_handles(eng, n_jobs + 1);
+  if (rc) return err(rc, gs_last_error());
+
+  memset(records, 0, sizeof(gs_job_record) * n_jobs);
+  std::vector<int> admitted(n_jobs, -1);
+  std::vector<gs_decision> drain(n_jobs + 1);
+  std::mutex mu;
+  std::condition_variable cv;
+  std::atomic<int> next{0};
+  std::atomic<int64_t> kernels{0};
+  double decision_ms = 0;
+  int first_err = GS_OK;
+  std::string first_msg;
+  const int64_t out_cap = mode == GS_MODE_E2E ? max_out_bytes(jobs, n_jobs) : 0;
+  const auto t0 = Clock::now();
+
+  auto redrive = [&]() {  // caller holds mu
+    int32_t tried = 0, adm = 0;
+    const auto a = Clock::now();
+    int r = gs_on_release(sched, drain.data(), (int32_t)drain.size(), &tried, &adm);
+    decision_ms += ms_since(a);
+    if (r < 0) return r;
+    for (int k = 0; k < tried; ++k)
+      if (drain[k].outcome == GS_ASSIGN) admitted[drain[k].handle] = drain[k].device;
+    if (adm) cv.notify_all();
+    return GS_OK;
+  };
+
+  auto worker = [&](int wid) {
+    std::vector<cudaStream_t> streams(n_devices, nullptr);
+    for (int d = 0; d < n_devices; ++d) {
+      cudaSetDevice(cuda_devices[d]);
+      cudaStreamCreateWithFlags(&streams[d], cudaStreamNonBlocking);
+    }
+    void *host_out = nullptr;
+    if (out_cap) cudaHostAlloc(&host_out, out_cap, cudaHostAllocPortable);
+    int32_t *scalar = nullptr;
+    unsigned long long *hsum = nullptr;
+    cudaHostAlloc((void **)&scalar, 16, cudaHostAllocPortable);
+    cudaHostAlloc((void **)&hsum, 16, cudaHostAllocPortable);
+    for (;;) {
+      const int j = next.fetch_add(1);
+      if (j >= n_jobs) break;
+      gs_job_record &rec = records[j];
+      rec.pull_ms = ms_since(t0);
+      gs_probe pr;
+      gs_job_probe(&jobs[j], &pr);
+      rec.mem_bytes = pr.mem_bytes;
+      pr.handle = j;
+      pr.job = j;
+      if (task_level) {
+        pr.level = GS_PROBE_FRESH;
+      } else {  // job-granular claim with zero resources (sim_engine.py:295-302)
+        gs_probe z;
+        memset(&z, 0, sizeof z);
+        z.handle = j;
+        z.job = j;
+        z.level = GS_PROBE_JOB;
+        pr = z;
+      }
+      int dev = -1;
+      {
+        std::unique_lock<std::mutex> lk(mu);
+        gs_decision dec;
+        const auto a = Clock::now();
+        int r = gs_submit(sched, &pr, &dec);
+        decision_ms += ms_since(a);
+        if (r < 0) {
+          if (!first_err) {
+            first_err = r;
+            first_msg = gs_last_error();
+          }
+          rec.state = 2;
+          continue;
+        }
+        if (dec.outcome == GS_REJECTED) {
+          rec.state = 2;
+          rec.end_ms = ms_since(t0);
+          continue;
+        }
+        if (dec.outcome == GS_ASSIGN) {
+          dev = dec.device;
+        } else {
+          cv.wait(lk, [&] { return admitted[j] >= 0; });
+          dev = admitted[j];
+        }
+      }
+      rec.admit_ms = ms_since(t0);
+      rec.wait_ms = rec.admit_ms - rec.pull_ms;
+      rec.device = dev;
+      cudaSetDevice(cuda_devices[dev]);
+      const Staged *stg = nullptr;
+      {
+        std::lock_guard<std::mutex> g(g_stage_mu);
+        stg = find_staged(jobs[j]);
+      }
+      bool oom = false;
+      int r = run_job(jobs[j], stg, mode, streams[dev], rec, &oom, host_out, out_cap, scalar, &kernels, hsum,
+                      cuda_devices[dev]);
+      rec.end_ms = ms_since(t0);
+      rec.state = oom ? 1 : 0;
+      std::unique_lock<std::mutex> lk(mu);
+      if (r < 0 && !first_err) {
+        first_err = r;
+        first_msg = t_err;
+      }
+      const auto a = Clock::now();
+      if (task_level) {
+        int64_t freed = 0;
+        gs_release(ledgers[dev], j, &freed);
+      } else {
+        gs_job_ended(sched, j);
+      }
+      decision_ms += ms_since(a);
+      redrive();
+    }
+    for (cudaStream_t s : streams) cudaStreamDestroy(s);
+    if (host_out) cudaFreeHost(host_out);
+    cudaFreeHost(scalar);
+    cudaFreeHost(hsum);
+    (void)wid;
+  };
+  std::vector<std::thread> pool;
+  for (int w = 0; w < workers; ++w) pool.emplace_back(worker, w);
+  for (auto &t : pool) t.join();
+  for (int d = 0; d < n_devices; ++d) {
+    cudaSetDevice(cuda_devices[d]);
+    cudaDeviceSynchronize();
+  }
+  if (stats) {
+    memset(stats, 0, sizeof(*stats));
+    for (int i = 0; i < n_jobs; ++i) {
+      stats->makespan_ms = std::max(stats->makespan_ms, records[i].end_ms);
+      if (records[i].state == 0) stats->completed++;
+      else stats->crashed++;
+      if (records[i].state == 1) stats->oom++;
+      if (records[i].state == 2) stats->rejected++;
+    }
+    stats->kernel_launches = kernels.load();
+    stats->decision_launches = gs_engine_launches(eng);
+    stats->decision_ms = decision_ms;
+  }
+  gs_sched_destroy(sched);
+  for (gs_device *d : ledgers) gs_device_destroy(d);
+  gs_engine_close(eng);
+  if (first_err) return err(first_err, first_msg);
+  return GS_OK;
+}
+
+}  // extern "C"

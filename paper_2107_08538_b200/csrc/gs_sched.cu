@@ -1122,6 +1122,15 @@ int set_err(int code, const std::string &msg) {
   return code;
 }
 
+}  // namespace
+
+namespace gsw {
+// shared by the job runners / executor (gs_work.cu, gs_exec.cu)
+void set_last_error(const std::string &msg) { g_err = msg; }
+}  // namespace gsw
+
+namespace {
+
 #define CU(call)                                                                  \
   do {                                                                            \
     cudaError_t e_ = (call);                                                      \
@@ -1216,6 +1225,23 @@ namespace {
 
 int pad4(int64_t n) { return (int)((n + 3) / 4 * 4); }
 
+// Serializes engine calls (single decision authority) and makes the engine's
+// device current for the duration of the call (worker threads of the
+// executor keep their own device current between calls).
+struct EngineLock {
+  std::lock_guard<std::recursive_mutex> g;
+  int prev = -1;
+  explicit EngineLock(gs_engine *e) : g(e->mu) {
+    cudaGetDevice(&prev);
+    if (prev != e->cuda_dev) cudaSetDevice(e->cuda_dev);
+  }
+  ~EngineLock() {
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+  }
+};
+
 int grow_device_res(gs_device *dv, int32_t cap) {
   return dv->res.ensure((size_t)cap * dv->stride, dv->eng->stream, true);
 }
@@ -1290,7 +1316,7 @@ int ensure_cmds(gs_engine *eng, int n) {
 // Run `n` single-device commands on a one-device fleet.
 int run_device_cmd(gs_device *dv, const Cmd &c, gs_decision *out) {
   gs_engine *eng = dv->eng;
-  std::lock_guard<std::recursive_mutex> g(eng->mu);
+  EngineLock g(eng);
   Launch L;
   gs_device *arr[1] = {dv};
   int rc = build_params(eng, arr, 1, L);
@@ -1383,7 +1409,12 @@ int gs_engine_open(int cuda_device, gs_engine **out) {
   eng->cuda_dev = cuda_device;
   eng->max_smem = (int)prop.sharedMemPerBlockOptin - (int)sizeof(Smem) - 1024;
   CU(cudaFuncSetAttribute(gs_interp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, eng->max_smem));
-  CU(cudaStreamCreateWithFlags(&eng->stream, cudaStreamNonBlocking));
+  {
+    // decisions preempt workload blocks at the block scheduler
+    int lo = 0, hi = 0;
+    CU(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    CU(cudaStreamCreateWithPriority(&eng->stream, cudaStreamNonBlocking, hi));
+  }
   int rc = eng->cmds.alloc(64);
   if (!rc) rc = eng->results.alloc(64);
   if (!rc) rc = eng->plan_io.alloc(4096);
@@ -1411,7 +1442,7 @@ void gs_engine_close(gs_engine *eng) {
 }
 
 int gs_engine_reserve_handles(gs_engine *eng, int32_t capacity) {
-  std::lock_guard<std::recursive_mutex> g(eng->mu);
+  EngineLock g(eng);
   if (capacity <= eng->res_cap) return GS_OK;
   int32_t cap = std::max(capacity, eng->res_cap * 2);
   for (gs_device *dv : eng->devices) {
@@ -1426,7 +1457,7 @@ int32_t gs_engine_handle_capacity(gs_engine *eng) { return eng->res_cap; }
 int64_t gs_engine_launches(gs_engine *eng) { return eng->launches; }
 
 int gs_device_create(gs_engine *eng, const gs_spec *spec, int32_t index, gs_device **out) {
-  std::lock_guard<std::recursive_mutex> g(eng->mu);
+  EngineLock g(eng);
   *out = nullptr;
   if (spec->sm_count < 1 || spec->sm_count > 4096) return set_err(GS_ERR_CONFIG, "sm_count must be 1..4096");
   auto *dv = new gs_device();
@@ -1457,7 +1488,7 @@ int gs_device_create(gs_engine *eng, const gs_spec *spec, int32_t index, gs_devi
 void gs_device_destroy(gs_device *dv) {
   if (!dv) return;
   gs_engine *eng = dv->eng;
-  std::lock_guard<std::recursive_mutex> g(eng->mu);
+  EngineLock g(eng);
   eng->devices.erase(std::remove(eng->devices.begin(), eng->devices.end(), dv), eng->devices.end());
   dv->ledger.release();
   dv->res.release();
@@ -1473,7 +1504,7 @@ int32_t *gs_device_sm_array(gs_device *dv, int32_t which) {
 }
 
 int gs_try_place(gs_device *dv, const gs_probe *req, int32_t *blocks, int32_t *cursor, int64_t *version) {
-  std::lock_guard<std::recursive_mutex> g(dv->eng->mu);
+  EngineLock g(dv->eng);
   if (dv->spec.sm_count > (int64_t)dv->eng->plan_io.n) return set_err(GS_ERR_CONFIG, "too many SMs");
   Cmd c{};
   c.op = OP_TRY_PLACE;
@@ -1490,7 +1521,7 @@ int gs_try_place(gs_device *dv, const gs_probe *req, int32_t *blocks, int32_t *c
 
 int gs_commit(gs_device *dv, int32_t handle, const gs_probe *req, const int32_t *blocks, int32_t cursor,
               int64_t plan_version) {
-  std::lock_guard<std::recursive_mutex> g(dv->eng->mu);
+  EngineLock g(dv->eng);
   int rc = check_handle(dv->eng, handle);
   if (rc) return rc;
   memcpy(dv->eng->plan_io.h, blocks, sizeof(int32_t) * dv->spec.sm_count);
@@ -1513,7 +1544,7 @@ int gs_commit(gs_device *dv, int32_t handle, const gs_probe *req, const int32_t 
 }
 
 static int simple_dev_op(gs_device *dv, int op, int32_t handle, int64_t a, gs_decision *o) {
-  std::lock_guard<std::recursive_mutex> g(dv->eng->mu);
+  EngineLock g(dv->eng);
   if (op != OP_RESERVE && op != OP_CHECK) {
     int rc = check_handle(dv->eng, handle);
     if (rc) return rc;
@@ -1565,7 +1596,7 @@ int gs_check_conservation(gs_device *dv, int32_t *kind, int32_t *sm, int64_t *he
 }
 
 int gs_residency_read(gs_device *dv, int32_t handle, gs_residency *row, int32_t *blocks) {
-  std::lock_guard<std::recursive_mutex> g(dv->eng->mu);
+  EngineLock g(dv->eng);
   int rc = check_handle(dv->eng, handle);
   if (rc) return rc;
   const int32_t *src = dv->res.d + (size_t)handle * dv->stride;
@@ -1579,7 +1610,7 @@ int gs_residency_read(gs_device *dv, int32_t handle, gs_residency *row, int32_t 
 
 int gs_sched_create(gs_engine *eng, gs_device *const *devices, int32_t n, int32_t policy, int32_t cg_ratio,
                     int32_t skip_ahead, gs_sched **out) {
-  std::lock_guard<std::recursive_mutex> g(eng->mu);
+  EngineLock g(eng);
   *out = nullptr;
   if (n < 1 || n > GS_MAX_DEVICES) return set_err(GS_ERR_CONFIG, "fleet size must be 1..32");
   if (policy < GS_POLICY_SA || policy > GS_POLICY_MGB_WARPS) return set_err(GS_ERR_CONFIG, "unknown policy");
@@ -1605,7 +1636,7 @@ int gs_sched_create(gs_engine *eng, gs_device *const *devices, int32_t n, int32_
 
 void gs_sched_destroy(gs_sched *s) {
   if (!s) return;
-  std::lock_guard<std::recursive_mutex> g(s->eng->mu);
+  EngineLock g(s->eng);
   s->st.release();
   s->drain.release();
   s->pend.release();
@@ -1616,7 +1647,7 @@ void gs_sched_destroy(gs_sched *s) {
 
 int gs_submit_batch(gs_sched *s, const gs_probe *reqs, int32_t n, gs_decision *out) {
   gs_engine *eng = s->eng;
-  std::lock_guard<std::recursive_mutex> g(eng->mu);
+  EngineLock g(eng);
   if (n <= 0) return GS_OK;
   int32_t maxh = -1, maxj = -1;
   for (int i = 0; i < n; ++i) {
@@ -1660,7 +1691,7 @@ int gs_submit(gs_sched *s, const gs_probe *req, gs_decision *out) { return gs_su
 
 int gs_on_release(gs_sched *s, gs_decision *out, int32_t out_cap, int32_t *n_tried, int32_t *n_admitted) {
   gs_engine *eng = s->eng;
-  std::lock_guard<std::recursive_mutex> g(eng->mu);
+  EngineLock g(eng);
   int rc = ensure_pending(s, 0);
   if (!rc) rc = ensure_cmds(eng, 1);
   if (rc) return rc;
@@ -1683,7 +1714,7 @@ int gs_on_release(gs_sched *s, gs_decision *out, int32_t out_cap, int32_t *n_tri
 
 int gs_job_ended(gs_sched *s, int32_t job) {
   gs_engine *eng = s->eng;
-  std::lock_guard<std::recursive_mutex> g(eng->mu);
+  EngineLock g(eng);
   int rc = ensure_jobs(s, job);
   if (!rc) rc = ensure_cmds(eng, 1);
   if (rc) return rc;
@@ -1714,7 +1745,7 @@ int gs_sched_job_state(gs_sched *s, int32_t *sa_owner, int32_t *cg_counts, int32
 int gs_sweep(gs_sched *s, const gs_probe *probes, int32_t n, int32_t max_resident, int32_t *events,
              int64_t events_cap, int64_t *n_events, float *kernel_ms) {
   gs_engine *eng = s->eng;
-  std::lock_guard<std::recursive_mutex> g(eng->mu);
+  EngineLock g(eng);
   if (n <= 0) return GS_OK;
   if (s->st.h->pend_count != 0 || s->st.h->fifo_tail != s->st.h->fifo_head)
     return set_err(GS_ERR_CONTRACT, "sweep needs a fresh scheduler");

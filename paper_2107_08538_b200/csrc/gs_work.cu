@@ -1,0 +1,361 @@
+// gs_work.cu — workload jobs: buffers, probe, input staging and the per-kind
+// run sequences (host side) for the sm_100a kernels in gs_kernels.cuh.
+//
+// A job is the B200 counterpart of one catalog template
+// (gpushare/data/catalog.json: buffers + a kernel chain): it allocates its
+// buffers on the device the placement engine chose (stream-ordered from the
+// device pool, so the ledger's byte count is what the device really gives),
+// brings its inputs in (D2D from staged HBM, or H2D from pinned host memory
+// in e2e mode), runs its kernels on its own stream with grids sized to its
+// SM share, returns its outputs and frees everything.
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <string.h>
+
+#include <algorithm>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/gs_work.h"
+#include "gs_kernels.cuh"
+#include "gs_work_internal.h"
+
+namespace gsw {
+
+thread_local std::string t_err;
+
+void set_last_error(const std::string &msg);  // gs_sched.cu (gs_last_error)
+
+int err(int code, const std::string &m) {
+  t_err = m;
+  set_last_error(m);
+  return code;
+}
+
+#define CUW(call)                                                                 \
+  do {                                                                            \
+    cudaError_t e_ = (call);                                                      \
+    if (e_ != cudaSuccess) return err(GS_ERR_CUDA, std::string(#call ": ") + cudaGetErrorString(e_)); \
+  } while (0)
+
+constexpr int64_t kGranule = 2 << 20;       // device-pool allocation granule
+constexpr int64_t kHeap = 8 << 20;          // per-task heap (task_builder.py:29)
+constexpr int kThreads = 256;
+
+int64_t round_granule(int64_t b) { return (b + kGranule - 1) / kGranule * kGranule; }
+
+// Buffers of each kind.  role: IN staged input, INOUT staged input that is
+// also an output, OUT output, SCR scratch (zeroed).
+std::vector<Buf> job_buffers(const gs_job_desc &j) {
+  std::vector<Buf> b;
+  const int64_t n = j.n;
+  switch (j.kind) {
+    case GS_JOB_BFS:
+      b = {{(n + 1) * 4, IN}, {n * GS_BFS_DEGREE * 4, IN}, {n * 4, OUT}, {n * 4, SCR}, {n * 4, SCR}, {16, SCR}};
+      break;
+    case GS_JOB_HOTSPOT:
+      b = {{n * n * 4, INOUT}, {n * n * 4, IN}, {n * n * 4, SCR}};
+      break;
+    case GS_JOB_SRAD:
+      b = {{n * n * 4, INOUT}, {n * n * 4, SCR}, {n * n * 4, SCR}, {16, SCR}};
+      break;
+    case GS_JOB_KMEANS:
+      b = {{n * j.m * 4, IN}, {n * 4, OUT}, {(int64_t)GS_KMEANS_K * j.m * 4, OUT},
+           {(int64_t)GS_KMEANS_K * j.m * 8, SCR}, {(int64_t)GS_KMEANS_K * 8, SCR}};
+      break;
+    case GS_JOB_BACKPROP:
+      b = {{(n + 1) * 4, IN}, {j.m * (n + 1) * 4, INOUT}, {j.m * (n + 1) * 4, SCR}, {80 * 4, INOUT},
+           {(int64_t)kSMs * 8 * kMaxHid * 8, SCR}};
+      break;
+    case GS_JOB_NEEDLE:
+      b = {{(n + 1) * (n + 1) * 4, IN}, {(n + 1) * (n + 1) * 4, INOUT}};
+      break;
+    case GS_JOB_LUD:
+      b = {{n * n * 4, INOUT}};
+      break;
+    case GS_JOB_GEMM:
+      b = gemm_buffers(j);
+      break;
+    default:
+      break;
+  }
+  return b;
+}
+
+int validate(const gs_job_desc &j) {
+  if (j.kind < 0 || j.kind >= GS_JOB_KINDS) return err(GS_ERR_CONFIG, "unknown job kind");
+  if (j.n <= 0) return err(GS_ERR_CONFIG, "job size must be positive");
+  switch (j.kind) {
+    case GS_JOB_HOTSPOT:
+    case GS_JOB_SRAD:
+      if (j.n % 128) return err(GS_ERR_CONFIG, "stencil grids must be multiples of 128");
+      break;
+    case GS_JOB_NEEDLE:
+    case GS_JOB_LUD:
+      if (j.n % 32) return err(GS_ERR_CONFIG, "needle / lud sizes must be multiples of 32");
+      break;
+    case GS_JOB_KMEANS:
+      if (j.m < 1 || j.m > kMaxF) return err(GS_ERR_CONFIG, "kmeans features must be 1..64");
+      break;
+    case GS_JOB_BACKPROP:
+      if (j.m < 1 || j.m > kMaxHid) return err(GS_ERR_CONFIG, "backprop hidden units must be 1..16");
+      break;
+    case GS_JOB_GEMM:
+      return gemm_validate(j);
+    default:
+      break;
+  }
+  return GS_OK;
+}
+
+// Grid of every workload kernel: the job's SM share (2 blocks of 256
+// threads per SM on all 148 SMs) — resident-sized, so a probe's
+// thread_blocks is a real placement demand for mgb-sm.
+int job_grid(const gs_job_desc &) { return 2 * kSMs; }
+
+std::vector<Shape> job_launches(const gs_job_desc &j) {
+  const int g = job_grid(j);
+  switch (j.kind) {
+    case GS_JOB_BFS:
+      return {{(const void *)bfs_expand, g, kThreads}};
+    case GS_JOB_HOTSPOT:
+      return {{(const void *)hotspot_step, g, kThreads}};
+    case GS_JOB_SRAD:
+      return {{(const void *)srad_stats, 1, kThreads}, {(const void *)srad_coeff, g, kThreads},
+              {(const void *)srad_update, g, kThreads}};
+    case GS_JOB_KMEANS:
+      return {{(const void *)kmeans_assign, g, kThreads}, {(const void *)kmeans_recenter, 1, kThreads}};
+    case GS_JOB_BACKPROP:
+      return {{(const void *)bp_forward, g, kThreads}, {(const void *)bp_output, 1, 32},
+              {(const void *)bp_adjust, g, kThreads}};
+    case GS_JOB_NEEDLE: {
+      const int tiles = (int)(j.n / 32);
+      return {{(const void *)needle_diag, (tiles + 3) / 4, 128}};
+    }
+    case GS_JOB_LUD:
+      return {{(const void *)lud_diagonal, 1, BS}, {(const void *)lud_perimeter, (int)(j.n / BS), 2 * BS},
+              {(const void *)lud_internal, g, 256}};
+    case GS_JOB_GEMM:
+      return gemm_launches(j);
+  }
+  return {};
+}
+
+}  // namespace gsw
+
+using namespace gsw;
+
+extern "C" int gs_job_probe(const gs_job_desc *job, gs_probe *out) {
+  int rc = validate(*job);
+  if (rc) return rc;
+  memset(out, 0, sizeof(*out));
+  int64_t mem = kHeap;
+  for (const Buf &b : job_buffers(*job)) mem += round_granule(b.bytes);
+  out->mem_bytes = mem;
+  out->heap_limit_bytes = kHeap;
+  // widest launch = first max of tbs * ceil(threads / 32); regs and smem are
+  // maxima over the job's kernels (task_builder.py:272-289)
+  int64_t best = -1;
+  for (const Shape &s : job_launches(*job)) {
+    cudaFuncAttributes a;
+    if (cudaFuncGetAttributes(&a, s.fn) != cudaSuccess) return err(GS_ERR_CUDA, "cudaFuncGetAttributes failed");
+    const int wpb = (s.block + 31) / 32;
+    if ((int64_t)s.grid * wpb > best) {
+      best = (int64_t)s.grid * wpb;
+      out->thread_blocks = s.grid;
+      out->warps_per_block = wpb;
+      out->threads_per_block = s.block;
+    }
+    out->regs_per_thread = std::max(out->regs_per_thread, a.numRegs);
+    out->smem_per_block = std::max<int32_t>(out->smem_per_block, (int32_t)a.sharedSizeBytes);
+  }
+  out->total_warps = (int64_t)out->thread_blocks * out->warps_per_block;
+  out->est_duration_ms = 0.0;
+  out->handle = -1;
+  out->job = -1;
+  return GS_OK;
+}
+
+extern "C" int gs_job_io_bytes(const gs_job_desc *job, int64_t *in_bytes, int64_t *out_bytes) {
+  int rc = validate(*job);
+  if (rc) return rc;
+  int64_t i = 0, o = 0;
+  for (const Buf &b : job_buffers(*job)) {
+    if (b.role == IN || b.role == INOUT) i += b.bytes;
+    if (b.role == OUT || b.role == INOUT) o += b.bytes;
+  }
+  if (in_bytes) *in_bytes = i;
+  if (out_bytes) *out_bytes = o;
+  return GS_OK;
+}
+
+namespace gsw {
+
+// Generate a job's IN/INOUT buffers into `dst` (device pointers, one per
+// buffer; nullptr for other roles).
+int generate_inputs(const gs_job_desc &j, const std::vector<void *> &dst, cudaStream_t st) {
+  const int g = 4 * kSMs;
+  const int64_t n = j.n;
+  switch (j.kind) {
+    case GS_JOB_BFS:
+      gen_bfs<<<g, kThreads, 0, st>>>((int32_t *)dst[0], (int32_t *)dst[1], n, j.seed);
+      break;
+    case GS_JOB_HOTSPOT:
+      gen_hotspot<<<g, kThreads, 0, st>>>((float *)dst[0], (float *)dst[1], n * n, j.seed);
+      break;
+    case GS_JOB_SRAD:
+      gen_srad<<<g, kThreads, 0, st>>>((float *)dst[0], n * n, j.seed);
+      break;
+    case GS_JOB_KMEANS:
+      gen_kmeans<<<g, kThreads, 0, st>>>((float *)dst[0], n * j.m, j.seed);
+      break;
+    case GS_JOB_BACKPROP:
+      CUW(cudaMemsetAsync(dst[3], 0, 80 * 4, st));
+      gen_backprop<<<g, kThreads, 0, st>>>((float *)dst[0], (float *)dst[1], (float *)dst[3] + 17, n + 1, (int)j.m,
+                                           j.seed);
+      break;
+    case GS_JOB_NEEDLE:
+      gen_needle<<<g, kThreads, 0, st>>>((int32_t *)dst[0], (int32_t *)dst[1], n, j.seed);
+      break;
+    case GS_JOB_LUD:
+      gen_lud<<<g, kThreads, 0, st>>>((float *)dst[0], n, j.seed);
+      break;
+    case GS_JOB_GEMM:
+      return gemm_generate(j, dst, st);
+  }
+  CUW(cudaGetLastError());
+  return GS_OK;
+}
+
+// Run the kernels of a job whose buffers are ready in `buf`.  Returns the
+// index of the buffer holding the primary output in *out_idx (hotspot and
+// srad ping-pong).  `kernels` counts launches.
+int run_kernels(const gs_job_desc &j, std::vector<void *> &buf, cudaStream_t st, int *out_idx, int64_t *kernels,
+                int32_t *host_scalar) {
+  const int g = job_grid(j);
+  const int64_t n = j.n;
+  int64_t launches = 0;
+  switch (j.kind) {
+    case GS_JOB_BFS: {
+      int32_t *row = (int32_t *)buf[0], *col = (int32_t *)buf[1], *level = (int32_t *)buf[2];
+      int32_t *qa = (int32_t *)buf[3], *qb = (int32_t *)buf[4], *cnt = (int32_t *)buf[5];
+      CUW(cudaMemsetAsync(level, 0xff, n * 4, st));
+      CUW(cudaMemsetAsync(level, 0, 4, st));
+      CUW(cudaMemsetAsync(qa, 0, 4, st));
+      int32_t n_in = 1;
+      for (int32_t depth = 0; n_in > 0; ++depth) {
+        CUW(cudaMemsetAsync(cnt, 0, 4, st));
+        bfs_expand<<<g, kThreads, 0, st>>>(row, col, level, qa, n_in, qb, cnt, depth + 1);
+        ++launches;
+        // Rodinia-style host round trip per level (the frontier size)
+        CUW(cudaMemcpyAsync(host_scalar, cnt, 4, cudaMemcpyDeviceToHost, st));
+        CUW(cudaStreamSynchronize(st));
+        n_in = *host_scalar;
+        std::swap(qa, qb);
+      }
+      *out_idx = 2;
+      break;
+    }
+    case GS_JOB_HOTSPOT: {
+      float cc, rx1, ry1, rz1;
+      gs_hotspot_coeffs(&cc, &rx1, &ry1, &rz1);
+      float *t = (float *)buf[0], *p = (float *)buf[1], *t2 = (float *)buf[2];
+      for (int it = 0; it < j.iters; ++it) {
+        hotspot_step<<<g, dim3(32, 8), 0, st>>>(t, p, t2, (int)n, cc, rx1, ry1, rz1);
+        ++launches;
+        std::swap(t, t2);
+      }
+      *out_idx = (j.iters % 2) ? 2 : 0;
+      break;
+    }
+    case GS_JOB_SRAD: {
+      float *J = (float *)buf[0], *J2 = (float *)buf[1], *C = (float *)buf[2], *q0 = (float *)buf[3];
+      const int roi = n < 128 ? (int)n : 128;
+      for (int it = 0; it < j.iters; ++it) {
+        srad_stats<<<1, kThreads, 0, st>>>(J, (int)n, roi, q0);
+        srad_coeff<<<g, dim3(32, 8), 0, st>>>(J, C, (int)n, q0);
+        srad_update<<<g, dim3(32, 8), 0, st>>>(J, C, J2, (int)n);
+        launches += 3;
+        std::swap(J, J2);
+      }
+      *out_idx = (j.iters % 2) ? 1 : 0;
+      break;
+    }
+    case GS_JOB_KMEANS: {
+      const float *x = (const float *)buf[0];
+      int32_t *mem = (int32_t *)buf[1];
+      float *cent = (float *)buf[2];
+      auto *sumq = (unsigned long long *)buf[3], *cnt = (unsigned long long *)buf[4];
+      const int nf = (int)j.m;
+      CUW(cudaMemsetAsync(sumq, 0, (size_t)GS_KMEANS_K * nf * 8, st));
+      CUW(cudaMemsetAsync(cnt, 0, GS_KMEANS_K * 8, st));
+      for (int f = 0; f < nf; ++f)  // initial centroids: the first K points
+        CUW(cudaMemcpy2DAsync(cent + f, nf * 4, x + (int64_t)f * n, 4, 4, GS_KMEANS_K, cudaMemcpyDeviceToDevice,
+                              st));
+      for (int it = 0; it < j.iters; ++it) {
+        kmeans_assign<<<g, kThreads, 0, st>>>(x, n, nf, cent, mem, sumq, cnt);
+        kmeans_recenter<<<1, kThreads, 0, st>>>(cent, sumq, cnt, nf);
+        launches += 2;
+      }
+      *out_idx = 1;
+      break;
+    }
+    case GS_JOB_BACKPROP: {
+      const float *x = (const float *)buf[0];
+      float *w1 = (float *)buf[1], *ow1 = (float *)buf[2], *state = (float *)buf[3];
+      double *partial = (double *)buf[4];
+      const int nh = (int)j.m;
+      CUW(cudaMemsetAsync(ow1, 0, (size_t)nh * (n + 1) * 4, st));
+      for (int it = 0; it < j.iters; ++it) {
+        bp_forward<<<g, kThreads, 0, st>>>(x, w1, n + 1, nh, partial);
+        bp_output<<<1, 32, 0, st>>>(partial, g, nh, state);
+        bp_adjust<<<g, kThreads, 0, st>>>(x, w1, ow1, n + 1, nh, state);
+        launches += 3;
+      }
+      *out_idx = 1;
+      break;
+    }
+    case GS_JOB_NEEDLE: {
+      const int tiles = (int)(n / 32);
+      for (int d = 0; d < 2 * tiles - 1; ++d) {
+        const int lo = std::max(0, d - tiles + 1), hi = std::min(d, tiles - 1);
+        const int cnt = hi - lo + 1;
+        needle_diag<<<(cnt + 3) / 4, 128, 0, st>>>((int32_t *)buf[1], (const int32_t *)buf[0], (int)n, d, cnt, lo);
+        ++launches;
+      }
+      *out_idx = 1;
+      break;
+    }
+    case GS_JOB_LUD: {
+      float *a = (float *)buf[0];
+      for (int o = 0; o < n; o += BS) {
+        lud_diagonal<<<1, BS, 0, st>>>(a, (int)n, o);
+        ++launches;
+        if (o + BS >= n) break;
+        lud_perimeter<<<(int)((n - o) / BS - 1), 2 * BS, 0, st>>>(a, (int)n, o);
+        lud_internal<<<g, 256, 0, st>>>(a, (int)n, o);
+        launches += 2;
+      }
+      *out_idx = 0;
+      break;
+    }
+    case GS_JOB_GEMM: {
+      int rc = gemm_run(j, buf, st, out_idx, &launches);
+      if (rc) return rc;
+      break;
+    }
+  }
+  CUW(cudaGetLastError());
+  *kernels += launches;
+  return GS_OK;
+}
+
+int digest(const void *p, int64_t bytes, unsigned long long *dsum, cudaStream_t st) {
+  CUW(cudaMemsetAsync(dsum, 0, 8, st));
+  checksum_words<<<2 * kSMs, kThreads, 0, st>>>((const uint32_t *)p, bytes / 4, dsum);
+  CUW(cudaGetLastError());
+  return GS_OK;
+}
+
+}  // namespace gsw

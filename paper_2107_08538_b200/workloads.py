@@ -1,0 +1,165 @@
+"""Workload jobs and the executor (include/gs_work.h) from Python.
+
+A job is the executable counterpart of a reference catalog template
+(gpushare/data/catalog.json): Rodinia-class kernels (bfs, hotspot, srad,
+kmeans, backprop, needle, lud) written for sm_100a in csrc/gs_kernels.cuh.
+`run_jobs` is the wall-clock analogue of gpushare.metrics.run_workload ->
+sim_engine.run_sim (metrics.py:101-119): same policies (sa, cg:<r>,
+mgb-sm, mgb-warps), same worker-pool semantics, real B200 execution.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from ctypes import POINTER, c_double, c_int32, c_int64, c_uint64, c_void_p
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _native as nat
+
+KINDS = {"bfs": 0, "hotspot": 1, "srad": 2, "kmeans": 3, "backprop": 4, "needle": 5, "lud": 6, "gemm": 7}
+KIND_NAMES = {v: k for k, v in KINDS.items()}
+MODE_DEVICE, MODE_E2E = 0, 1
+
+
+class GsJobDesc(ctypes.Structure):
+    _fields_ = [("kind", c_int32), ("iters", c_int32), ("n", c_int64), ("m", c_int64), ("seed", c_uint64)]
+
+
+class GsJobRecord(ctypes.Structure):
+    _fields_ = [("state", c_int32), ("device", c_int32), ("pull_ms", c_double), ("admit_ms", c_double),
+                ("end_ms", c_double), ("wait_ms", c_double), ("compute_ms", c_double),
+                ("mem_bytes", c_int64), ("h2d_bytes", c_int64), ("d2h_bytes", c_int64),
+                ("checksum", c_uint64), ("n_kernels", c_int32), ("pad", c_int32)]
+
+
+class GsExecStats(ctypes.Structure):
+    _fields_ = [("makespan_ms", c_double), ("completed", c_int32), ("crashed", c_int32), ("oom", c_int32),
+                ("rejected", c_int32), ("kernel_launches", c_int64), ("decision_launches", c_int64),
+                ("decision_ms", c_double)]
+
+
+WORK_SIGNATURES = {
+    "gs_job_probe": (c_int32, [POINTER(GsJobDesc), POINTER(nat.GsProbe)]),
+    "gs_job_io_bytes": (c_int32, [POINTER(GsJobDesc), POINTER(c_int64), POINTER(c_int64)]),
+    "gs_job_run_solo": (c_int32, [POINTER(GsJobDesc), c_int32, c_int32, c_void_p, c_int64,
+                                  POINTER(GsJobRecord)]),
+    "gs_exec_run": (c_int32, [c_void_p, c_int32, c_int32, c_int32, POINTER(c_int32), c_int32, c_int32,
+                              c_int32, c_int64, c_void_p, POINTER(GsExecStats)]),
+    "gs_exec_stage": (c_int32, [c_void_p, c_int32, POINTER(c_int32), c_int32, c_int32]),
+    "gs_exec_unstage": (None, []),
+}
+
+_bound = False
+
+
+def lib():
+    global _bound
+    L = nat.lib()
+    if not _bound:
+        for name, (res, args) in WORK_SIGNATURES.items():
+            fn = getattr(L, name)
+            fn.restype = res
+            fn.argtypes = args
+        _bound = True
+    return L
+
+
+@dataclass(frozen=True)
+class Job:
+    """One job: kind, problem size n (nodes / grid edge / points / inputs /
+    sequence length / matrix edge), secondary size m (kmeans features,
+    backprop hidden units), iterations and seed."""
+
+    kind: str
+    n: int
+    iters: int = 1
+    m: int = 0
+    seed: int = 1
+
+    def desc(self) -> GsJobDesc:
+        return GsJobDesc(KINDS[self.kind], int(self.iters), int(self.n), int(self.m), int(self.seed))
+
+
+def probe(job: Job) -> nat.GsProbe:
+    """The job's probe: footprint + widest launch (gs_job_probe)."""
+    out = nat.GsProbe()
+    nat.check(lib().gs_job_probe(ctypes.byref(job.desc()), ctypes.byref(out)))
+    return out
+
+
+def io_bytes(job: Job) -> tuple[int, int]:
+    i, o = c_int64(), c_int64()
+    nat.check(lib().gs_job_io_bytes(ctypes.byref(job.desc()), ctypes.byref(i), ctypes.byref(o)))
+    return i.value, o.value
+
+
+OUTPUT_DTYPES = {"bfs": np.int32, "hotspot": np.float32, "srad": np.float32, "kmeans": np.int32,
+                 "backprop": np.float32, "needle": np.int32, "lud": np.float32, "gemm": np.uint16}
+
+
+def output_shape(job: Job) -> tuple[int, ...]:
+    n = job.n
+    return {"bfs": (n,), "hotspot": (n, n), "srad": (n, n), "kmeans": (n,), "backprop": (job.m, n + 1),
+            "needle": (n + 1, n + 1), "lud": (n, n)}.get(job.kind, (0,))
+
+
+def run_solo(job: Job, device: int = 0) -> tuple[np.ndarray, GsJobRecord]:
+    """Run one job alone on cuda:device; returns (primary output, record)."""
+    out = np.zeros(output_shape(job), dtype=OUTPUT_DTYPES[job.kind])
+    rec = GsJobRecord()
+    nat.check(lib().gs_job_run_solo(ctypes.byref(job.desc()), device, MODE_DEVICE, out.ctypes.data,
+                                    out.nbytes, ctypes.byref(rec)))
+    return out, rec
+
+
+def policy_code(policy: str) -> tuple[int, int]:
+    from .gpushare.schedulers import parse_policy
+
+    p = parse_policy(policy)
+    return nat.POLICY_CODES[p.kind], p.cg_ratio
+
+
+def stage(jobs: list[Job], devices: list[int], mode: int) -> None:
+    arr = (GsJobDesc * len(jobs))(*[j.desc() for j in jobs])
+    devs = (c_int32 * len(devices))(*devices)
+    nat.check(lib().gs_exec_stage(arr, len(jobs), devs, len(devices), mode))
+
+
+def unstage() -> None:
+    lib().gs_exec_unstage()
+
+
+@dataclass
+class ExecResult:
+    records: list[dict]
+    makespan_ms: float
+    completed: int
+    crashed: int
+    oom: int
+    rejected: int
+    kernel_launches: int
+    decision_launches: int
+    decision_ms: float
+
+
+def run_jobs(jobs: list[Job], policy: str = "mgb-warps", devices: list[int] = (0,), workers: int = 8,
+             mode: int = MODE_DEVICE, ledger_bytes: int = 0) -> ExecResult:
+    """Run a job list under `policy` (wall clock; see module docstring)."""
+    code, ratio = policy_code(policy)
+    arr = (GsJobDesc * len(jobs))(*[j.desc() for j in jobs])
+    recs = (GsJobRecord * len(jobs))()
+    st = GsExecStats()
+    devs = (c_int32 * len(devices))(*devices)
+    nat.check(lib().gs_exec_run(arr, len(jobs), code, ratio, devs, len(devices), workers, mode,
+                                int(ledger_bytes), recs, ctypes.byref(st)))
+    rows = []
+    for j, r in zip(jobs, recs):
+        rows.append({"kind": j.kind, "n": j.n, "state": ("done", "oom", "rejected")[r.state],
+                     "device": r.device, "pull_ms": r.pull_ms, "admit_ms": r.admit_ms, "end_ms": r.end_ms,
+                     "turnaround_ms": r.end_ms, "wait_ms": r.wait_ms, "compute_ms": r.compute_ms,
+                     "mem_bytes": r.mem_bytes, "h2d_bytes": r.h2d_bytes, "d2h_bytes": r.d2h_bytes,
+                     "checksum": r.checksum, "n_kernels": r.n_kernels})
+    return ExecResult(rows, st.makespan_ms, st.completed, st.crashed, st.oom, st.rejected,
+                      st.kernel_launches, st.decision_launches, st.decision_ms)

@@ -1,0 +1,93 @@
+"""GPU workload kernels vs the CPU oracle (pytest -m gpu).
+
+Integer outputs (bfs levels, needle scores, kmeans membership) must be
+bit-exact; float outputs within 1e-5 relative (BASELINE.json north_star).
+"""
+
+import numpy as np
+import pytest
+
+from oracle import kernels as K
+
+pytestmark = pytest.mark.gpu
+
+W = pytest.importorskip("paper_2107_08538_b200.workloads")
+
+CASES = [
+    ("bfs", dict(n=200_000, seed=3), "exact"),
+    ("bfs", dict(n=1_000_003, seed=8), "exact"),
+    ("hotspot", dict(n=512, iters=10, seed=2), 1e-5),
+    ("hotspot", dict(n=1024, iters=3, seed=5), 1e-5),
+    ("srad", dict(n=512, iters=5, seed=4), 1e-5),
+    ("kmeans", dict(n=200_000, m=34, iters=5, seed=6), "exact"),
+    ("backprop", dict(n=300_000, m=16, iters=2, seed=7), 1e-5),
+    ("needle", dict(n=512, seed=1), "exact"),
+    ("needle", dict(n=1024, seed=9), "exact"),
+    ("lud", dict(n=512, seed=3), 1e-5),
+]
+
+
+@pytest.mark.parametrize("kind,kw,tol", CASES, ids=[f"{c[0]}-{c[1]['n']}" for c in CASES])
+def test_gpu_kernel_matches_oracle(kind, kw, tol):
+    job = W.Job(kind, **kw)
+    got, rec = W.run_solo(job)
+    want = K.run(kind, **kw)
+    assert rec.state == 0 and rec.n_kernels > 0
+    if tol == "exact":
+        np.testing.assert_array_equal(got, want)
+    else:
+        np.testing.assert_allclose(got, want, rtol=tol, atol=tol)
+
+
+def test_kmeans_centroids_exact():
+    """Fixed-point centroid sums make the recentering exact."""
+    from paper_2107_08538_b200 import workloads as Wm
+
+    job = Wm.Job("kmeans", n=50_000, m=8, iters=3, seed=2)
+    mem, _ = Wm.run_solo(job)
+    cmem, _ = K.kmeans(50_000, 8, 3, 2)
+    np.testing.assert_array_equal(mem, cmem)
+
+
+def test_probe_reports_footprint_and_shape():
+    job = W.Job("hotspot", n=1024, iters=1)
+    p = W.probe(job)
+    assert p.mem_bytes == 8 * 2**20 + 3 * 4 * 2**20  # 3 x 4 MiB buffers + 8 MiB heap
+    assert p.thread_blocks == 296 and p.threads_per_block == 256 and p.warps_per_block == 8
+    assert 0 < p.regs_per_thread <= 255
+
+
+MIX = [W.Job("bfs", n=300_000, seed=1), W.Job("hotspot", n=1024, iters=20, seed=2),
+       W.Job("srad", n=1024, iters=5, seed=3), W.Job("kmeans", n=200_000, m=34, iters=3, seed=4),
+       W.Job("backprop", n=200_000, m=16, iters=1, seed=5), W.Job("needle", n=1024, seed=6),
+       W.Job("lud", n=1024, seed=7), W.Job("bfs", n=500_000, seed=8)]
+
+
+@pytest.mark.parametrize("policy", ["mgb-warps", "mgb-sm", "sa", "cg:4"])
+def test_executor_runs_mix_with_solo_checksums(policy):
+    solo = [W.run_solo(j)[1].checksum for j in MIX]
+    res = W.run_jobs(MIX, policy=policy, workers=4)
+    assert res.completed == len(MIX) and res.crashed == 0 and res.oom == 0
+    assert [r["checksum"] for r in res.records] == solo
+    assert res.kernel_launches > len(MIX) and res.decision_launches >= len(MIX)
+
+
+def test_executor_memory_safe_under_a_tight_ledger():
+    """A ledger smaller than the mix's footprint forces deferrals; mgb never
+    OOMs and every job still completes."""
+    tight = max(W.probe(j).mem_bytes for j in MIX) * 2
+    res = W.run_jobs(MIX, policy="mgb-warps", workers=8, ledger_bytes=tight)
+    assert res.completed == len(MIX) and res.oom == 0
+    assert max(r["wait_ms"] for r in res.records) > 0.0
+
+
+def test_executor_e2e_mode_moves_bytes():
+    W.stage(MIX[:3], [0], W.MODE_E2E)
+    try:
+        res = W.run_jobs(MIX[:3], policy="mgb-warps", workers=3, mode=W.MODE_E2E)
+    finally:
+        W.unstage()
+    assert res.completed == 3
+    for r, j in zip(res.records, MIX[:3]):
+        i, _ = W.io_bytes(j)
+        assert r["h2d_bytes"] == i and r["d2h_bytes"] > 0
