@@ -1,0 +1,365 @@
+"""Job-mix throughput on B200 under the GPU placement engine.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+A step runs BASELINE cfg 1's job mix (32 Rodinia-class jobs, 3:1
+large:small, synthetic seeded inputs) end to end: every job's probe is
+placed by the sm_100a decision kernel (mgb-warps, Alg. 3), jobs run
+concurrently on per-job streams with stream-ordered allocations, releases
+re-drive the FIFO.  One process per GPU; under torchrun each rank runs its
+own mix on its own device (jobs are independent: placement shards them, no
+collective on the data path) -> scaling "weak".
+
+value   jobs/s with inputs resident in HBM when the timed region starts
+e2e     jobs/s through the same API with inputs in pinned host memory:
+        H2D of every input and D2H of every output inside the timed region
+sa      the one-job-per-GPU baseline (policy sa) on the same mix and device
+
+--impl reference times the reference's path on the host CPU: the C port of
+the reference scheduler (oracle/gs_oracle.c, schedulers.py semantics) plus
+the CPU restatements of the kernels (oracle/kernels_cpu.c, all host
+threads) on a bounded sample of the same mix.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+METRIC = "job-mix jobs/s + mean turnaround at 1/2/4/8 B200 vs one-job-per-GPU; OOMs"
+UNIT = "jobs/s"
+
+
+def peaks() -> dict:
+    try:
+        with open(os.path.join(REPO, "MEASURED_PEAKS.json")) as f:
+            return json.load(f)
+    except OSError:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0, "_fallback": True}
+
+
+FP32_TFLOPS_NOMINAL = 148 * 128 * 2 * 1.965e9 / 1e12  # 74.4: 148 SMs x 128 FMA lanes
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", str(rank)))
+    return rank, world, local
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md)."""
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.path = f"/tmp/gs_clocks_{os.getpid()}.csv"
+
+    def __enter__(self):
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except OSError:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            self.proc.wait()
+
+    def summary(self) -> dict:
+        try:
+            rows = [r.split(",") for r in open(self.path).read().strip().splitlines()]
+        except OSError:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[1]) for r in rows if len(r) >= 9]
+        mx = [float(r[2]) for r in rows if len(r) >= 9]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows if len(r) >= 9 for i in range(4)
+                          if r[5 + i].strip().lower() == "active"})
+        loaded = sorted(sm)[len(sm) // 2:] if sm else []
+        return {"sm_mhz": statistics.median(loaded) if loaded else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(sm)}
+
+
+def run_steps(W, jobs, policy, device, workers, mode, steps, warmup, torch):
+    """W warm-up + K timed steps; device-timed with CUDA events."""
+    for _ in range(warmup):
+        W.run_jobs(jobs, policy=policy, devices=[device], workers=workers, mode=mode)
+    times, results = [], []
+    for _ in range(steps):
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record()
+        res = W.run_jobs(jobs, policy=policy, devices=[device], workers=workers, mode=mode)
+        e1.record()
+        torch.cuda.synchronize()
+        times.append(e0.elapsed_time(e1))
+        results.append(res)
+    return times, results
+
+
+def summarize(results, times):
+    done = [r for res in results for r in res.records if r["state"] == "done"]
+    return {
+        "ms_per_step": statistics.fmean(times),
+        "mean_turnaround_ms": statistics.fmean(r["turnaround_ms"] for r in done) if done else 0.0,
+        "mean_wait_ms": statistics.fmean(r["wait_ms"] for r in done) if done else 0.0,
+        "completed": sum(res.completed for res in results),
+        "oom": sum(res.oom for res in results),
+        "crashed": sum(res.crashed for res in results),
+        "kernel_launches": sum(res.kernel_launches for res in results),
+        "decision_launches": sum(res.decision_launches for res in results),
+        "decision_ms": sum(res.decision_ms for res in results),
+    }
+
+
+def kernel_rooflines(W, C, jobs, device, pk):
+    """Each kind's kernels alone on the device (CUDA events around its
+    kernels): algorithmic work / kernel time vs the measured peak."""
+    out = {}
+    seen = {}
+    for mj in jobs:
+        seen.setdefault(mj.job.kind, mj.job)
+    hbm = pk["hbm_gbs"]
+    for kind, job in seen.items():
+        W.run_solo(job, device)  # warm-up
+        recs = [W.run_solo(job, device)[1] for _ in range(2)]
+        ms = min(r.compute_ms for r in recs)
+        work, unit = C.algorithmic_work(job)
+        if unit == "B":
+            ach = work / (ms * 1e-3) / 1e9
+            out[kind] = {"bound": "hbm", "achieved": round(ach, 1), "peak": hbm, "unit": "GB/s",
+                         "frac": round(ach / hbm, 4), "ms": round(ms, 3), "launches": recs[0].n_kernels,
+                         "job": {"n": job.n, "iters": job.iters, "m": job.m}}
+        else:
+            ach = work / (ms * 1e-3) / 1e12
+            out[kind] = {"bound": "fp32", "achieved": round(ach, 2), "peak": round(FP32_TFLOPS_NOMINAL, 1),
+                         "unit": "TFLOP/s", "frac": round(ach / FP32_TFLOPS_NOMINAL, 4), "ms": round(ms, 3),
+                         "launches": recs[0].n_kernels, "job": {"n": job.n}}
+    return out
+
+
+def traffic_from_profiles(kind: str):
+    try:
+        with open(os.path.join(REPO, "profiles", "traffic.json")) as f:
+            return json.load(f).get(kind)
+    except (OSError, ValueError):
+        return None
+
+
+def cpu_sample(jobs, budget_s: float):
+    """The oracle's CPU kernels on all host threads over a bounded sample of
+    the mix (jobs in mix order until the time budget is spent)."""
+    from oracle import kernels as K
+
+    t0 = time.perf_counter()
+    n = 0
+    names = []
+    for mj in jobs:
+        j = mj.job
+        K.run(j.kind, n=j.n, iters=j.iters, m=j.m, seed=j.seed)
+        n += 1
+        names.append(mj.template)
+        if time.perf_counter() - t0 > budget_s:
+            break
+    dt = time.perf_counter() - t0
+    return n / dt, n, names, dt
+
+
+def reference_arm(args, jobs):
+    """--impl reference: the reference's path on host cores (C port)."""
+    from oracle import oracle as O
+    from paper_2107_08538_b200 import _native as nat
+    from paper_2107_08538_b200.catalog import host_footprint
+    from paper_2107_08538_b200.gpushare import device_spec
+
+    threads = os.cpu_count() or 1
+    values = []
+    sample_desc = ""
+    spec = device_spec("b200")
+    for step in range(args.warmup + args.steps):
+        # placement of the whole mix on the CPU scheduler port (B200
+        # ledgers), then the kernels of a bounded sample on all threads
+        t0 = time.perf_counter()
+        devs = [O.OracleDevice(spec, i) for i in range(max(1, args.gpus))]
+        sched = O.OracleScheduler(devs, 3, 6, True)
+        for i, mj in enumerate(jobs):
+            pr = nat.GsProbe(host_footprint(mj.job), 8 << 20, 296 * 8, 0.0, 296, 8, 256, 0, 0, i, i, 0)
+            sched.submit(pr)
+        rate, n, names, dt = cpu_sample(jobs[step % len(jobs):] + jobs[:step % len(jobs)], args.cpu_budget)
+        total = time.perf_counter() - t0
+        if step >= args.warmup:
+            values.append(n / total)
+            sample_desc = f"{n} of {len(jobs)} mix jobs per step ({', '.join(names)}) + placement of all {len(jobs)}"
+    v = statistics.fmean(values)
+    line = {
+        "metric": METRIC, "value": round(v, 4), "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(1000.0 / v, 1) if v else None, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32/i32", "data": "synthetic",
+        "impl": "reference",
+        "config": {"workload": f"cfg1: {len(jobs)}-job Rodinia mix {args.mix} (bounded CPU sample)",
+                   "policy": "mgb-warps (C port of schedulers.py)", "cpu_threads": threads},
+        "cpu_baseline": {"value": round(v, 4), "unit": UNIT, "cores": threads, "kind": "port",
+                         "sample": sample_desc},
+        "e2e": {"value": round(v, 4), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main() -> int:
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--policy", default="mgb-warps")
+    ap.add_argument("--mix", default="3:1")
+    ap.add_argument("--jobs", type=int, default=32)
+    ap.add_argument("--workers", type=int, default=8)
+    ap.add_argument("--cpu-budget", type=float, default=12.0)
+    ap.add_argument("--skip-e2e", action="store_true")
+    ap.add_argument("--skip-sa", action="store_true")
+    args = ap.parse_args()
+    rank, world, local = dist_env()
+
+    from paper_2107_08538_b200 import catalog as C
+
+    if args.impl == "reference":
+        if rank != 0:
+            return 0
+        reference_arm(args, C.gen_mix(args.mix, args.jobs, seed=1))
+        return 0
+
+    import torch
+
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    from paper_2107_08538_b200 import workloads as W
+
+    pk = peaks()
+    mix = C.gen_mix(args.mix, args.jobs, seed=1 + rank)
+    jobs = [m.job for m in mix]
+    device = local
+
+    # ---- device mode: inputs staged in HBM before the timed region ----
+    W.stage(jobs, [device], W.MODE_DEVICE)
+    if dist:
+        dist.barrier()
+    with Clocks(device) as clk:
+        times, results = run_steps(W, jobs, args.policy, device, args.workers, W.MODE_DEVICE, args.steps,
+                                   args.warmup, torch)
+    ours = summarize(results, times)
+    sa = None
+    if not args.skip_sa:
+        st, sr = run_steps(W, jobs, "sa", device, args.workers, W.MODE_DEVICE, args.steps, 1, torch)
+        sa = summarize(sr, st)
+    W.unstage()
+    kern = kernel_rooflines(W, C, mix, device, pk)
+
+    # ---- e2e mode: pinned host inputs, H2D + D2H inside the timed region ----
+    e2e = sa_e2e = None
+    if not args.skip_e2e:
+        W.stage(jobs, [device], W.MODE_E2E)
+        et, er = run_steps(W, jobs, args.policy, device, args.workers, W.MODE_E2E, args.steps, 1, torch)
+        e2e = summarize(er, et)
+        e2e["h2d"] = sum(r["h2d_bytes"] for r in er[-1].records)
+        e2e["d2h"] = sum(r["d2h_bytes"] for r in er[-1].records)
+        if not args.skip_sa:
+            st2, sr2 = run_steps(W, jobs, "sa", device, args.workers, W.MODE_E2E, args.steps, 1, torch)
+            sa_e2e = summarize(sr2, st2)
+        W.unstage()
+
+    # ---- max over ranks ----
+    ms_step = ours["ms_per_step"]
+    e2e_ms = e2e["ms_per_step"] if e2e else None
+    if dist:
+        t = torch.tensor([ms_step, e2e_ms or 0.0], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_step, e2e_ms = float(t[0]), float(t[1]) or None
+    n_total = len(jobs) * world
+    value = n_total / (ms_step / 1000.0)
+
+    # dominant kernel: the kind with the largest share of device time in the mix
+    share = {}
+    for r in results[-1].records:
+        share[r["kind"]] = share.get(r["kind"], 0.0) + r["compute_ms"]
+    dom = max(share, key=share.get)
+    kd = kern[dom]
+    roof = {"kernel": dom, "bound": kd["bound"], "achieved": kd["achieved"], "peak": kd["peak"],
+            "unit": kd["unit"], "frac": kd["frac"], "traffic": traffic_from_profiles(dom),
+            "share_of_mix_device_time": round(share[dom] / sum(share.values()), 3),
+            "peak_source": "MEASURED_PEAKS.json hbm_gbs (burst copy)" if kd["bound"] == "hbm"
+            else "nominal FP32 (148 SMs x 128 FMA x 1.965 GHz)"}
+    # aggregate HBM roofline fraction of the whole mix
+    mix_bytes = sum(C.algorithmic_work(j)[0] for j in jobs if C.algorithmic_work(j)[1] == "B")
+    mix_frac = mix_bytes / (ms_step / 1000.0) / 1e9 / pk["hbm_gbs"]
+
+    line = {
+        "metric": METRIC, "value": round(value, 4), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(ms_step, 2), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32/i32", "data": "synthetic (seeded hash inputs)",
+        "config": {"workload": f"cfg1: {args.jobs}-job Rodinia mix {args.mix} per GPU "
+                               "(bfs/hotspot/srad/kmeans/backprop/needle/lud)",
+                   "policy": args.policy, "workers_per_gpu": args.workers,
+                   "inputs": "staged in HBM, larger than L2 (no flush needed)", "parallelism": f"placement x{world}"},
+        "mean_turnaround_ms": round(ours["mean_turnaround_ms"], 2),
+        "mean_wait_ms": round(ours["mean_wait_ms"], 2),
+        "oom": ours["oom"], "crashed": ours["crashed"],
+        "gpu_launches": ours["kernel_launches"] + ours["decision_launches"],
+        "decision_launches": ours["decision_launches"],
+        "decision_ms_per_step": round(ours["decision_ms"] / args.steps, 3),
+        "roofline": roof,
+        "mix_hbm_frac": round(mix_frac, 4),
+        "kernels": kern,
+    }
+    if sa:
+        sa_value = n_total / (sa["ms_per_step"] / 1000.0)
+        line["sa"] = {"value": round(sa_value, 4), "ms_per_step": round(sa["ms_per_step"], 2),
+                      "mean_turnaround_ms": round(sa["mean_turnaround_ms"], 2), "oom": sa["oom"]}
+        line["speedup_vs_sa"] = round(value / sa_value, 3)
+        line["turnaround_speedup_vs_sa"] = round(sa["mean_turnaround_ms"] / max(ours["mean_turnaround_ms"], 1e-9), 3)
+    if e2e:
+        line["e2e"] = {"value": round(n_total / (e2e_ms / 1000.0), 4), "unit": UNIT,
+                       "h2d_bytes_per_step": e2e["h2d"], "d2h_bytes_per_step": e2e["d2h"],
+                       "mean_turnaround_ms": round(e2e["mean_turnaround_ms"], 2), "oom": e2e["oom"]}
+        if sa_e2e:
+            sv = n_total / (sa_e2e["ms_per_step"] / 1000.0)
+            line["e2e"]["sa_value"] = round(sv, 4)
+            line["e2e"]["speedup_vs_sa"] = round(line["e2e"]["value"] / sv, 3)
+    line["clocks"] = clk.summary()
+    if rank == 0:
+        rate, n, names, dt = cpu_sample(mix, args.cpu_budget)
+        line["cpu_baseline"] = {"value": round(rate, 4), "unit": UNIT, "cores": os.cpu_count() or 1,
+                                "kind": "port",
+                                "sample": f"{n} mix jobs ({', '.join(names)}) on the CPU restatements, "
+                                          f"{dt:.1f} s, OpenMP all host threads"}
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())
