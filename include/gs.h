@@ -209,6 +209,19 @@ int32_t gs_pending_count(gs_sched *s);
 int gs_sched_job_state(gs_sched *s, int32_t *sa_owner, int32_t *cg_counts,
                        int32_t *cg_cursor);
 
+/* ---- persistent decision kernel over a pinned host-mapped command ring --
+ * The paper's probe channel (probes and scheduler talk
+ * over shared memory) on B200: one resident decision warp polls the ring;
+ * submit / on_release / job_ended of this scheduler and the ledger ops of
+ * its devices become ring commands (no launch, no wait for a free SM).
+ * Capacities (pending queue, task handles, job handles) are fixed at start;
+ * the host must not write the ledgers while the ring runs.  An idle
+ * watchdog retires the kernel after 20 s; the next call relaunches it. */
+int gs_sched_ring_start(gs_sched *s, int32_t max_pending, int32_t max_handles, int32_t max_jobs);
+int gs_sched_ring_stop(gs_sched *s);
+/* Decisions served so far (kernel-launched commands + ring commands). */
+int64_t gs_engine_decisions(gs_engine *eng);
+
 /* ---- placement sweep (BASELINE cfg 4) -------------------------------- */
 /* Runs the whole synthetic stream on the GPU in one launch: for each probe
  * i: submit(i); then, if more than `max_resident` tasks are resident or the

@@ -116,6 +116,9 @@ SIGNATURES = {
     "gs_sched_job_state": (c_int32, [c_void_p, c_void_p, c_void_p, POINTER(c_int32)]),
     "gs_sweep": (c_int32, [c_void_p, c_void_p, c_int32, c_int32, c_void_p, c_int64,
                            POINTER(c_int64), POINTER(c_float)]),
+    "gs_sched_ring_start": (c_int32, [c_void_p, c_int32, c_int32, c_int32]),
+    "gs_sched_ring_stop": (c_int32, [c_void_p]),
+    "gs_engine_decisions": (c_int64, [c_void_p]),
 }
 
 _lib = None

@@ -314,6 +314,14 @@ int gs_exec_run(const gs_job_desc *jobs, int32_t n_jobs, int32_t policy, int32_t
   if (rc) return err(rc, gs_last_error());
   rc = gs_engine_reserve_handles(eng, n_jobs + 1);
   if (rc) return err(rc, gs_last_error());
+  // the resident decision warp serves every placement call of this run
+  // (GS_NO_RING=1 falls back to one decision launch per call, e.g. under
+  // ncu, which serializes kernels and would starve a persistent one)
+  const char *no_ring = getenv("GS_NO_RING");
+  if (!(no_ring && no_ring[0] == '1')) {
+    rc = gs_sched_ring_start(sched, n_jobs + 1, n_jobs + 1, n_jobs + 1);
+    if (rc) return err(rc, gs_last_error());
+  }
 
   memset(records, 0, sizeof(gs_job_record) * n_jobs);
   std::vector<int> admitted(n_jobs, -1);
@@ -451,9 +459,10 @@ int gs_exec_run(const gs_job_desc *jobs, int32_t n_jobs, int32_t policy, int32_t
       if (records[i].state == 2) stats->rejected++;
     }
     stats->kernel_launches = kernels.load();
-    stats->decision_launches = gs_engine_launches(eng);
+    stats->decision_launches = gs_engine_decisions(eng);
     stats->decision_ms = decision_ms;
   }
+  gs_sched_ring_stop(sched);
   gs_sched_destroy(sched);
   for (gs_device *d : ledgers) gs_device_destroy(d);
   gs_engine_close(eng);

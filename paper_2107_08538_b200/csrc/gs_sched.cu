@@ -36,6 +36,7 @@
 #include <stdio.h>
 #include <stdlib.h>
 #include <limits.h>
+#include <chrono>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -64,6 +65,7 @@ enum Op : int32_t {
   OP_TRY_PLACE = 15,
   OP_COMMIT = 16,
   OP_CHECK = 17,
+  OP_STOP = 99,
 };
 
 struct Cmd {
@@ -72,6 +74,21 @@ struct Cmd {
   gs_probe probe;
 };
 static_assert(sizeof(Cmd) == 96, "command record is 96 B");
+
+// Pinned host-mapped command ring of the persistent decision kernel
+// (single producer: the host, under the engine mutex; single consumer: the
+// decision warp).  tail / done are monotone command counters.
+constexpr int kRingSlots = 64;
+struct Ring {
+  long long tail;
+  long long pad0[7];
+  long long done;
+  long long pad1[7];
+  int32_t alive;
+  int32_t pad2[15];
+  Cmd cmds[kRingSlots];
+  gs_decision results[kRingSlots];
+};
 
 struct SchedState {  // pinned host-mapped
   int32_t sa_owner[GS_MAX_DEVICES];
@@ -118,6 +135,8 @@ struct KParams {
   int32_t *events;
   int64_t events_cap;
   const gs_probe *sweep_probes;
+  Ring *ring;
+  long long ring_idle_ns;
 };
 
 struct SLed {
@@ -908,6 +927,184 @@ __device__ Dec submit(const KParams &p, Smem &S, int *dyn, const gs_probe &pr, g
   return dc;
 }
 
+// One command of the interpreter (all lanes).
+__device__ void exec_cmd(const KParams &p, Smem &S, int *dyn, const Cmd &c, gs_decision *out, int lane) {
+  switch (c.op) {
+    case OP_SUBMIT:
+      submit(p, S, dyn, c.probe, out, lane);
+      break;
+    case OP_ON_RELEASE:
+      on_release(p, S, dyn, true, lane);
+      if (lane == 0) {
+        out->outcome = GS_OK;
+        out->free_mem_after = S.st.n_tried;
+        out->in_use_warps_after = S.st.n_admitted;
+      }
+      break;
+    case OP_JOB_ENDED:
+      // job_ended (schedulers.py:115-123)
+      if (lane == 0) {
+        for (int d = 0; d < p.n_dev; ++d)
+          if (S.st.sa_owner[d] == c.job) S.st.sa_owner[d] = -1;
+        if (p.policy == GS_POLICY_CG && c.job >= 0 && c.job < p.job_cap) {
+          const int d = p.claims[c.job];
+          if (d >= 0) {
+            S.st.cg_counts[d] -= 1;
+            p.claims[c.job] = -1;
+          }
+        }
+        out->outcome = GS_OK;
+      }
+      break;
+    case OP_RELEASE: {
+      long long freed = 0;
+      const int rc = warp_release(p.dev[c.dev], dyn, S, c.dev, c.handle, &freed, lane);
+      if (lane == 0) {
+        out->outcome = rc;
+        out->free_mem_after = freed;
+      }
+      break;
+    }
+    case OP_RESERVE:
+    case OP_ALLOC_RAW:
+      // reserve_memory (device_model.py:169-174) / allocate_raw (:185-190)
+      if (lane == 0) {
+        SLed &L = S.led[c.dev];
+        if (c.a > L.free_mem) {
+          out->outcome = GS_INFEASIBLE;
+        } else {
+          L.free_mem -= c.a;
+          L.version += 1;
+          L.dirty = 1;
+          if (c.a < 0) L.grow_epoch += 1;
+          if (c.op == OP_ALLOC_RAW) {
+            gs_residency *row = entry(p.dev[c.dev], c.handle);
+            row->mem_bytes += c.a;
+            L.held_mem += c.a;
+            L.version += 1;
+          }
+          out->outcome = GS_OK;
+        }
+      }
+      break;
+    case OP_ASSIGN:
+      if (lane == 0) {
+        SLed &L = S.led[c.dev];
+        gs_residency *row = entry(p.dev[c.dev], c.handle);
+        row->mem_bytes += c.a;
+        L.held_mem += c.a;
+        L.version += 1;
+        L.dirty = 1;
+        out->outcome = GS_OK;
+      }
+      break;
+    case OP_ADD_WARPS:
+      if (lane == 0) {
+        SLed &L = S.led[c.dev];
+        gs_residency *row = entry(p.dev[c.dev], c.handle);
+        row->warps += c.a;
+        L.in_use_warps += c.a;
+        L.held_warps += c.a;
+        L.version += 1;
+        L.dirty = 1;
+        out->outcome = GS_OK;
+      }
+      break;
+    case OP_TRY_PLACE: {
+      const Shape sh = shape_of(c.probe);
+      int *cap = dyn + p.scratch_off, *P = cap + p.max_sm_pad;
+      const int cur = warp_plan(p.dev[c.dev], dyn, S.led[c.dev], sh, cap, P, lane);
+      for (int s = lane; s < p.dev[c.dev].n_sm; s += 32) p.plan_io[s] = cur >= 0 ? P[s] : 0;
+      if (lane == 0) {
+        out->outcome = cur >= 0 ? GS_OK : GS_INFEASIBLE;
+        out->device = cur;
+        out->free_mem_after = S.led[c.dev].version;
+      }
+      break;
+    }
+    case OP_COMMIT: {
+      SLed &L = S.led[c.dev];
+      if (c.b != L.version) {
+        if (lane == 0) {
+          out->outcome = GS_ERR_CONTRACT;
+          out->free_mem_after = L.version;
+        }
+      } else {
+        const Shape sh = shape_of(c.probe);
+        warp_commit(p.dev[c.dev], dyn, L, c.handle, sh, p.plan_io, (int)c.a, lane);
+        if (lane == 0) {
+          out->outcome = GS_OK;
+          S.agg_ok[c.dev] = 0;  // arbitrary plans: stop trusting the bound
+        }
+      }
+      break;
+    }
+    case OP_CHECK: {
+      // check_conservation (device_model.py:220-245), first violation
+      const KDev &D = p.dev[c.dev];
+      const SLed &L = S.led[c.dev];
+      int k = GS_CHECK_OK, sm = -1;
+      if (L.free_mem < 0 || L.free_mem + L.held_mem != D.spec.mem_bytes) k = GS_CHECK_MEM;
+      else if (L.held_warps != L.in_use_warps) k = GS_CHECK_WARPS;
+      if (k == GS_CHECK_OK) {
+        int best = INT_MAX;
+        const int *w = arr(dyn, D, 0), *t = arr(dyn, D, 1), *r = arr(dyn, D, 2), *m = arr(dyn, D, 3);
+        for (int s = lane; s < D.n_sm && best == INT_MAX; s += 32) {
+          int kk = 0;
+          if (!(t[s] >= 0 && t[s] <= D.spec.max_tbs_per_sm)) kk = GS_CHECK_SM_TBS;
+          else if (!(w[s] >= 0 && w[s] <= D.spec.max_warps_per_sm)) kk = GS_CHECK_SM_WARPS;
+          else if (!(r[s] >= 0 && r[s] <= D.spec.regs_per_sm)) kk = GS_CHECK_SM_REGS;
+          else if (!(m[s] >= 0 && m[s] <= D.spec.smem_per_sm_bytes)) kk = GS_CHECK_SM_SMEM;
+          if (kk) best = s * 8 + kk;
+        }
+        best = __reduce_min_sync(kFull, best);
+        if (best != INT_MAX) {
+          k = best & 7;
+          sm = best >> 3;
+        }
+      }
+      if (lane == 0) {
+        out->outcome = k == GS_CHECK_OK ? GS_OK : GS_ERR_CONTRACT;
+        out->device = k;
+        out->pending_index = sm;
+        out->free_mem_after = L.held_mem;
+        out->in_use_warps_after = L.held_warps;
+      }
+      break;
+    }
+    default:
+      if (lane == 0) out->outcome = GS_ERR_CONFIG;
+      break;
+  }
+  __syncwarp();
+}
+
+// Write dirty ledgers and the scheduler state back to mapped memory.
+__device__ void writeback(const KParams &p, int *dyn, Smem &S, int lane) {
+  led_to_stage(p, dyn, S, lane);
+  stage(p, dyn, S, false, lane);
+  const int nw = sizeof(SchedState) / 4;
+  for (int i = lane; i < nw; i += 32)
+    reinterpret_cast<int32_t *>(p.st)[i] = reinterpret_cast<const int32_t *>(&S.st)[i];
+  if (lane < p.n_dev) S.led[lane].dirty = 0;
+  __threadfence_system();
+  __syncwarp();
+}
+
+__device__ __forceinline__ long long ld_acquire_sys(const long long *a) {
+  long long v;
+  asm volatile("ld.acquire.sys.global.b64 %0, [%1];" : "=l"(v) : "l"(a) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_sys(long long *a, long long v) {
+  asm volatile("st.release.sys.global.b64 [%0], %1;" ::"l"(a), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
 __global__ void __launch_bounds__(kThreads, 1) gs_interp_kernel(KParams p) {
   extern __shared__ __align__(16) int dyn[];
   __shared__ Smem S;
@@ -942,173 +1139,58 @@ __global__ void __launch_bounds__(kThreads, 1) gs_interp_kernel(KParams p) {
       }
       if (S.st.error) break;
     }
+  } else if (p.ring) {
+    // Persistent mode: poll the pinned host-mapped command ring; ledgers
+    // stay in shared memory between commands, dirty ones are written back
+    // after every command so host reads stay current.
+    Ring *ring = p.ring;
+    long long processed = ring->done;
+    for (;;) {
+      long long t = 0;
+      if (lane == 0) {
+        const unsigned long long t0 = globaltimer();
+        while ((t = ld_acquire_sys(&ring->tail)) <= processed) {
+          __nanosleep(256);
+          if (globaltimer() - t0 > (unsigned long long)p.ring_idle_ns) {
+            t = -1;
+            break;
+          }
+        }
+      }
+      t = __shfl_sync(kFull, t, 0);
+      if (t < 0) break;  // idle watchdog: the host relaunches on demand
+      const int slot = (int)(processed % kRingSlots);
+      if (lane < (int)(sizeof(Cmd) / 4))
+        reinterpret_cast<int32_t *>(&S.cmd)[lane] =
+            reinterpret_cast<const volatile int32_t *>(ring->cmds + slot)[lane];
+      __syncwarp();
+      if (S.cmd.op == OP_STOP) {
+        processed++;
+        break;
+      }
+      exec_cmd(p, S, dyn, S.cmd, ring->results + slot, lane);
+      writeback(p, dyn, S, lane);
+      processed++;
+      if (lane == 0) st_release_sys(&ring->done, processed);
+      __syncwarp();
+    }
+    writeback(p, dyn, S, lane);
+    if (lane == 0) {
+      ring->alive = 0;
+      st_release_sys(&ring->done, processed);
+    }
+    return;
   } else {
     for (int ci = 0; ci < p.n_cmds; ++ci) {
       if (lane < (int)(sizeof(Cmd) / 4))
         reinterpret_cast<int32_t *>(&S.cmd)[lane] = reinterpret_cast<const int32_t *>(p.cmds + ci)[lane];
       __syncwarp();
-      const Cmd &c = S.cmd;
-      gs_decision *out = p.results + ci;
-      switch (c.op) {
-        case OP_SUBMIT:
-          submit(p, S, dyn, c.probe, out, lane);
-          break;
-        case OP_ON_RELEASE:
-          on_release(p, S, dyn, true, lane);
-          if (lane == 0) {
-            out->outcome = GS_OK;
-            out->free_mem_after = S.st.n_tried;
-            out->in_use_warps_after = S.st.n_admitted;
-          }
-          break;
-        case OP_JOB_ENDED:
-          // job_ended (schedulers.py:115-123)
-          if (lane == 0) {
-            for (int d = 0; d < p.n_dev; ++d)
-              if (S.st.sa_owner[d] == c.job) S.st.sa_owner[d] = -1;
-            if (p.policy == GS_POLICY_CG && c.job >= 0 && c.job < p.job_cap) {
-              const int d = p.claims[c.job];
-              if (d >= 0) {
-                S.st.cg_counts[d] -= 1;
-                p.claims[c.job] = -1;
-              }
-            }
-            out->outcome = GS_OK;
-          }
-          break;
-        case OP_RELEASE: {
-          long long freed = 0;
-          const int rc = warp_release(p.dev[c.dev], dyn, S, c.dev, c.handle, &freed, lane);
-          if (lane == 0) {
-            out->outcome = rc;
-            out->free_mem_after = freed;
-          }
-          break;
-        }
-        case OP_RESERVE:
-        case OP_ALLOC_RAW:
-          // reserve_memory (device_model.py:169-174) / allocate_raw (:185-190)
-          if (lane == 0) {
-            SLed &L = S.led[c.dev];
-            if (c.a > L.free_mem) {
-              out->outcome = GS_INFEASIBLE;
-            } else {
-              L.free_mem -= c.a;
-              L.version += 1;
-              L.dirty = 1;
-              if (c.a < 0) L.grow_epoch += 1;
-              if (c.op == OP_ALLOC_RAW) {
-                gs_residency *row = entry(p.dev[c.dev], c.handle);
-                row->mem_bytes += c.a;
-                L.held_mem += c.a;
-                L.version += 1;
-              }
-              out->outcome = GS_OK;
-            }
-          }
-          break;
-        case OP_ASSIGN:
-          if (lane == 0) {
-            SLed &L = S.led[c.dev];
-            gs_residency *row = entry(p.dev[c.dev], c.handle);
-            row->mem_bytes += c.a;
-            L.held_mem += c.a;
-            L.version += 1;
-            L.dirty = 1;
-            out->outcome = GS_OK;
-          }
-          break;
-        case OP_ADD_WARPS:
-          if (lane == 0) {
-            SLed &L = S.led[c.dev];
-            gs_residency *row = entry(p.dev[c.dev], c.handle);
-            row->warps += c.a;
-            L.in_use_warps += c.a;
-            L.held_warps += c.a;
-            L.version += 1;
-            L.dirty = 1;
-            out->outcome = GS_OK;
-          }
-          break;
-        case OP_TRY_PLACE: {
-          const Shape sh = shape_of(c.probe);
-          int *cap = dyn + p.scratch_off, *P = cap + p.max_sm_pad;
-          const int cur = warp_plan(p.dev[c.dev], dyn, S.led[c.dev], sh, cap, P, lane);
-          for (int s = lane; s < p.dev[c.dev].n_sm; s += 32) p.plan_io[s] = cur >= 0 ? P[s] : 0;
-          if (lane == 0) {
-            out->outcome = cur >= 0 ? GS_OK : GS_INFEASIBLE;
-            out->device = cur;
-            out->free_mem_after = S.led[c.dev].version;
-          }
-          break;
-        }
-        case OP_COMMIT: {
-          SLed &L = S.led[c.dev];
-          if (c.b != L.version) {
-            if (lane == 0) {
-              out->outcome = GS_ERR_CONTRACT;
-              out->free_mem_after = L.version;
-            }
-          } else {
-            const Shape sh = shape_of(c.probe);
-            warp_commit(p.dev[c.dev], dyn, L, c.handle, sh, p.plan_io, (int)c.a, lane);
-            if (lane == 0) {
-              out->outcome = GS_OK;
-              S.agg_ok[c.dev] = 0;  // arbitrary plans: stop trusting the bound
-            }
-          }
-          break;
-        }
-        case OP_CHECK: {
-          // check_conservation (device_model.py:220-245), first violation
-          const KDev &D = p.dev[c.dev];
-          const SLed &L = S.led[c.dev];
-          int k = GS_CHECK_OK, sm = -1;
-          if (L.free_mem < 0 || L.free_mem + L.held_mem != D.spec.mem_bytes) k = GS_CHECK_MEM;
-          else if (L.held_warps != L.in_use_warps) k = GS_CHECK_WARPS;
-          if (k == GS_CHECK_OK) {
-            int best = INT_MAX;
-            const int *w = arr(dyn, D, 0), *t = arr(dyn, D, 1), *r = arr(dyn, D, 2), *m = arr(dyn, D, 3);
-            for (int s = lane; s < D.n_sm && best == INT_MAX; s += 32) {
-              int kk = 0;
-              if (!(t[s] >= 0 && t[s] <= D.spec.max_tbs_per_sm)) kk = GS_CHECK_SM_TBS;
-              else if (!(w[s] >= 0 && w[s] <= D.spec.max_warps_per_sm)) kk = GS_CHECK_SM_WARPS;
-              else if (!(r[s] >= 0 && r[s] <= D.spec.regs_per_sm)) kk = GS_CHECK_SM_REGS;
-              else if (!(m[s] >= 0 && m[s] <= D.spec.smem_per_sm_bytes)) kk = GS_CHECK_SM_SMEM;
-              if (kk) best = s * 8 + kk;
-            }
-            best = __reduce_min_sync(kFull, best);
-            if (best != INT_MAX) {
-              k = best & 7;
-              sm = best >> 3;
-            }
-          }
-          if (lane == 0) {
-            out->outcome = k == GS_CHECK_OK ? GS_OK : GS_ERR_CONTRACT;
-            out->device = k;
-            out->pending_index = sm;
-            out->free_mem_after = L.held_mem;
-            out->in_use_warps_after = L.held_warps;
-          }
-          break;
-        }
-        default:
-          if (lane == 0) out->outcome = GS_ERR_CONFIG;
-          break;
-      }
-      __syncwarp();
+      exec_cmd(p, S, dyn, S.cmd, p.results + ci, lane);
     }
   }
 
   // ---- write back dirty ledgers + scheduler state ----
-  led_to_stage(p, dyn, S, lane);
-  stage(p, dyn, S, false, lane);
-  {
-    const int nw = sizeof(SchedState) / 4;
-    for (int i = lane; i < nw; i += 32)
-      reinterpret_cast<int32_t *>(p.st)[i] = reinterpret_cast<const int32_t *>(&S.st)[i];
-  }
-  __threadfence_system();
+  writeback(p, dyn, S, lane);
 }
 
 // ---------------------------------------------------------------------------
@@ -1197,6 +1279,8 @@ struct gs_engine {
   Mapped<SchedState> dummy_state;
   DevBuf<Cmd> dcmds;
   int64_t launches = 0;
+  int64_t decisions = 0;
+  int rings_active = 0;
   int max_smem = 0;
 };
 
@@ -1208,6 +1292,8 @@ struct gs_device {
   int32_t stride = 0;
   Mapped<char> ledger;  // header + 4 arrays
   DevBuf<int32_t> res;
+  gs_sched *ring_owner = nullptr;  // scheduler whose persistent kernel owns this ledger
+  int32_t ring_index = -1;
 };
 
 struct gs_sched {
@@ -1219,6 +1305,12 @@ struct gs_sched {
   DevBuf<int32_t> claims;
   DevBuf<int32_t> events;
   Mapped<gs_decision> drain;
+  // persistent decision kernel (command ring)
+  Mapped<Ring> ring;
+  bool ring_active = false;
+  cudaStream_t ring_stream = nullptr;
+  size_t ring_smem = 0;
+  KParams ring_params{};
 };
 
 namespace {
@@ -1301,6 +1393,60 @@ int launch(gs_engine *eng, Launch &L) {
   return GS_OK;
 }
 
+// ---- command ring (persistent decision kernel) ----------------------------
+
+int ring_launch(gs_sched *s) {
+  Ring *r = s->ring.h;
+  r->alive = 1;
+  __atomic_thread_fence(__ATOMIC_SEQ_CST);
+  KParams p = s->ring_params;
+  p.ring = s->ring.d;
+  gs_interp_kernel<<<1, kThreads, s->ring_smem, s->ring_stream>>>(p);
+  CU(cudaGetLastError());
+  s->eng->launches++;
+  return GS_OK;
+}
+
+// Push n commands (in order) and wait for their results.  Caller holds the
+// engine lock.
+int ring_call(gs_sched *s, const Cmd *cmds, int n, gs_decision *results) {
+  Ring *r = s->ring.h;
+  for (int base = 0; base < n; base += kRingSlots) {
+    const int m = std::min(n - base, kRingSlots);
+    if (!__atomic_load_n(&r->alive, __ATOMIC_ACQUIRE)) {
+      // the idle watchdog retired the kernel: ledgers were written back,
+      // relaunch it (it restages from mapped memory)
+      CU(cudaStreamSynchronize(s->ring_stream));
+      int rc = ring_launch(s);
+      if (rc) return rc;
+    }
+    long long t = __atomic_load_n(&r->tail, __ATOMIC_RELAXED);
+    for (int k = 0; k < m; ++k) {
+      Cmd &dst = r->cmds[(t + k) % kRingSlots];
+      dst = cmds[base + k];
+    }
+    __atomic_store_n(&r->tail, t + m, __ATOMIC_RELEASE);
+    const auto t0 = std::chrono::steady_clock::now();
+    while (__atomic_load_n(&r->done, __ATOMIC_ACQUIRE) < t + m) {
+#if defined(__x86_64__)
+      __builtin_ia32_pause();
+#endif
+      if (!__atomic_load_n(&r->alive, __ATOMIC_ACQUIRE) &&
+          __atomic_load_n(&r->done, __ATOMIC_ACQUIRE) < t + m) {
+        // retired between our check and the push: relaunch, it resumes at done
+        CU(cudaStreamSynchronize(s->ring_stream));
+        int rc = ring_launch(s);
+        if (rc) return rc;
+      }
+      if (std::chrono::steady_clock::now() - t0 > std::chrono::seconds(30))
+        return set_err(GS_ERR_CUDA, "decision ring did not answer within 30 s");
+    }
+    for (int k = 0; k < m; ++k) results[base + k] = r->results[(t + k) % kRingSlots];
+    s->eng->decisions += m;
+  }
+  return GS_OK;
+}
+
 int ensure_cmds(gs_engine *eng, int n) {
   if ((size_t)n > eng->cmds.n) {
     int rc = eng->cmds.alloc(std::max<size_t>(n, eng->cmds.n * 2));
@@ -1317,6 +1463,12 @@ int ensure_cmds(gs_engine *eng, int n) {
 int run_device_cmd(gs_device *dv, const Cmd &c, gs_decision *out) {
   gs_engine *eng = dv->eng;
   EngineLock g(eng);
+  if (dv->ring_owner && dv->ring_owner->ring_active) {
+    Cmd rc = c;
+    rc.dev = dv->ring_index;
+    return ring_call(dv->ring_owner, &rc, 1, out);
+  }
+  eng->decisions++;
   Launch L;
   gs_device *arr[1] = {dv};
   int rc = build_params(eng, arr, 1, L);
@@ -1354,6 +1506,11 @@ int sched_params(gs_sched *s, Launch &L) {
 
 int ensure_pending(gs_sched *s, int extra) {
   const size_t need = (size_t)s->st.h->pend_count + extra + 1;
+  if (s->ring_active) {
+    if (need > s->pend.n || need > s->drain.n)
+      return set_err(GS_ERR_NOMEM, "pending queue capacity reserved at ring start exceeded");
+    return GS_OK;
+  }
   int rc = s->pend.ensure(need, s->eng->stream, true);
   if (rc) return rc;
   if (need > s->drain.n) {
@@ -1367,6 +1524,7 @@ int ensure_jobs(gs_sched *s, int32_t job) {
   if (job < 0) return GS_OK;
   size_t old = s->claims.n;
   if ((size_t)job < old) return GS_OK;
+  if (s->ring_active) return set_err(GS_ERR_NOMEM, "job capacity reserved at ring start exceeded");
   size_t nn = std::max<size_t>((size_t)job + 1, old * 2);
   int32_t *nd = nullptr;
   CU(cudaMalloc((void **)&nd, nn * sizeof(int32_t)));
@@ -1444,6 +1602,7 @@ void gs_engine_close(gs_engine *eng) {
 int gs_engine_reserve_handles(gs_engine *eng, int32_t capacity) {
   EngineLock g(eng);
   if (capacity <= eng->res_cap) return GS_OK;
+  if (eng->rings_active) return set_err(GS_ERR_NOMEM, "handle capacity reserved at ring start exceeded");
   int32_t cap = std::max(capacity, eng->res_cap * 2);
   for (gs_device *dv : eng->devices) {
     int rc = grow_device_res(dv, cap);
@@ -1636,6 +1795,7 @@ int gs_sched_create(gs_engine *eng, gs_device *const *devices, int32_t n, int32_
 
 void gs_sched_destroy(gs_sched *s) {
   if (!s) return;
+  gs_sched_ring_stop(s);
   EngineLock g(s->eng);
   s->st.release();
   s->drain.release();
@@ -1671,6 +1831,13 @@ int gs_submit_batch(gs_sched *s, const gs_probe *reqs, int32_t n, gs_decision *o
     c.job = reqs[i].job;
     c.probe = reqs[i];
   }
+  eng->decisions += s->ring_active ? 0 : n;
+  if (s->ring_active) {
+    rc = ring_call(s, eng->cmds.h, n, eng->results.h);
+    if (rc) return rc;
+    if (out) memcpy(out, eng->results.h, sizeof(gs_decision) * n);
+    return GS_OK;
+  }
   if (n > 32) {
     rc = eng->dcmds.ensure(n, eng->stream, false);
     if (rc) return rc;
@@ -1701,9 +1868,14 @@ int gs_on_release(gs_sched *s, gs_decision *out, int32_t out_cap, int32_t *n_tri
   Cmd &c = eng->cmds.h[0];
   memset(&c, 0, sizeof c);
   c.op = OP_ON_RELEASE;
-  L.p.cmds = eng->cmds.d;
-  L.p.n_cmds = 1;
-  rc = launch(eng, L);
+  if (s->ring_active) {
+    rc = ring_call(s, &c, 1, eng->results.h);
+  } else {
+    eng->decisions++;
+    L.p.cmds = eng->cmds.d;
+    L.p.n_cmds = 1;
+    rc = launch(eng, L);
+  }
   if (rc) return rc;
   const int tried = s->st.h->n_tried, adm = s->st.h->n_admitted;
   if (n_tried) *n_tried = tried;
@@ -1725,10 +1897,74 @@ int gs_job_ended(gs_sched *s, int32_t job) {
   memset(&c, 0, sizeof c);
   c.op = OP_JOB_ENDED;
   c.job = job;
+  if (s->ring_active) return ring_call(s, &c, 1, eng->results.h);
+  eng->decisions++;
   L.p.cmds = eng->cmds.d;
   L.p.n_cmds = 1;
   return launch(eng, L);
 }
+
+int gs_sched_ring_start(gs_sched *s, int32_t max_pending, int32_t max_handles, int32_t max_jobs) {
+  gs_engine *eng = s->eng;
+  EngineLock g(eng);
+  if (s->ring_active) return GS_OK;
+  for (gs_device *dv : s->devs)
+    if (dv->ring_owner) return set_err(GS_ERR_CONTRACT, "a device of this fleet is owned by another ring");
+  int rc = gs_engine_reserve_handles(eng, std::max(max_handles, 1));
+  if (!rc) rc = ensure_jobs(s, std::max(max_jobs, 1));
+  if (!rc) rc = ensure_pending(s, std::max(max_pending, 1));
+  if (!rc) rc = ensure_cmds(eng, kRingSlots);
+  if (!rc && !s->ring.h) rc = s->ring.alloc(1);
+  if (rc) return rc;
+  Launch L;
+  rc = sched_params(s, L);
+  if (rc) return rc;
+  s->ring_params = L.p;
+  s->ring_params.ring_idle_ns = 20LL * 1000 * 1000 * 1000;  // idle watchdog: 20 s
+  s->ring_smem = L.smem;
+  if (!s->ring_stream) {
+    int lo = 0, hi = 0;
+    CU(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    CU(cudaStreamCreateWithPriority(&s->ring_stream, cudaStreamNonBlocking, hi));
+  }
+  memset(s->ring.h, 0, sizeof(Ring));
+  rc = ring_launch(s);
+  if (rc) return rc;
+  s->ring_active = true;
+  eng->rings_active++;
+  for (size_t d = 0; d < s->devs.size(); ++d) {
+    s->devs[d]->ring_owner = s;
+    s->devs[d]->ring_index = (int32_t)d;
+  }
+  return GS_OK;
+}
+
+int gs_sched_ring_stop(gs_sched *s) {
+  gs_engine *eng = s->eng;
+  EngineLock g(eng);
+  if (!s->ring_active) return GS_OK;
+  Ring *r = s->ring.h;
+  int rc = GS_OK;
+  if (__atomic_load_n(&r->alive, __ATOMIC_ACQUIRE)) {
+    Cmd stop;
+    memset(&stop, 0, sizeof stop);
+    stop.op = OP_STOP;
+    const long long t = __atomic_load_n(&r->tail, __ATOMIC_RELAXED);
+    r->cmds[t % kRingSlots] = stop;
+    __atomic_store_n(&r->tail, t + 1, __ATOMIC_RELEASE);
+  }
+  cudaError_t e = cudaStreamSynchronize(s->ring_stream);
+  if (e != cudaSuccess) rc = set_err(GS_ERR_CUDA, cudaGetErrorString(e));
+  s->ring_active = false;
+  eng->rings_active--;
+  for (gs_device *dv : s->devs) {
+    dv->ring_owner = nullptr;
+    dv->ring_index = -1;
+  }
+  return rc;
+}
+
+int64_t gs_engine_decisions(gs_engine *eng) { return eng->decisions; }
 
 int32_t gs_pending_count(gs_sched *s) { return s->st.h->pend_count; }
 
@@ -1747,6 +1983,7 @@ int gs_sweep(gs_sched *s, const gs_probe *probes, int32_t n, int32_t max_residen
   gs_engine *eng = s->eng;
   EngineLock g(eng);
   if (n <= 0) return GS_OK;
+  if (s->ring_active) return set_err(GS_ERR_CONTRACT, "stop the decision ring before a sweep");
   if (s->st.h->pend_count != 0 || s->st.h->fifo_tail != s->st.h->fifo_head)
     return set_err(GS_ERR_CONTRACT, "sweep needs a fresh scheduler");
   int rc = gs_engine_reserve_handles(eng, n);

@@ -119,6 +119,17 @@ class Scheduler:
 
         self._finalizer = weakref.finalize(self, _destroy_sched, self._lib, ptr)
 
+    # -- persistent decision kernel ---------------------------------------------
+
+    def start_ring(self, max_pending: int = 4096, max_handles: int = 4096, max_jobs: int = 4096) -> None:
+        """Serve this scheduler's calls from a resident decision warp over a
+        pinned host-mapped command ring (include/gs.h gs_sched_ring_start).
+        While it runs, ledgers must only change through the API."""
+        nat.check(self._lib.gs_sched_ring_start(self._ptr, max_pending, max_handles, max_jobs))
+
+    def stop_ring(self) -> None:
+        nat.check(self._lib.gs_sched_ring_stop(self._ptr))
+
     # -- job-granular state mirrors ------------------------------------------
 
     def _job_state(self):

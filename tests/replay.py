@@ -68,13 +68,14 @@ class _Res:
 class DropinBackend:
     """Drives the product's public drop-in API (GPU)."""
 
-    def __init__(self):
+    def __init__(self, ring: bool = False):
         from paper_2107_08538_b200 import gpushare as G
 
         self.G = G
         self.devs = []
         self.sched = None
         self.log = None
+        self.ring = ring
 
     def dev(self, spec, index):
         self.devs.append(self.G.DeviceState(self.G.DeviceSpec(*spec), index))
@@ -83,6 +84,12 @@ class DropinBackend:
         self.log = [] if log else None
         pol = self.G.PolicyConfig(policy, cg)
         self.sched = self.G.Scheduler([self.devs[k] for k in devs], pol, skip_ahead=skip, log=self.log)
+        if self.ring:
+            self.sched.start_ring()
+
+    def close(self):
+        if self.ring and self.sched is not None:
+            self.sched.stop_ring()
 
     def submit(self, job, uid, res, level, t, now):
         n0 = len(self.log) if self.log is not None else 0

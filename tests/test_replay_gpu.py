@@ -76,3 +76,17 @@ def test_gpu_sweep_matches_oracle_at_scale(n, policy):
     oev = O.OracleScheduler(devs, 2 if policy == "mgb-sm" else 3, 6, True).sweep(probes, 32)
     np.testing.assert_array_equal(ev, oev)
     np.testing.assert_array_equal(final, np.array([d.snapshot() for d in devs], dtype=np.int64))
+
+
+@pytest.mark.parametrize("chunk", range(4))
+def test_ring_mode_replays_reference_streams(chunk):
+    """The same golden streams served by the persistent decision kernel
+    over the host-mapped command ring."""
+    n = 0
+    for run in RUNS[chunk::16]:
+        be = DropinBackend(ring=True)
+        try:
+            n += replay_run(be, run)
+        finally:
+            be.close()
+    assert n > 0

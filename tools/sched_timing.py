@@ -93,5 +93,38 @@ def main():
         print(json.dumps({"what": "sync_dropin_per_probe_us", "policy": policy, "us": round(us, 2)}), flush=True)
 
 
-if __name__ == "__main__":
+if __name__ == "__main__" and "--ring" not in sys.argv:
     main()
+
+
+def ring_latency(policy="mgb-warps", n=3000):
+    spec = device_spec("b200")
+    devs = [DeviceState(spec, i) for i in range(8)]
+    sched = Scheduler(devs, parse_policy(policy))
+    sched.start_ring(max_pending=n + 1, max_handles=n + 1, max_jobs=8)
+    probes = gen_probes(n, seed=3)
+    reqs = [ScheduleRequest("j", f"p{i}", ResourceRequest(int(p["mem_bytes"]), 0, int(p["thread_blocks"]),
+                                                          int(p["warps_per_block"]), int(p["total_warps"]),
+                                                          int(p["threads_per_block"]), int(p["regs_per_thread"]),
+                                                          int(p["smem_per_block"]), 1.0), "task", 0.0)
+            for i, p in enumerate(probes)]
+    fifo = []
+    t = time.perf_counter()
+    for r in reqs:
+        d = sched.submit(r, 0.0)
+        if d.outcome == "assign":
+            fifo.append((d.device, r.task_uid))
+        if len(fifo) > 32 or sched.pending:
+            if fifo:
+                dv, u = fifo.pop(0)
+                devs[dv].release_task(u)
+            for q, dv in sched.on_release(0.0):
+                fifo.append((dv, q.task_uid))
+    us = (time.perf_counter() - t) / n * 1e6
+    sched.stop_ring()
+    return us
+
+
+if __name__ == "__main__" and "--ring" in sys.argv:
+    for pol in ("mgb-warps", "mgb-sm"):
+        print(json.dumps({"what": "sync_dropin_ring_per_probe_us", "policy": pol, "us": round(ring_latency(pol), 2)}))
