@@ -31,7 +31,7 @@ extern "C" {
 #define GS_JOB_BACKPROP 4
 #define GS_JOB_NEEDLE 5
 #define GS_JOB_LUD 6
-#define GS_JOB_GEMM 7      /* Darknet-style connected / conv layer stack (bf16, tcgen05) */
+#define GS_JOB_YOLO 7      /* Darknet YOLOv3-tiny inference (bf16 im2col + tcgen05 GEMM) */
 #define GS_JOB_KINDS 8
 
 /* executor modes */
@@ -40,9 +40,9 @@ extern "C" {
 
 typedef struct gs_job_desc {
     int32_t kind;
-    int32_t iters;        /* iterations (hotspot/srad/kmeans), layers (gemm) */
-    int64_t n;            /* problem size: nodes / grid edge / points / inputs / matrix edge */
-    int64_t m;            /* secondary size: features (kmeans), hidden (backprop), batch (gemm) */
+    int32_t iters;        /* iterations (hotspot/srad/kmeans/backprop), forward passes (yolo) */
+    int64_t n;            /* problem size: nodes / grid edge / points / inputs / matrix edge / image edge */
+    int64_t m;            /* secondary size: features (kmeans), hidden (backprop), batch (yolo) */
     uint64_t seed;
 } gs_job_desc;
 
@@ -93,6 +93,13 @@ int gs_exec_run(const gs_job_desc *jobs, int32_t n_jobs, int32_t policy, int32_t
 
 /* Prepare (generate) the inputs of a job list ahead of gs_exec_run so the
  * timed region starts with inputs resident (device) or pinned (e2e). */
+/* Darknet layer GEMM on tcgen05 (csrc/gs_gemm.cu): D = act(A . B^T + bias)
+ * with A [m x k] and B [n x k] bf16 row-major (K contiguous, k % 8 == 0),
+ * bias fp32 [n] or NULL, D [m x n] bf16 or fp32 (out_f32) with row pitch ldo,
+ * act 0 linear / 1 leaky-ReLU 0.1.  Device pointers; stream may be NULL. */
+int gs_gemm_bf16(const void *A, int64_t lda, const void *B, int64_t ldb, const float *bias, void *out,
+                 int64_t ldo, int32_t m, int32_t n, int32_t k, int32_t out_f32, int32_t act, void *stream);
+
 int gs_exec_stage(const gs_job_desc *jobs, int32_t n_jobs, const int32_t *cuda_devices, int32_t n_devices,
                   int32_t mode);
 void gs_exec_unstage(void);

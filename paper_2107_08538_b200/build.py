@@ -30,6 +30,7 @@ SOURCES = {
     "gs_work.cu": ["-fmad=false"],
     "gs_exec.cu": [],
     "gs_gemm.cu": [],
+    "gs_darknet.cu": [],
 }
 TARGET = os.path.join(PKG, "libgs.so")
 

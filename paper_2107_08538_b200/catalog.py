@@ -81,12 +81,12 @@ def host_footprint(job: Job) -> int:
     g = 2 << 20
     n, m = job.n, job.m
     sizes = {
-        "bfs": [(n + 1) * 4, n * 24, n * 4, n * 4, n * 4, 16],
+        "bfs": [(n + 1) * 4, n * 24, n * 4, n * 4, n * 4, 16, (n // 32 + 1) * 4],
         "hotspot": [n * n * 4] * 3,
         "srad": [n * n * 4] * 3 + [16],
         "kmeans": [n * m * 4, n * 4, 5 * m * 4, 5 * m * 8, 40],
         "backprop": [(n + 1) * 4, m * (n + 1) * 4, m * (n + 1) * 4, 320, 148 * 8 * 16 * 8],
-        "needle": [(n + 1) * (n + 1) * 4] * 2,
+        "needle": [(n + 1) * (n + 1) * 4] * 2 + [(n // 32 + 1) * 4],
         "lud": [n * n * 4],
     }[job.kind]
     return (8 << 20) + sum((s + g - 1) // g * g for s in sizes)

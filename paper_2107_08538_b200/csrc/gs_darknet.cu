@@ -1,0 +1,364 @@
+// gs_darknet.cu — Darknet-style inference jobs: YOLOv3-tiny on B200.
+//
+// The reference's neural catalog (gpushare/data/neural_catalog.json:6-57)
+// stands Darknet jobs in as footprints + durations; BASELINE cfg 2 names
+// YOLOv3-tiny (random init, batch 1-64).  This is that network, layer for
+// layer as Darknet's yolov3-tiny.cfg defines it (13 convolutions with folded
+// batch-norm + leaky ReLU, 6 max-pools, a route / upsample / concat to the
+// second head, two 255-channel YOLO heads), run Darknet's way: every
+// convolution is im2col + GEMM, and every layer keeps its own resident
+// output buffer (Darknet's l.output), so a job's footprint is the sum of its
+// activations — which is what makes large batches exercise memory-safe
+// placement.
+//
+// Layout is NHWC bf16 (a 3x3 tap's channels are contiguous, so im2row moves
+// 16-byte vectors); the GEMM is the tcgen05 kernel of gs_gemm.cu with the
+// bias + leaky (or YOLO logistic) epilogue fused; route/concat is free (the
+// producing GEMM writes into a channel slice of the concat tensor) and the
+// 2x upsample writes straight into its slice.
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+
+#include <algorithm>
+#include <string>
+#include <vector>
+
+#include "../../include/gs_work.h"
+#include "gs_work_internal.h"
+
+namespace gsw {
+
+namespace {
+
+constexpr int kThr = 256;
+enum LType { CONV = 0, MAXPOOL = 1, UPSAMPLE = 2 };
+
+// A tensor view: NHWC with a per-pixel pitch and a channel offset inside buffer `buf`.
+struct TView {
+  int buf;
+  int64_t off;  // element offset (channel offset)
+  int n, h, w, c, pitch;
+  bool f32;
+};
+
+struct LPlan {
+  int type;
+  TView in, out;
+  int k, stride, cout, act;  // act: 0 linear, 1 leaky, 2 yolo
+  int kdim, kpad;            // im2row width (k*k*cin) and its 8-aligned pitch
+  int64_t woff, boff;        // weight (bf16 elements) / bias (floats) offsets
+};
+
+struct NetPlan {
+  std::vector<Buf> bufs;
+  std::vector<LPlan> layers;
+  int out_buf = 3;
+  int64_t flops = 0;
+};
+
+constexpr int B_IMG = 0, B_W = 1, B_BIAS = 2, B_DET = 3, B_WS = 4;
+
+int64_t elems(const TView &v) { return (int64_t)v.n * v.h * v.w * v.pitch; }
+
+NetPlan yolo_plan(const gs_job_desc &j) {
+  NetPlan P;
+  const int S = (int)j.n, N = (int)j.m;
+  P.bufs.resize(5);
+  P.bufs[B_IMG] = {(int64_t)N * S * S * 3 * 2, IN};
+  int64_t wcount = 0, bcount = 0;
+  auto new_act = [&](int h, int w, int c, bool f32 = false) {
+    TView v{(int)P.bufs.size(), 0, N, h, w, c, c, f32};
+    P.bufs.push_back({elems(v) * (f32 ? 4 : 2), WRK});
+    return v;
+  };
+  int64_t ws = 0;
+  auto conv = [&](const TView &in, TView out, int k, int cout, int act) {
+    LPlan L{};
+    L.type = CONV;
+    L.in = in;
+    L.out = out;
+    L.k = k;
+    L.stride = 1;
+    L.cout = cout;
+    L.act = act;
+    L.kdim = k * k * in.c;
+    L.kpad = (L.kdim + 7) / 8 * 8;
+    L.woff = wcount;
+    L.boff = bcount;
+    wcount += (int64_t)cout * L.kpad;
+    wcount = (wcount + 7) / 8 * 8;  // 16-byte aligned next layer
+    bcount += cout;
+    const int64_t pix = (int64_t)in.n * in.h * in.w;
+    if (!(k == 1 && in.pitch % 8 == 0 && in.off % 8 == 0)) ws = std::max(ws, pix * L.kpad * 2);
+    P.flops += 2 * pix * (int64_t)L.kdim * cout;
+    P.layers.push_back(L);
+    return out;
+  };
+  auto pool = [&](const TView &in, int stride) {
+    const int ho = stride == 2 ? in.h / 2 : in.h, wo = stride == 2 ? in.w / 2 : in.w;
+    TView out = new_act(ho, wo, in.c);
+    LPlan L{};
+    L.type = MAXPOOL;
+    L.in = in;
+    L.out = out;
+    L.k = 2;
+    L.stride = stride;
+    P.layers.push_back(L);
+    return out;
+  };
+  TView x{B_IMG, 0, N, S, S, 3, 3, false};
+  // yolov3-tiny.cfg
+  x = conv(x, new_act(S, S, 16), 3, 16, 1);                      // 0
+  x = pool(x, 2);                                                // 1
+  x = conv(x, new_act(S / 2, S / 2, 32), 3, 32, 1);              // 2
+  x = pool(x, 2);                                                // 3
+  x = conv(x, new_act(S / 4, S / 4, 64), 3, 64, 1);              // 4
+  x = pool(x, 2);                                                // 5
+  x = conv(x, new_act(S / 8, S / 8, 128), 3, 128, 1);            // 6
+  x = pool(x, 2);                                                // 7
+  // route target: [upsampled layer 18 (128) | layer 8 (256)] at S/16
+  TView cat = new_act(S / 16, S / 16, 384);
+  TView l8 = cat;
+  l8.off = 128;
+  l8.c = 256;
+  x = conv(x, l8, 3, 256, 1);                                    // 8 -> concat[128:384]
+  x = pool(x, 2);                                                // 9
+  x = conv(x, new_act(S / 32, S / 32, 512), 3, 512, 1);          // 10
+  x = pool(x, 1);                                                // 11 (size 2, stride 1)
+  x = conv(x, new_act(S / 32, S / 32, 1024), 3, 1024, 1);        // 12
+  TView l13 = conv(x, new_act(S / 32, S / 32, 256), 1, 256, 1);  // 13
+  x = conv(l13, new_act(S / 32, S / 32, 512), 3, 512, 1);        // 14
+  // 15 + 16: conv 255 linear, YOLO head 1 -> det[0 : N*(S/32)^2*255]
+  TView det1{B_DET, 0, N, S / 32, S / 32, 255, 255, true};
+  conv(x, det1, 1, 255, 2);
+  // 17 route 13; 18 conv 128 1x1; 19 upsample -> concat[0:128]
+  TView l18 = conv(l13, new_act(S / 32, S / 32, 128), 1, 128, 1);
+  {
+    TView up = cat;
+    up.c = 128;
+    LPlan L{};
+    L.type = UPSAMPLE;
+    L.in = l18;
+    L.out = up;
+    L.stride = 2;
+    P.layers.push_back(L);
+  }
+  // 20 route 19, 8 (= cat); 21 conv 256 3x3; 22 conv 255 linear; 23 YOLO head 2
+  x = conv(cat, new_act(S / 16, S / 16, 256), 3, 256, 1);        // 21
+  TView det2{B_DET, (int64_t)N * (S / 32) * (S / 32) * 255, N, S / 16, S / 16, 255, 255, true};
+  conv(x, det2, 1, 255, 2);                                      // 22 + 23
+  P.bufs[B_W] = {wcount * 2, IN};
+  P.bufs[B_BIAS] = {bcount * 4, IN};
+  P.bufs[B_DET] = {((int64_t)N * (S / 32) * (S / 32) + (int64_t)N * (S / 16) * (S / 16)) * 255 * 4, OUT};
+  P.bufs[B_WS] = {std::max<int64_t>(ws, 16), WRK};
+  return P;
+}
+
+// ---- kernels ------------------------------------------------------------------
+
+__device__ __forceinline__ float unitf(uint64_t seed, uint64_t i) { return gs_unit(seed, i); }
+
+__global__ void gen_image(__nv_bfloat16 *x, int64_t n, uint64_t seed) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    x[i] = __float2bfloat16_rn(unitf(seed, (uint64_t)i));
+}
+
+// one layer's filters [cout x kpad]: U(-s, s), s = sqrt(6 / fan_in) (He
+// uniform, so activations stay O(1) through the stack); padding columns 0.
+__global__ void gen_filters(__nv_bfloat16 *w, int cout, int kdim, int kpad, float s, uint64_t seed) {
+  const int64_t total = (int64_t)cout * kpad;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int col = (int)(i % kpad);
+    const float v = col < kdim ? (2.0f * unitf(seed, (uint64_t)i) - 1.0f) * s : 0.0f;
+    w[i] = __float2bfloat16_rn(v);
+  }
+}
+
+__global__ void gen_bias(float *b, int n, uint64_t seed) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    b[i] = 0.1f * (2.0f * unitf(seed, (uint64_t)i) - 1.0f);
+}
+
+struct ViewArgs {
+  const __nv_bfloat16 *p;
+  int n, h, w, c, pitch;
+};
+
+// im2row, 3x3 / stride 1 / pad 1 (every yolov3-tiny conv with k > 1):
+// ws[pixel][(kh*3 + kw)*C + c], zero outside the image and in the pad columns.
+// 16-byte vectors when C % 8 == 0 (all layers but the first).
+__global__ void __launch_bounds__(kThr) im2row3(ViewArgs in, __nv_bfloat16 *ws, int kdim, int kpad) {
+  const int C = in.c;
+  const bool vec = (C % 8 == 0) && (in.pitch % 8 == 0);
+  const int64_t pix = (int64_t)in.n * in.h * in.w;
+  const int chunks = kpad / 8;
+  const int64_t total = pix * chunks;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t p = t / chunks;
+    const int col0 = (int)(t % chunks) * 8;
+    const int ox = (int)(p % in.w), oy = (int)((p / in.w) % in.h), b = (int)(p / ((int64_t)in.w * in.h));
+    uint4 out;
+    if (vec) {
+      out = make_uint4(0, 0, 0, 0);
+      if (col0 < kdim) {
+        const int tap = col0 / C, c = col0 % C;
+        const int iy = oy + tap / 3 - 1, ix = ox + tap % 3 - 1;
+        if (iy >= 0 && iy < in.h && ix >= 0 && ix < in.w)
+          out = *reinterpret_cast<const uint4 *>(in.p + (((int64_t)b * in.h + iy) * in.w + ix) * in.pitch + c);
+      }
+    } else {
+      __align__(16) __nv_bfloat16 v[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const int col = col0 + q;
+        float x = 0.0f;
+        if (col < kdim) {
+          const int tap = col / C, c = col % C;
+          const int iy = oy + tap / 3 - 1, ix = ox + tap % 3 - 1;
+          if (iy >= 0 && iy < in.h && ix >= 0 && ix < in.w)
+            x = __bfloat162float(in.p[(((int64_t)b * in.h + iy) * in.w + ix) * in.pitch + c]);
+        }
+        v[q] = __float2bfloat16_rn(x);
+      }
+      out = *reinterpret_cast<uint4 *>(v);
+    }
+    *reinterpret_cast<uint4 *>(ws + p * kpad + col0) = out;
+  }
+}
+
+// Darknet maxpool, size 2: stride 2 halves the map; stride 1 keeps it
+// (window clipped at the bottom / right edge, Darknet's pad = size - 1).
+__global__ void __launch_bounds__(kThr) maxpool2(ViewArgs in, __nv_bfloat16 *out, int oh, int ow, int opitch,
+                                                 int stride) {
+  const int cv = in.c / 8;
+  const int64_t total = (int64_t)in.n * oh * ow * cv;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+    const int c = (int)(t % cv) * 8;
+    const int64_t p = t / cv;
+    const int ox = (int)(p % ow), oy = (int)((p / ow) % oh), b = (int)(p / ((int64_t)ow * oh));
+    __nv_bfloat162 m[4];
+    bool first = true;
+    for (int dy = 0; dy < 2; ++dy)
+      for (int dx = 0; dx < 2; ++dx) {
+        const int iy = oy * stride + dy, ix = ox * stride + dx;
+        if (iy >= in.h || ix >= in.w) continue;
+        const uint4 v = *reinterpret_cast<const uint4 *>(in.p + (((int64_t)b * in.h + iy) * in.w + ix) * in.pitch + c);
+        const __nv_bfloat162 *h = reinterpret_cast<const __nv_bfloat162 *>(&v);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) m[q] = first ? h[q] : __hmax2(m[q], h[q]);
+        first = false;
+      }
+    *reinterpret_cast<uint4 *>(out + p * opitch + c) = *reinterpret_cast<uint4 *>(m);
+  }
+}
+
+// nearest 2x upsample into a channel slice of the route tensor
+__global__ void __launch_bounds__(kThr) upsample2(ViewArgs in, __nv_bfloat16 *out, int opitch) {
+  const int cv = in.c / 8, oh = in.h * 2, ow = in.w * 2;
+  const int64_t total = (int64_t)in.n * oh * ow * cv;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+    const int c = (int)(t % cv) * 8;
+    const int64_t p = t / cv;
+    const int ox = (int)(p % ow), oy = (int)((p / ow) % oh), b = (int)(p / ((int64_t)ow * oh));
+    *reinterpret_cast<uint4 *>(out + p * opitch + c) = *reinterpret_cast<const uint4 *>(
+        in.p + (((int64_t)b * in.h + oy / 2) * in.w + ox / 2) * in.pitch + c);
+  }
+}
+
+ViewArgs vargs(const TView &v, const std::vector<void *> &buf) {
+  return {reinterpret_cast<const __nv_bfloat16 *>(buf[v.buf]) + v.off, v.n, v.h, v.w, v.c, v.pitch};
+}
+
+int grid_for(int64_t total) { return (int)std::min<int64_t>((total + kThr - 1) / kThr, 4 * kSMs); }
+
+}  // namespace
+
+// ---- job hooks (gs_work_internal.h) ------------------------------------------
+
+int gemm_validate(const gs_job_desc &j) {
+  if (j.n < 32 || j.n % 32) return err(GS_ERR_CONFIG, "yolo input size must be a positive multiple of 32");
+  if (j.m < 1 || j.m > 1024) return err(GS_ERR_CONFIG, "yolo batch must be 1..1024");
+  if (j.iters < 1) return err(GS_ERR_CONFIG, "yolo needs at least one forward pass");
+  return GS_OK;
+}
+
+std::vector<Buf> gemm_buffers(const gs_job_desc &j) { return yolo_plan(j).bufs; }
+
+// launch shapes for the probe: the widest launch (im2row / pool grids) and
+// the GEMM's dynamic shared memory (largest tile variant the net can pick)
+std::vector<Shape> gemm_launches(const gs_job_desc &j) {
+  const NetPlan P = yolo_plan(j);
+  int bn_max = 32;
+  for (const LPlan &L : P.layers)
+    if (L.type == CONV)
+      bn_max = std::max(bn_max, gemm_pick_bn((int)((int64_t)L.in.n * L.in.h * L.in.w), L.cout));
+  const int64_t pix0 = (int64_t)j.m * j.n * j.n;
+  Shape g{gemm_kernel_fn(bn_max), kSMs, 128};
+  g.dsmem = (int)gemm_smem_for(bn_max);
+  return {g, {(const void *)im2row3, grid_for(pix0 * 4), kThr}, {(const void *)maxpool2, grid_for(pix0), kThr}};
+}
+
+int gemm_generate(const gs_job_desc &j, const std::vector<void *> &dst, cudaStream_t st) {
+  const NetPlan P = yolo_plan(j);
+  const int64_t nimg = (int64_t)j.m * j.n * j.n * 3;
+  gen_image<<<grid_for(nimg), kThr, 0, st>>>((__nv_bfloat16 *)dst[B_IMG], nimg, j.seed);
+  int li = 0;
+  for (const LPlan &L : P.layers) {
+    if (L.type != CONV) continue;
+    const float s = sqrtf(6.0f / (float)L.kdim);
+    gen_filters<<<grid_for((int64_t)L.cout * L.kpad), kThr, 0, st>>>((__nv_bfloat16 *)dst[B_W] + L.woff, L.cout,
+                                                                      L.kdim, L.kpad, s, j.seed + 100 + li);
+    gen_bias<<<grid_for(L.cout), kThr, 0, st>>>((float *)dst[B_BIAS] + L.boff, L.cout, j.seed + 200 + li);
+    ++li;
+  }
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return err(GS_ERR_CUDA, std::string("yolo generate: ") + cudaGetErrorString(e));
+  return GS_OK;
+}
+
+int gemm_run(const gs_job_desc &j, std::vector<void *> &buf, cudaStream_t st, int *out_idx, int64_t *launches) {
+  const NetPlan P = yolo_plan(j);
+  for (int pass = 0; pass < j.iters; ++pass) {
+    for (const LPlan &L : P.layers) {
+      const ViewArgs in = vargs(L.in, buf);
+      if (L.type == MAXPOOL) {
+        maxpool2<<<grid_for((int64_t)L.out.n * L.out.h * L.out.w * (L.in.c / 8)), kThr, 0, st>>>(
+            in, (__nv_bfloat16 *)buf[L.out.buf] + L.out.off, L.out.h, L.out.w, L.out.pitch, L.stride);
+        ++*launches;
+        continue;
+      }
+      if (L.type == UPSAMPLE) {
+        upsample2<<<grid_for((int64_t)L.in.n * L.in.h * L.in.w * 4 * (L.in.c / 8)), kThr, 0, st>>>(
+            in, (__nv_bfloat16 *)buf[L.out.buf] + L.out.off, L.out.pitch);
+        ++*launches;
+        continue;
+      }
+      const int64_t pix = (int64_t)L.in.n * L.in.h * L.in.w;
+      const void *A;
+      int64_t lda;
+      if (L.k == 1 && L.in.pitch % 8 == 0 && L.in.off % 8 == 0) {
+        A = in.p;  // 1x1 / stride 1: the activation is already the im2row matrix
+        lda = L.in.pitch;
+      } else {
+        im2row3<<<grid_for(pix * (L.kpad / 8)), kThr, 0, st>>>(in, (__nv_bfloat16 *)buf[B_WS], L.kdim, L.kpad);
+        ++*launches;
+        A = buf[B_WS];
+        lda = L.kpad;
+      }
+      void *out = L.out.f32 ? (void *)((float *)buf[L.out.buf] + L.out.off)
+                            : (void *)((__nv_bfloat16 *)buf[L.out.buf] + L.out.off);
+      int rc = gemm_bf16(A, lda, (const __nv_bfloat16 *)buf[B_W] + L.woff, L.kpad, (const float *)buf[B_BIAS] + L.boff,
+                         out, L.out.pitch, (int)pix, L.cout, L.kpad, L.out.f32 ? 1 : 0, L.act, kSMs, st);
+      if (rc) return rc;
+      ++*launches;
+    }
+  }
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return err(GS_ERR_CUDA, std::string("yolo run: ") + cudaGetErrorString(e));
+  *out_idx = B_DET;
+  return GS_OK;
+}
+
+}  // namespace gsw

@@ -54,6 +54,8 @@ struct Staged {
   int device = 0;
   bool host = false;
   std::vector<void *> ptr;
+  void *host_out = nullptr;  // e2e: pinned destination of the job's outputs
+  int64_t host_out_bytes = 0;
 };
 
 std::mutex g_stage_mu;
@@ -66,6 +68,17 @@ void free_staged(Staged &s) {
     else cudaFree(p);
   }
   s.ptr.clear();
+  if (s.host_out) cudaFreeHost(s.host_out);
+  s.host_out = nullptr;
+}
+
+// Capacity of a job's pinned output area: every buffer that can hold an
+// output (OUT, INOUT, and the ping-pong scratch SCR of hotspot / srad).
+int64_t e2e_out_bytes(const gs_job_desc &j) {
+  int64_t o = 0;
+  for (const Buf &b : job_buffers(j))
+    if (b.role != IN && b.role != WRK) o += b.bytes;
+  return o;
 }
 
 bool same_desc(const gs_job_desc &a, const gs_job_desc &b) { return memcmp(&a, &b, sizeof(a)) == 0; }
@@ -99,6 +112,10 @@ int stage_one(const gs_job_desc &j, int device, int mode, Staged &out) {
       out.ptr[i] = dev[i];
       dev[i] = nullptr;
     }
+  }
+  if (out.host) {  // the user's pinned output buffers, allocated outside the timed region
+    out.host_out_bytes = e2e_out_bytes(j);
+    CUE(cudaHostAlloc(&out.host_out, out.host_out_bytes, cudaHostAllocPortable));
   }
   CUE(cudaStreamSynchronize(st));
   for (void *p : dev)
@@ -178,6 +195,10 @@ int run_job(const gs_job_desc &j, const Staged *stg, int mode, cudaStream_t st, 
   rc = digest(buf[out_idx], bufs[out_idx].bytes, dsum, st);
   if (rc) return rc;
   if (mode == GS_MODE_E2E) {
+    if (stg && stg->host_out) {
+      host_out = stg->host_out;
+      host_out_bytes = stg->host_out_bytes;
+    }
     int64_t off = 0;
     for (size_t i = 0; i < bufs.size(); ++i) {
       const bool is_out = bufs[i].role == OUT || (int)i == out_idx;
@@ -333,7 +354,14 @@ int gs_exec_run(const gs_job_desc *jobs, int32_t n_jobs, int32_t policy, int32_t
   double decision_ms = 0;
   int first_err = GS_OK;
   std::string first_msg;
-  const int64_t out_cap = mode == GS_MODE_E2E ? max_out_bytes(jobs, n_jobs) : 0;
+  // e2e outputs land in the staged jobs' pinned buffers; a per-worker
+  // fallback buffer is allocated only for jobs that were not staged
+  int64_t out_cap = 0;
+  if (mode == GS_MODE_E2E) {
+    std::lock_guard<std::mutex> g(g_stage_mu);
+    for (int i = 0; i < n_jobs; ++i)
+      if (!find_staged(jobs[i])) out_cap = std::max(out_cap, max_out_bytes(jobs + i, 1));
+  }
   const auto t0 = Clock::now();
 
   auto redrive = [&]() {  // caller holds mu

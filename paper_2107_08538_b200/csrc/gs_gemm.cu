@@ -1,13 +1,297 @@
-// gs_gemm.cu — Darknet-style layer stacks on tcgen05 (placeholder until the
-// tcgen05 GEMM lands; GEMM jobs are refused with a config error).
+// gs_gemm.cu — Darknet-style layers on the 5th-generation tensor cores.
+//
+// The reference models Darknet jobs as catalog entries (conv1 / conv2 / fc /
+// backbone ..., gpushare/data/neural_catalog.json:6-57) with no code; here
+// they run for real.  A Darknet convolution is im2col + GEMM (Darknet's
+// gemm_gpu path); on B200 the GEMM is a tcgen05 kernel:
+//
+//   D[M x N] = act(A[M x K] . B[N x K]^T + bias[N])      (bf16 in, fp32 acc)
+//
+// A = activation patches (NHWC im2row: one row per output pixel, K =
+// kh*kw*C_in contiguous), B = filters [C_out x K] (Darknet's weight layout),
+// D = the next NHWC activation.  Both operands are K-major and arrive by TMA
+// (128-byte swizzle) into a 4-stage shared-memory ring; one elected thread
+// issues tcgen05.mma (M = 128, N = BN, K = 16 per instruction) into a TMEM
+// accumulator; all four warps drain TMEM with tcgen05.ld and apply the bias +
+// leaky-ReLU epilogue (Darknet's activate_array LEAKY, slope 0.1).
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <string.h>
+
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "gs_tc.cuh"
 #include "gs_work_internal.h"
 
 namespace gsw {
 
-std::vector<Buf> gemm_buffers(const gs_job_desc &) { return {}; }
-int gemm_validate(const gs_job_desc &) { return err(GS_ERR_CONFIG, "gemm jobs are not available in this build"); }
-std::vector<Shape> gemm_launches(const gs_job_desc &) { return {}; }
-int gemm_generate(const gs_job_desc &, const std::vector<void *> &, cudaStream_t) { return GS_ERR_CONFIG; }
-int gemm_run(const gs_job_desc &, std::vector<void *> &, cudaStream_t, int *, int64_t *) { return GS_ERR_CONFIG; }
+struct GemmArgs {
+  int m, n;              // valid rows / columns of D
+  int m_tiles, n_tiles, k_blocks;
+  const float *bias;     // [n] or nullptr
+  void *out;             // D + column offset
+  int64_t ldo;           // row pitch of D (elements)
+  int out_f32;           // 1: fp32 D, 0: bf16 D
+  int act;               // 0 linear, 1 leaky (0.1), 2 YOLO logistic
+};
+
+constexpr int kGemmBM = 128, kGemmBK = 64, kGemmStages = 4;
+
+template <int BN>
+constexpr size_t gemm_smem_bytes() {
+  return (size_t)kGemmStages * (kGemmBM + BN) * kGemmBK * 2 + 1024 + 256;
+}
+
+__device__ __forceinline__ float leaky(float v) { return v > 0.0f ? v : 0.1f * v; }
+// YOLO layer (Darknet yolo_layer forward): logistic on x, y, objectness and
+// class scores of each 85-channel anchor group; w, h (entries 2, 3) linear.
+__device__ __forceinline__ float yolo_act(float v, int col) {
+  const int e = col % 85;
+  return (e == 2 || e == 3) ? v : 1.0f / (1.0f + expf(-v));
+}
+
+template <int BN>
+__global__ void __launch_bounds__(128, 1) gemm_bf16_tc(const __grid_constant__ CUtensorMap ta,
+                                                       const __grid_constant__ CUtensorMap tb, GemmArgs g) {
+  using namespace tc;
+  constexpr uint32_t A_BYTES = kGemmBM * kGemmBK * 2, B_BYTES = BN * kGemmBK * 2;
+  constexpr uint32_t TM_COLS = BN < 32 ? 32 : BN;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t *sa = smem;
+  uint8_t *sb = smem + kGemmStages * A_BYTES;
+  uint64_t *full = reinterpret_cast<uint64_t *>(sb + kGemmStages * B_BYTES);
+  uint64_t *empty = full + kGemmStages;
+  uint64_t *done = empty + kGemmStages;
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(done + 1);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&ta);
+    tma_prefetch(&tb);
+    for (int s = 0; s < kGemmStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(done, 1);
+    fence_mbar_init();
+  }
+  if (warp == 1) tmem_alloc<TM_COLS>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  constexpr uint32_t idesc = idesc_bf16_f32(kGemmBM, BN);
+
+  uint32_t stage = 0, phase = 0, tile_phase = 0;
+  const int tiles = g.m_tiles * g.n_tiles;
+  for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+    const int mt = tile / g.n_tiles, nt = tile % g.n_tiles;
+    if (warp == 0 && lane == 0) {
+      // TMA producer
+      for (int kb = 0; kb < g.k_blocks; ++kb) {
+        mbar_wait(&empty[stage], phase ^ 1);
+        mbar_expect_tx(&full[stage], A_BYTES + B_BYTES);
+        tma_load_2d(sa + stage * A_BYTES, &ta, &full[stage], kb * kGemmBK, mt * kGemmBM);
+        tma_load_2d(sb + stage * B_BYTES, &tb, &full[stage], kb * kGemmBK, nt * BN);
+        if (++stage == kGemmStages) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+    } else if (warp == 1 && lane == 0) {
+      // MMA issuer
+      for (int kb = 0; kb < g.k_blocks; ++kb) {
+        mbar_wait(&full[stage], phase);
+        tc_fence_after();
+        const uint64_t ad = sdesc_k_sw128(sa + stage * A_BYTES);
+        const uint64_t bd = sdesc_k_sw128(sb + stage * B_BYTES);
+#pragma unroll
+        for (int k = 0; k < kGemmBK / 16; ++k)
+          mma_bf16(tmem, ad + 2 * k, bd + 2 * k, idesc, (kb | k) != 0);
+        mma_commit(&empty[stage]);  // frees the smem slot when these MMAs finish
+        if (++stage == kGemmStages) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+      mma_commit(done);
+    }
+    __syncwarp();
+    // epilogue: TMEM lane = tile row; this warp owns lanes 32*warp .. +31
+    mbar_wait(done, tile_phase);
+    tile_phase ^= 1;
+    tc_fence_after();
+    const int row = mt * kGemmBM + warp * 32 + lane;
+#pragma unroll 1
+    for (int c0 = 0; c0 < BN; c0 += 32) {
+      float v[32];
+      tmem_ld32(tmem + ((uint32_t)(warp * 32) << 16) + c0, v);
+      const int col0 = nt * BN + c0;
+      if (row >= g.m || col0 >= g.n) continue;
+#pragma unroll
+      for (int i = 0; i < 32; ++i) {
+        float x = v[i];
+        if (g.bias && col0 + i < g.n) x += g.bias[col0 + i];
+        v[i] = g.act == 1 ? leaky(x) : (g.act == 2 ? yolo_act(x, col0 + i) : x);
+      }
+      const bool whole = col0 + 32 <= g.n;
+      if (g.out_f32) {
+        float *o = reinterpret_cast<float *>(g.out) + (int64_t)row * g.ldo + col0;
+        if (whole && ((reinterpret_cast<uintptr_t>(o) & 15) == 0)) {
+#pragma unroll
+          for (int i = 0; i < 32; i += 4) *reinterpret_cast<float4 *>(o + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+        } else {
+          for (int i = 0; i < 32 && col0 + i < g.n; ++i) o[i] = v[i];
+        }
+      } else {
+        __nv_bfloat16 *o = reinterpret_cast<__nv_bfloat16 *>(g.out) + (int64_t)row * g.ldo + col0;
+        if (whole && ((reinterpret_cast<uintptr_t>(o) & 15) == 0)) {
+#pragma unroll
+          for (int i = 0; i < 32; i += 8) {
+            uint4 q;
+            __nv_bfloat162 p0 = __floats2bfloat162_rn(v[i], v[i + 1]), p1 = __floats2bfloat162_rn(v[i + 2], v[i + 3]);
+            __nv_bfloat162 p2 = __floats2bfloat162_rn(v[i + 4], v[i + 5]), p3 = __floats2bfloat162_rn(v[i + 6], v[i + 7]);
+            q.x = *reinterpret_cast<uint32_t *>(&p0);
+            q.y = *reinterpret_cast<uint32_t *>(&p1);
+            q.z = *reinterpret_cast<uint32_t *>(&p2);
+            q.w = *reinterpret_cast<uint32_t *>(&p3);
+            *reinterpret_cast<uint4 *>(o + i) = q;
+          }
+        } else {
+          for (int i = 0; i < 32 && col0 + i < g.n; ++i) o[i] = __float2bfloat16_rn(v[i]);
+        }
+      }
+    }
+    tc_fence_before();
+    __syncthreads();  // TMEM is free for the next tile's MMAs
+    tc_fence_after();
+  }
+  if (warp == 1) tmem_dealloc<TM_COLS>(tmem);
+}
+
+// ---------------------------------------------------------------------------
+// host side
+// ---------------------------------------------------------------------------
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
+                                  const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void *p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  });
+  return fn;
+}
+
+// K-major bf16 matrix [rows x k] (row pitch ld elements), box [box_rows x 64],
+// 128-byte swizzle; out-of-bounds rows / columns read as zero.
+static int make_tmap(CUtensorMap *m, const void *ptr, int64_t rows, int64_t k, int64_t ld, int box_rows) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return err(GS_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  if ((ld * 2) % 16 || (reinterpret_cast<uintptr_t>(ptr) & 15))
+    return err(GS_ERR_CONFIG, "gemm operands need 16-byte aligned rows (K % 8 == 0)");
+  cuuint64_t dims[2] = {(cuuint64_t)k, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)(ld * 2)};
+  cuuint32_t box[2] = {(cuuint32_t)kGemmBK, (cuuint32_t)box_rows};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void *>(ptr), dims, strides, box, es,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return err(GS_ERR_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
+  return GS_OK;
+}
+
+template <int BN>
+static int launch_bn(const CUtensorMap &ta, const CUtensorMap &tb, GemmArgs g, int max_ctas, cudaStream_t st) {
+  static std::once_flag once;
+  static cudaError_t attr_rc = cudaSuccess;
+  std::call_once(once, [] {
+    attr_rc = cudaFuncSetAttribute(gemm_bf16_tc<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)gemm_smem_bytes<BN>());
+  });
+  if (attr_rc != cudaSuccess) return err(GS_ERR_CUDA, std::string("gemm smem attribute: ") + cudaGetErrorString(attr_rc));
+  g.n_tiles = (g.n + BN - 1) / BN;
+  const int tiles = g.m_tiles * g.n_tiles;
+  const int grid = tiles < max_ctas ? tiles : max_ctas;
+  gemm_bf16_tc<BN><<<grid, 128, gemm_smem_bytes<BN>(), st>>>(ta, tb, g);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return err(GS_ERR_CUDA, std::string("gemm launch: ") + cudaGetErrorString(e));
+  return GS_OK;
+}
+
+int gemm_pick_bn(int m, int n) {
+  if (n <= 32) return 32;
+  if (n <= 64) return 64;
+  const int m_tiles = (m + kGemmBM - 1) / kGemmBM;
+  if (n >= 256 && (int64_t)m_tiles * ((n + 255) / 256) >= 2 * kSMs) return 256;
+  return 128;
+}
+
+// D = act(A . B^T + bias): A [m x k] (pitch lda), B [n x k] (pitch ldb), D
+// [m x n] at `out` (pitch ldo).  max_ctas bounds the grid (the job's SM share).
+int gemm_bf16(const void *A, int64_t lda, const void *B, int64_t ldb, const float *bias, void *out, int64_t ldo,
+              int m, int n, int k, int out_f32, int act, int max_ctas, cudaStream_t st) {
+  if (m <= 0 || n <= 0 || k <= 0) return err(GS_ERR_CONFIG, "gemm dims must be positive");
+  if (k % 8) return err(GS_ERR_CONFIG, "gemm K must be a multiple of 8");
+  const int bn = gemm_pick_bn(m, n);
+  CUtensorMap ta, tb;
+  int rc = make_tmap(&ta, A, m, k, lda, kGemmBM);
+  if (rc) return rc;
+  rc = make_tmap(&tb, B, n, k, ldb, bn);
+  if (rc) return rc;
+  GemmArgs g;
+  g.m = m;
+  g.n = n;
+  g.m_tiles = (m + kGemmBM - 1) / kGemmBM;
+  g.n_tiles = 0;
+  g.k_blocks = (k + kGemmBK - 1) / kGemmBK;
+  g.bias = bias;
+  g.out = out;
+  g.ldo = ldo;
+  g.out_f32 = out_f32;
+  g.act = act;
+  if (max_ctas <= 0) max_ctas = kSMs;
+  switch (bn) {
+    case 32: return launch_bn<32>(ta, tb, g, max_ctas, st);
+    case 64: return launch_bn<64>(ta, tb, g, max_ctas, st);
+    case 128: return launch_bn<128>(ta, tb, g, max_ctas, st);
+    default: return launch_bn<256>(ta, tb, g, max_ctas, st);
+  }
+}
+
+size_t gemm_smem_for(int bn) {
+  switch (bn) {
+    case 32: return gemm_smem_bytes<32>();
+    case 64: return gemm_smem_bytes<64>();
+    case 128: return gemm_smem_bytes<128>();
+    default: return gemm_smem_bytes<256>();
+  }
+}
+
+const void *gemm_kernel_fn(int bn) {
+  switch (bn) {
+    case 32: return (const void *)gemm_bf16_tc<32>;
+    case 64: return (const void *)gemm_bf16_tc<64>;
+    case 128: return (const void *)gemm_bf16_tc<128>;
+    default: return (const void *)gemm_bf16_tc<256>;
+  }
+}
 
 }  // namespace gsw
+
+extern "C" int gs_gemm_bf16(const void *A, int64_t lda, const void *B, int64_t ldb, const float *bias, void *out,
+                            int64_t ldo, int32_t m, int32_t n, int32_t k, int32_t out_f32, int32_t act, void *stream) {
+  return gsw::gemm_bf16(A, lda, B, ldb, bias, out, ldo, m, n, k, out_f32, act, 0, (cudaStream_t)stream);
+}

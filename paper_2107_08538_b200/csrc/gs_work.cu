@@ -52,7 +52,9 @@ std::vector<Buf> job_buffers(const gs_job_desc &j) {
   const int64_t n = j.n;
   switch (j.kind) {
     case GS_JOB_BFS:
-      b = {{(n + 1) * 4, IN}, {n * GS_BFS_DEGREE * 4, IN}, {n * 4, OUT}, {n * 4, SCR}, {n * 4, SCR}, {16, SCR}};
+      // row_ptr, col, level, frontier queues, counter, visited bitmap
+      b = {{(n + 1) * 4, IN}, {n * GS_BFS_DEGREE * 4, IN}, {n * 4, OUT}, {n * 4, SCR}, {n * 4, SCR}, {16, SCR},
+           {(n / 32 + 1) * 4, SCR}};
       break;
     case GS_JOB_HOTSPOT:
       b = {{n * n * 4, INOUT}, {n * n * 4, IN}, {n * n * 4, SCR}};
@@ -68,13 +70,13 @@ std::vector<Buf> job_buffers(const gs_job_desc &j) {
       b = {{(n + 1) * 4, IN}, {j.m * (n + 1) * 4, INOUT}, {j.m * (n + 1) * 4, SCR}, {80 * 4, INOUT},
            {(int64_t)kSMs * 8 * kMaxHid * 8, SCR}};
       break;
-    case GS_JOB_NEEDLE:
-      b = {{(n + 1) * (n + 1) * 4, IN}, {(n + 1) * (n + 1) * 4, INOUT}};
+    case GS_JOB_NEEDLE:  // ref, score, band tickets + progress flags
+      b = {{(n + 1) * (n + 1) * 4, IN}, {(n + 1) * (n + 1) * 4, INOUT}, {(n / 32 + 1) * 4, SCR}};
       break;
     case GS_JOB_LUD:
       b = {{n * n * 4, INOUT}};
       break;
-    case GS_JOB_GEMM:
+    case GS_JOB_YOLO:
       b = gemm_buffers(j);
       break;
     default:
@@ -101,7 +103,7 @@ int validate(const gs_job_desc &j) {
     case GS_JOB_BACKPROP:
       if (j.m < 1 || j.m > kMaxHid) return err(GS_ERR_CONFIG, "backprop hidden units must be 1..16");
       break;
-    case GS_JOB_GEMM:
+    case GS_JOB_YOLO:
       return gemm_validate(j);
     default:
       break;
@@ -114,6 +116,12 @@ int validate(const gs_job_desc &j) {
 // thread_blocks is a real placement demand for mgb-sm.
 int job_grid(const gs_job_desc &) { return 2 * kSMs; }
 
+// needle: one warp per 32-row band in flight, at most the job's SM share
+int needle_grid(const gs_job_desc &j) {
+  const int bands = (int)(j.n / 32);
+  return std::min((bands + kNwWarps - 1) / kNwWarps, 2 * kSMs);
+}
+
 std::vector<Shape> job_launches(const gs_job_desc &j) {
   const int g = job_grid(j);
   switch (j.kind) {
@@ -125,18 +133,16 @@ std::vector<Shape> job_launches(const gs_job_desc &j) {
       return {{(const void *)srad_stats, 1, kThreads}, {(const void *)srad_coeff, g, kThreads},
               {(const void *)srad_update, g, kThreads}};
     case GS_JOB_KMEANS:
-      return {{(const void *)kmeans_assign, g, kThreads}, {(const void *)kmeans_recenter, 1, kThreads}};
+      return {{(const void *)kmeans_assign_fn((int)j.m), g, kThreads}, {(const void *)kmeans_recenter, 1, kThreads}};
     case GS_JOB_BACKPROP:
       return {{(const void *)bp_forward, g, kThreads}, {(const void *)bp_output, 1, 32},
               {(const void *)bp_adjust, g, kThreads}};
-    case GS_JOB_NEEDLE: {
-      const int tiles = (int)(j.n / 32);
-      return {{(const void *)needle_diag, (tiles + 3) / 4, 128}};
-    }
+    case GS_JOB_NEEDLE:
+      return {{(const void *)needle_bands, needle_grid(j), 32 * kNwWarps}};
     case GS_JOB_LUD:
       return {{(const void *)lud_diagonal, 1, BS}, {(const void *)lud_perimeter, (int)(j.n / BS), 2 * BS},
               {(const void *)lud_internal, g, 256}};
-    case GS_JOB_GEMM:
+    case GS_JOB_YOLO:
       return gemm_launches(j);
   }
   return {};
@@ -168,7 +174,7 @@ extern "C" int gs_job_probe(const gs_job_desc *job, gs_probe *out) {
       out->threads_per_block = s.block;
     }
     out->regs_per_thread = std::max(out->regs_per_thread, a.numRegs);
-    out->smem_per_block = std::max<int32_t>(out->smem_per_block, (int32_t)a.sharedSizeBytes);
+    out->smem_per_block = std::max<int32_t>(out->smem_per_block, (int32_t)a.sharedSizeBytes + s.dsmem);
   }
   out->total_warps = (int64_t)out->thread_blocks * out->warps_per_block;
   out->est_duration_ms = 0.0;
@@ -221,7 +227,7 @@ int generate_inputs(const gs_job_desc &j, const std::vector<void *> &dst, cudaSt
     case GS_JOB_LUD:
       gen_lud<<<g, kThreads, 0, st>>>((float *)dst[0], n, j.seed);
       break;
-    case GS_JOB_GEMM:
+    case GS_JOB_YOLO:
       return gemm_generate(j, dst, st);
   }
   CUW(cudaGetLastError());
@@ -240,13 +246,16 @@ int run_kernels(const gs_job_desc &j, std::vector<void *> &buf, cudaStream_t st,
     case GS_JOB_BFS: {
       int32_t *row = (int32_t *)buf[0], *col = (int32_t *)buf[1], *level = (int32_t *)buf[2];
       int32_t *qa = (int32_t *)buf[3], *qb = (int32_t *)buf[4], *cnt = (int32_t *)buf[5];
+      uint32_t *vis = (uint32_t *)buf[6];
       CUW(cudaMemsetAsync(level, 0xff, n * 4, st));
       CUW(cudaMemsetAsync(level, 0, 4, st));
       CUW(cudaMemsetAsync(qa, 0, 4, st));
+      CUW(cudaMemsetAsync(vis, 0, (n / 32 + 1) * 4, st));
+      CUW(cudaMemsetAsync(vis, 1, 1, st));  // source vertex 0
       int32_t n_in = 1;
       for (int32_t depth = 0; n_in > 0; ++depth) {
         CUW(cudaMemsetAsync(cnt, 0, 4, st));
-        bfs_expand<<<g, kThreads, 0, st>>>(row, col, level, qa, n_in, qb, cnt, depth + 1);
+        bfs_expand<<<g, kThreads, 0, st>>>(row, col, level, vis, qa, n_in, qb, cnt, depth + 1);
         ++launches;
         // Rodinia-style host round trip per level (the frontier size)
         CUW(cudaMemcpyAsync(host_scalar, cnt, 4, cudaMemcpyDeviceToHost, st));
@@ -294,7 +303,7 @@ int run_kernels(const gs_job_desc &j, std::vector<void *> &buf, cudaStream_t st,
         CUW(cudaMemcpy2DAsync(cent + f, nf * 4, x + (int64_t)f * n, 4, 4, GS_KMEANS_K, cudaMemcpyDeviceToDevice,
                               st));
       for (int it = 0; it < j.iters; ++it) {
-        kmeans_assign<<<g, kThreads, 0, st>>>(x, n, nf, cent, mem, sumq, cnt);
+        kmeans_assign_fn(nf)<<<g, kThreads, 0, st>>>(x, n, nf, cent, mem, sumq, cnt);
         kmeans_recenter<<<1, kThreads, 0, st>>>(cent, sumq, cnt, nf);
         launches += 2;
       }
@@ -317,13 +326,10 @@ int run_kernels(const gs_job_desc &j, std::vector<void *> &buf, cudaStream_t st,
       break;
     }
     case GS_JOB_NEEDLE: {
-      const int tiles = (int)(n / 32);
-      for (int d = 0; d < 2 * tiles - 1; ++d) {
-        const int lo = std::max(0, d - tiles + 1), hi = std::min(d, tiles - 1);
-        const int cnt = hi - lo + 1;
-        needle_diag<<<(cnt + 3) / 4, 128, 0, st>>>((int32_t *)buf[1], (const int32_t *)buf[0], (int)n, d, cnt, lo);
-        ++launches;
-      }
+      CUW(cudaMemsetAsync(buf[2], 0, (n / 32 + 1) * 4, st));
+      needle_bands<<<needle_grid(j), 32 * kNwWarps, 0, st>>>((int32_t *)buf[1], (const int32_t *)buf[0], (int)n,
+                                                            (int32_t *)buf[2]);
+      ++launches;
       *out_idx = 1;
       break;
     }
@@ -340,7 +346,7 @@ int run_kernels(const gs_job_desc &j, std::vector<void *> &buf, cudaStream_t st,
       *out_idx = 0;
       break;
     }
-    case GS_JOB_GEMM: {
+    case GS_JOB_YOLO: {
       int rc = gemm_run(j, buf, st, out_idx, &launches);
       if (rc) return rc;
       break;

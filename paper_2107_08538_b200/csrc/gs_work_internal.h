@@ -12,7 +12,11 @@
 
 namespace gsw {
 
-enum Role { IN = 0, INOUT = 1, OUT = 2, SCR = 3 };
+constexpr int kSMs = 148;  // B200
+
+// IN staged input, INOUT staged input that is also an output, OUT output,
+// SCR zeroed scratch, WRK uninitialized workspace (fully overwritten)
+enum Role { IN = 0, INOUT = 1, OUT = 2, SCR = 3, WRK = 4 };
 
 struct Buf {
   int64_t bytes;
@@ -22,6 +26,7 @@ struct Buf {
 struct Shape {
   const void *fn;
   int grid, block;
+  int dsmem = 0;  // dynamic shared memory per block
 };
 
 std::vector<Shape> gemm_launches(const gs_job_desc &j);
@@ -42,5 +47,10 @@ std::vector<Buf> gemm_buffers(const gs_job_desc &j);
 int gemm_validate(const gs_job_desc &j);
 int gemm_generate(const gs_job_desc &j, const std::vector<void *> &dst, cudaStream_t st);
 int gemm_run(const gs_job_desc &j, std::vector<void *> &buf, cudaStream_t st, int *out_idx, int64_t *launches);
+int gemm_pick_bn(int m, int n);
+size_t gemm_smem_for(int bn);
+const void *gemm_kernel_fn(int bn);
+int gemm_bf16(const void *A, int64_t lda, const void *B, int64_t ldb, const float *bias, void *out, int64_t ldo,
+              int m, int n, int k, int out_f32, int act, int max_ctas, cudaStream_t st);
 
 }  // namespace gsw

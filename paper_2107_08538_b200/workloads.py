@@ -18,7 +18,7 @@ import numpy as np
 
 from . import _native as nat
 
-KINDS = {"bfs": 0, "hotspot": 1, "srad": 2, "kmeans": 3, "backprop": 4, "needle": 5, "lud": 6, "gemm": 7}
+KINDS = {"bfs": 0, "hotspot": 1, "srad": 2, "kmeans": 3, "backprop": 4, "needle": 5, "lud": 6, "yolo": 7}
 KIND_NAMES = {v: k for k, v in KINDS.items()}
 MODE_DEVICE, MODE_E2E = 0, 1
 
@@ -49,6 +49,8 @@ WORK_SIGNATURES = {
                               c_int32, c_int64, c_void_p, POINTER(GsExecStats)]),
     "gs_exec_stage": (c_int32, [c_void_p, c_int32, POINTER(c_int32), c_int32, c_int32]),
     "gs_exec_unstage": (None, []),
+    "gs_gemm_bf16": (c_int32, [c_void_p, c_int64, c_void_p, c_int64, c_void_p, c_void_p, c_int64, c_int32,
+                               c_int32, c_int32, c_int32, c_int32, c_void_p]),
 }
 
 _bound = False
@@ -96,11 +98,13 @@ def io_bytes(job: Job) -> tuple[int, int]:
 
 
 OUTPUT_DTYPES = {"bfs": np.int32, "hotspot": np.float32, "srad": np.float32, "kmeans": np.int32,
-                 "backprop": np.float32, "needle": np.int32, "lud": np.float32, "gemm": np.uint16}
+                 "backprop": np.float32, "needle": np.int32, "lud": np.float32, "yolo": np.float32}
 
 
 def output_shape(job: Job) -> tuple[int, ...]:
     n = job.n
+    if job.kind == "yolo":  # both YOLO heads, NHWC, 255 channels each
+        return ((job.m * (n // 32) ** 2 + job.m * (n // 16) ** 2) * 255,)
     return {"bfs": (n,), "hotspot": (n, n), "srad": (n, n), "kmeans": (n,), "backprop": (job.m, n + 1),
             "needle": (n + 1, n + 1), "lud": (n, n)}.get(job.kind, (0,))
 
@@ -112,6 +116,24 @@ def run_solo(job: Job, device: int = 0) -> tuple[np.ndarray, GsJobRecord]:
     nat.check(lib().gs_job_run_solo(ctypes.byref(job.desc()), device, MODE_DEVICE, out.ctypes.data,
                                     out.nbytes, ctypes.byref(rec)))
     return out, rec
+
+
+def gemm_bf16(a, b, bias=None, out=None, act: int = 0, out_f32: bool = True):
+    """D = act(a @ b.T + bias) on the tcgen05 GEMM (csrc/gs_gemm.cu).
+
+    a [m, k] and b [n, k] are CUDA bf16 tensors (k % 8 == 0), bias fp32 [n];
+    torch provides the device memory and the current stream only."""
+    import torch
+
+    m, k = a.shape
+    n = b.shape[0]
+    if out is None:
+        out = torch.empty((m, n), dtype=torch.float32 if out_f32 else torch.bfloat16, device=a.device)
+    stream = torch.cuda.current_stream(a.device).cuda_stream
+    nat.check(lib().gs_gemm_bf16(a.data_ptr(), a.stride(0), b.data_ptr(), b.stride(0),
+                                 bias.data_ptr() if bias is not None else None, out.data_ptr(), out.stride(0),
+                                 m, n, k, 1 if out.dtype == torch.float32 else 0, act, stream))
+    return out
 
 
 def policy_code(policy: str) -> tuple[int, int]:

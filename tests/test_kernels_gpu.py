@@ -21,9 +21,16 @@ CASES = [
     ("srad", dict(n=512, iters=5, seed=4), 1e-5),
     ("kmeans", dict(n=200_000, m=34, iters=5, seed=6), "exact"),
     ("backprop", dict(n=300_000, m=16, iters=2, seed=7), 1e-5),
+    ("needle", dict(n=32, seed=2), "exact"),      # one band, one chunk
+    ("needle", dict(n=96, seed=3), "exact"),      # odd chunk count
     ("needle", dict(n=512, seed=1), "exact"),
     ("needle", dict(n=1024, seed=9), "exact"),
+    ("needle", dict(n=4096, seed=4), "exact"),    # 128 bands in a wavefront
+    ("kmeans", dict(n=100_003, m=8, iters=3, seed=5), "exact"),    # nf < 32, ragged tail
+    ("kmeans", dict(n=65_537, m=40, iters=2, seed=6), "exact"),    # generic nf > 32
+    ("lud", dict(n=160, seed=4), 1e-5),           # trailing edge exactly one 128 tile
     ("lud", dict(n=512, seed=3), 1e-5),
+    ("lud", dict(n=1056, seed=5), 1e-5),          # partial 128 tiles
 ]
 
 
