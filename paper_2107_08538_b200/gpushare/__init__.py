@@ -24,6 +24,19 @@ from .errors import (
     GpuShareError,
     LazyBindingError,
 )
+from .lazy_runtime import (
+    GpuOp,
+    LazyState,
+    OpKind,
+    PseudoAddress,
+    kernel_launch_prepare,
+    lazy_alloc,
+    queued_bytes,
+    record_op,
+    release_bound,
+    replay,
+    set_heap_limit,
+)
 from .schedulers import (
     ASSIGN,
     DEFER,
@@ -50,4 +63,6 @@ __all__ = [
     "LaunchShape", "LazyBindingError", "PlacementPlan", "PolicyConfig",
     "ResourceRequest", "ScheduleRequest", "Scheduler", "compute_resource_request",
     "device_spec", "occupancy_limit_per_sm", "parse_policy",
+    "GpuOp", "LazyState", "OpKind", "PseudoAddress", "kernel_launch_prepare", "lazy_alloc",
+    "queued_bytes", "record_op", "release_bound", "replay", "set_heap_limit",
 ]
