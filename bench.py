@@ -49,13 +49,6 @@ def peaks() -> dict:
 FP32_TFLOPS_NOMINAL = 148 * 128 * 2 * 1.965e9 / 1e12  # 74.4: 148 SMs x 128 FMA lanes
 
 
-def dist_env():
-    rank = int(os.environ.get("RANK", "0"))
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    local = int(os.environ.get("LOCAL_RANK", str(rank)))
-    return rank, world, local
-
-
 class Clocks:
     """nvidia-smi sampling during the timed region (B200_PROFILING.md)."""
 
@@ -147,6 +140,12 @@ def kernel_rooflines(W, C, jobs, device, pk):
             out[kind] = {"bound": "hbm", "achieved": round(ach, 1), "peak": hbm, "unit": "GB/s",
                          "frac": round(ach / hbm, 4), "ms": round(ms, 3), "launches": recs[0].n_kernels,
                          "job": {"n": job.n, "iters": job.iters, "m": job.m}}
+        elif unit == "TC_FLOP":
+            ach = work / (ms * 1e-3) / 1e12
+            pkt = pk["bf16_tflops"]
+            out[kind] = {"bound": "tensor", "achieved": round(ach, 1), "peak": pkt, "unit": "TFLOP/s",
+                         "frac": round(ach / pkt, 4), "ms": round(ms, 3), "launches": recs[0].n_kernels,
+                         "job": {"n": job.n, "batch": job.m}}
         else:
             ach = work / (ms * 1e-3) / 1e12
             out[kind] = {"bound": "fp32", "achieved": round(ach, 2), "peak": round(FP32_TFLOPS_NOMINAL, 1),
@@ -236,9 +235,10 @@ def main() -> int:
     ap.add_argument("--skip-e2e", action="store_true")
     ap.add_argument("--skip-sa", action="store_true")
     args = ap.parse_args()
-    rank, world, local = dist_env()
-
     from paper_2107_08538_b200 import catalog as C
+    from paper_2107_08538_b200.multi import dist_env, max_over_ranks, rank_mix, whole_job_rate
+
+    rank, world, local = dist_env()
 
     if args.impl == "reference":
         if rank != 0:
@@ -258,7 +258,7 @@ def main() -> int:
     from paper_2107_08538_b200 import workloads as W
 
     pk = peaks()
-    mix = C.gen_mix(args.mix, args.jobs, seed=1 + rank)
+    mix = rank_mix(args.mix, args.jobs, rank)
     jobs = [m.job for m in mix]
     device = local
 
@@ -293,12 +293,10 @@ def main() -> int:
     # ---- max over ranks ----
     ms_step = ours["ms_per_step"]
     e2e_ms = e2e["ms_per_step"] if e2e else None
-    if dist:
-        t = torch.tensor([ms_step, e2e_ms or 0.0], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms_step, e2e_ms = float(t[0]), float(t[1]) or None
+    ms_step, e2e_max = max_over_ranks([ms_step, e2e_ms or 0.0], dist, device="cuda")
+    e2e_ms = e2e_max or None
     n_total = len(jobs) * world
-    value = n_total / (ms_step / 1000.0)
+    value = whole_job_rate(len(jobs), world, ms_step)
 
     # dominant kernel: the kind with the largest share of device time in the mix
     share = {}

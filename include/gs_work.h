@@ -50,7 +50,8 @@ typedef struct gs_job_desc {
 typedef struct gs_job_record {
     int32_t state;        /* 0 done, 1 crashed (oom), 2 rejected */
     int32_t device;
-    double pull_ms;       /* worker picked the job */
+    double arrival_ms;    /* job arrival (0 for a batch, sim_engine.py:607) */
+    double pull_ms;       /* worker picked the job (>= arrival) */
     double admit_ms;      /* placement decided ASSIGN */
     double end_ms;
     double wait_ms;       /* admit - pull */
@@ -90,6 +91,13 @@ int gs_job_run_solo(const gs_job_desc *job, int cuda_device, int mode, void *hos
 int gs_exec_run(const gs_job_desc *jobs, int32_t n_jobs, int32_t policy, int32_t cg_ratio,
                 const int32_t *cuda_devices, int32_t n_devices, int32_t workers, int32_t mode,
                 int64_t ledger_bytes, gs_job_record *records, gs_exec_stats *stats);
+/* Same, with per-job arrival times (ms after the run starts, non-decreasing;
+ * NULL = batch arrival): a worker that pulls a job before it arrives waits
+ * for it (BASELINE cfg 3's Poisson stream; the reference has batch arrival
+ * only). */
+int gs_exec_run_arrivals(const gs_job_desc *jobs, int32_t n_jobs, const double *arrival_ms, int32_t policy,
+                         int32_t cg_ratio, const int32_t *cuda_devices, int32_t n_devices, int32_t workers,
+                         int32_t mode, int64_t ledger_bytes, gs_job_record *records, gs_exec_stats *stats);
 
 /* Prepare (generate) the inputs of a job list ahead of gs_exec_run so the
  * timed region starts with inputs resident (device) or pinned (e2e). */

@@ -27,6 +27,11 @@ RODINIA = {
     "lud": (dict(n=4096), dict(n=6144)),
 }
 
+# Darknet YOLOv3-tiny inference jobs (BASELINE cfg 2): image edge, batch
+DARKNET = {
+    "yolo": (dict(n=416, m=8), dict(n=608, m=32)),
+}
+
 # the 8-job CPU-runnable mix of cfg 0 (2x bfs, hotspot, srad, kmeans, repeated)
 CFG0 = [("bfs", dict(n=1_000_000)), ("bfs", dict(n=1_000_000)), ("hotspot", dict(n=1024, iters=20)),
         ("srad", dict(n=2048, iters=5)), ("kmeans", dict(n=494_020, m=34, iters=5))]
@@ -74,6 +79,35 @@ def cfg0_mix(seed: int = 1) -> list[MixJob]:
     return out
 
 
+# yolov3-tiny conv layers as (edge divisor, cin, cout, k) in plan order
+# (csrc/gs_darknet.cu yolo_plan); pools / upsample move no GEMM work
+YOLO_CONVS = [(1, 3, 16, 3), (2, 16, 32, 3), (4, 32, 64, 3), (8, 64, 128, 3), (16, 128, 256, 3),
+              (32, 256, 512, 3), (32, 512, 1024, 3), (32, 1024, 256, 1), (32, 256, 512, 3), (32, 512, 255, 1),
+              (32, 256, 128, 1), (16, 384, 256, 3), (16, 256, 255, 1)]
+
+
+def yolo_buffers(S: int, N: int) -> list[int]:
+    """Byte sizes of the YOLOv3-tiny job's buffers (yolo_plan order)."""
+    act = lambda d, c: N * (S // d) ** 2 * c * 2  # noqa: E731  bf16 NHWC
+    w = 0
+    ws = 0
+    for d, cin, cout, k in YOLO_CONVS:
+        kpad = (k * k * cin + 7) // 8 * 8
+        w = (w + cout * kpad + 7) // 8 * 8
+        if k != 1:
+            ws = max(ws, N * (S // d) ** 2 * kpad * 2)
+    bias = sum(c[2] for c in YOLO_CONVS) * 4
+    det = (N * (S // 32) ** 2 + N * (S // 16) ** 2) * 255 * 4
+    acts = [act(1, 16), act(2, 16), act(2, 32), act(4, 32), act(4, 64), act(8, 64), act(8, 128), act(16, 128),
+            act(16, 384), act(32, 256), act(32, 512), act(32, 512), act(32, 1024), act(32, 256), act(32, 512),
+            act(32, 128), act(16, 256)]
+    return [N * S * S * 3 * 2, w * 2, bias, det, max(ws, 16)] + acts
+
+
+def yolo_flops(S: int, N: int) -> float:
+    return float(sum(2 * N * (S // d) ** 2 * k * k * cin * cout for d, cin, cout, k in YOLO_CONVS))
+
+
 def host_footprint(job: Job) -> int:
     """The probe's mem_bytes computed on the host alone (same rule as
     gs_job_probe: buffers rounded to 2 MiB + the 8 MiB task heap) — used by
@@ -83,11 +117,12 @@ def host_footprint(job: Job) -> int:
     sizes = {
         "bfs": [(n + 1) * 4, n * 24, n * 4, n * 4, n * 4, 16, (n // 32 + 1) * 4],
         "hotspot": [n * n * 4] * 3,
-        "srad": [n * n * 4] * 3 + [16],
+        "srad": [n * n * 4] * 2 + [16],
         "kmeans": [n * m * 4, n * 4, 5 * m * 4, 5 * m * 8, 40],
         "backprop": [(n + 1) * 4, m * (n + 1) * 4, m * (n + 1) * 4, 320, 148 * 8 * 16 * 8],
         "needle": [(n + 1) * (n + 1) * 4] * 2 + [(n // 32 + 1) * 4],
         "lud": [n * n * 4],
+        "yolo": yolo_buffers(n, m) if job.kind == "yolo" else [],
     }[job.kind]
     return (8 << 20) + sum((s + g - 1) // g * g for s in sizes)
 
@@ -98,8 +133,8 @@ def algorithmic_work(job: Job) -> tuple[float, str]:
     n, it, m = job.n, max(job.iters, 1), job.m
     if job.kind == "hotspot":
         return 12.0 * n * n * it, "B"
-    if job.kind == "srad":
-        return 24.0 * n * n * it, "B"
+    if job.kind == "srad":  # fused coefficient + update: read J, write J
+        return 8.0 * n * n * it, "B"
     if job.kind == "bfs":
         return 4.0 * 6 * n + 13.0 * n, "B"
     if job.kind == "kmeans":
@@ -110,4 +145,6 @@ def algorithmic_work(job: Job) -> tuple[float, str]:
         return 8.0 * (n + 1) * (n + 1), "B"
     if job.kind == "lud":
         return 2.0 / 3.0 * n ** 3, "FLOP"
+    if job.kind == "yolo":
+        return yolo_flops(n, m) * it, "TC_FLOP"
     return 0.0, "B"

@@ -296,6 +296,13 @@ int gs_job_run_solo(const gs_job_desc *job, int cuda_device, int mode, void *hos
 int gs_exec_run(const gs_job_desc *jobs, int32_t n_jobs, int32_t policy, int32_t cg_ratio,
                 const int32_t *cuda_devices, int32_t n_devices, int32_t workers, int32_t mode, int64_t ledger_bytes,
                 gs_job_record *records, gs_exec_stats *stats) {
+  return gs_exec_run_arrivals(jobs, n_jobs, nullptr, policy, cg_ratio, cuda_devices, n_devices, workers, mode,
+                              ledger_bytes, records, stats);
+}
+
+int gs_exec_run_arrivals(const gs_job_desc *jobs, int32_t n_jobs, const double *arrival_ms, int32_t policy,
+                         int32_t cg_ratio, const int32_t *cuda_devices, int32_t n_devices, int32_t workers,
+                         int32_t mode, int64_t ledger_bytes, gs_job_record *records, gs_exec_stats *stats) {
   if (n_jobs <= 0) return GS_OK;
   if (n_devices < 1 || n_devices > GS_MAX_DEVICES) return err(GS_ERR_CONFIG, "1..32 devices");
   if (workers < 1) return err(GS_ERR_CONFIG, "need at least one worker");
@@ -392,6 +399,12 @@ int gs_exec_run(const gs_job_desc *jobs, int32_t n_jobs, int32_t policy, int32_t
       const int j = next.fetch_add(1);
       if (j >= n_jobs) break;
       gs_job_record &rec = records[j];
+      if (arrival_ms) {  // the job has not arrived yet: this worker waits for it
+        rec.arrival_ms = arrival_ms[j];
+        const double now = ms_since(t0);
+        if (arrival_ms[j] > now)
+          std::this_thread::sleep_for(std::chrono::duration<double, std::milli>(arrival_ms[j] - now));
+      }
       rec.pull_ms = ms_since(t0);
       gs_probe pr;
       gs_job_probe(&jobs[j], &pr);

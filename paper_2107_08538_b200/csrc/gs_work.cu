@@ -60,7 +60,7 @@ std::vector<Buf> job_buffers(const gs_job_desc &j) {
       b = {{n * n * 4, INOUT}, {n * n * 4, IN}, {n * n * 4, SCR}};
       break;
     case GS_JOB_SRAD:
-      b = {{n * n * 4, INOUT}, {n * n * 4, SCR}, {n * n * 4, SCR}, {16, SCR}};
+      b = {{n * n * 4, INOUT}, {n * n * 4, SCR}, {16, SCR}};  // J, J ping-pong, q0
       break;
     case GS_JOB_KMEANS:
       b = {{n * j.m * 4, IN}, {n * 4, OUT}, {(int64_t)GS_KMEANS_K * j.m * 4, OUT},
@@ -130,8 +130,7 @@ std::vector<Shape> job_launches(const gs_job_desc &j) {
     case GS_JOB_HOTSPOT:
       return {{(const void *)hotspot_step, g, kThreads}};
     case GS_JOB_SRAD:
-      return {{(const void *)srad_stats, 1, kThreads}, {(const void *)srad_coeff, g, kThreads},
-              {(const void *)srad_update, g, kThreads}};
+      return {{(const void *)srad_stats, 1, kThreads}, {(const void *)srad_fused, g, kThreads}};
     case GS_JOB_KMEANS:
       return {{(const void *)kmeans_assign_fn((int)j.m), g, kThreads}, {(const void *)kmeans_recenter, 1, kThreads}};
     case GS_JOB_BACKPROP:
@@ -279,13 +278,12 @@ int run_kernels(const gs_job_desc &j, std::vector<void *> &buf, cudaStream_t st,
       break;
     }
     case GS_JOB_SRAD: {
-      float *J = (float *)buf[0], *J2 = (float *)buf[1], *C = (float *)buf[2], *q0 = (float *)buf[3];
+      float *J = (float *)buf[0], *J2 = (float *)buf[1], *q0 = (float *)buf[2];
       const int roi = n < 128 ? (int)n : 128;
       for (int it = 0; it < j.iters; ++it) {
         srad_stats<<<1, kThreads, 0, st>>>(J, (int)n, roi, q0);
-        srad_coeff<<<g, dim3(32, 8), 0, st>>>(J, C, (int)n, q0);
-        srad_update<<<g, dim3(32, 8), 0, st>>>(J, C, J2, (int)n);
-        launches += 3;
+        srad_fused<<<g, dim3(32, 8), 0, st>>>(J, J2, (int)n, q0);
+        launches += 2;
         std::swap(J, J2);
       }
       *out_idx = (j.iters % 2) ? 1 : 0;

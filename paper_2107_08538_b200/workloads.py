@@ -28,7 +28,8 @@ class GsJobDesc(ctypes.Structure):
 
 
 class GsJobRecord(ctypes.Structure):
-    _fields_ = [("state", c_int32), ("device", c_int32), ("pull_ms", c_double), ("admit_ms", c_double),
+    _fields_ = [("state", c_int32), ("device", c_int32), ("arrival_ms", c_double), ("pull_ms", c_double),
+                ("admit_ms", c_double),
                 ("end_ms", c_double), ("wait_ms", c_double), ("compute_ms", c_double),
                 ("mem_bytes", c_int64), ("h2d_bytes", c_int64), ("d2h_bytes", c_int64),
                 ("checksum", c_uint64), ("n_kernels", c_int32), ("pad", c_int32)]
@@ -47,6 +48,8 @@ WORK_SIGNATURES = {
                                   POINTER(GsJobRecord)]),
     "gs_exec_run": (c_int32, [c_void_p, c_int32, c_int32, c_int32, POINTER(c_int32), c_int32, c_int32,
                               c_int32, c_int64, c_void_p, POINTER(GsExecStats)]),
+    "gs_exec_run_arrivals": (c_int32, [c_void_p, c_int32, c_void_p, c_int32, c_int32, POINTER(c_int32), c_int32,
+                                       c_int32, c_int32, c_int64, c_void_p, POINTER(GsExecStats)]),
     "gs_exec_stage": (c_int32, [c_void_p, c_int32, POINTER(c_int32), c_int32, c_int32]),
     "gs_exec_unstage": (None, []),
     "gs_gemm_bf16": (c_int32, [c_void_p, c_int64, c_void_p, c_int64, c_void_p, c_void_p, c_int64, c_int32,
@@ -167,20 +170,25 @@ class ExecResult:
 
 
 def run_jobs(jobs: list[Job], policy: str = "mgb-warps", devices: list[int] = (0,), workers: int = 8,
-             mode: int = MODE_DEVICE, ledger_bytes: int = 0) -> ExecResult:
-    """Run a job list under `policy` (wall clock; see module docstring)."""
+             mode: int = MODE_DEVICE, ledger_bytes: int = 0, arrivals_ms=None) -> ExecResult:
+    """Run a job list under `policy` (wall clock; see module docstring).
+    `arrivals_ms`: optional non-decreasing arrival time per job (ms)."""
     code, ratio = policy_code(policy)
     arr = (GsJobDesc * len(jobs))(*[j.desc() for j in jobs])
     recs = (GsJobRecord * len(jobs))()
     st = GsExecStats()
     devs = (c_int32 * len(devices))(*devices)
-    nat.check(lib().gs_exec_run(arr, len(jobs), code, ratio, devs, len(devices), workers, mode,
-                                int(ledger_bytes), recs, ctypes.byref(st)))
+    arrv = None
+    if arrivals_ms is not None:
+        arrv = (c_double * len(jobs))(*[float(a) for a in arrivals_ms])
+    nat.check(lib().gs_exec_run_arrivals(arr, len(jobs), arrv, code, ratio, devs, len(devices), workers, mode,
+                                         int(ledger_bytes), recs, ctypes.byref(st)))
     rows = []
     for j, r in zip(jobs, recs):
         rows.append({"kind": j.kind, "n": j.n, "state": ("done", "oom", "rejected")[r.state],
-                     "device": r.device, "pull_ms": r.pull_ms, "admit_ms": r.admit_ms, "end_ms": r.end_ms,
-                     "turnaround_ms": r.end_ms, "wait_ms": r.wait_ms, "compute_ms": r.compute_ms,
+                     "device": r.device, "arrival_ms": r.arrival_ms, "pull_ms": r.pull_ms,
+                     "admit_ms": r.admit_ms, "end_ms": r.end_ms, "turnaround_ms": r.end_ms - r.arrival_ms,
+                     "wait_ms": r.wait_ms, "compute_ms": r.compute_ms,
                      "mem_bytes": r.mem_bytes, "h2d_bytes": r.h2d_bytes, "d2h_bytes": r.d2h_bytes,
                      "checksum": r.checksum, "n_kernels": r.n_kernels})
     return ExecResult(rows, st.makespan_ms, st.completed, st.crashed, st.oom, st.rejected,

@@ -80,3 +80,12 @@ def test_yolov3_tiny_job_matches_torch_reference(S, N):
     err = abs(got.astype("float64") - want.astype("float64"))
     assert got.shape == want.shape
     assert err.max() < 5e-2 and err.mean() < 2e-3, (err.max(), err.mean())
+
+
+def test_yolo_probe_matches_host_footprint_and_reports_gemm_smem():
+    from paper_2107_08538_b200 import catalog as C
+
+    job = W.Job("yolo", n=416, m=4, iters=1, seed=1)
+    p = W.probe(job)
+    assert p.mem_bytes == C.host_footprint(job)
+    assert p.smem_per_block > 64 * 1024  # the tcgen05 GEMM's dynamic shared-memory ring is counted

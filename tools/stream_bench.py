@@ -1,0 +1,114 @@
+"""BASELINE cfg 2 and cfg 3 on one B200 (the bench line is cfg 1).
+
+    python tools/stream_bench.py --config 2 [--jobs 32] [--seed 1]
+    python tools/stream_bench.py --config 3 [--jobs 128] [--seed 1] [--load 0.7]
+
+cfg 2  Darknet YOLOv3-tiny inference mix (random init, batch 1-64, image
+       edge 416-1024) whose summed footprint exceeds the device: run under
+       mgb-warps (memory-safe), cg:<r> (no memory check) and sa; reports
+       jobs/s, mean turnaround and OOMs per policy.
+cfg 3  a 128-job stream mixing cfg 1's Rodinia jobs with cfg 2's Darknet
+       jobs, Poisson arrivals (seeded) at the offered load `--load` of one
+       GPU's solo service rate; reports jobs/s, mean turnaround and the
+       per-kernel slowdown against each job run alone
+       ((co-located / solo device time - 1) * 100, metrics.py:75-79).
+Inputs are synthesized on the device by each job (unstaged), so every
+job's time includes its input generation.  One JSON line per policy.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import random
+import statistics
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+from paper_2107_08538_b200 import catalog as C  # noqa: E402
+from paper_2107_08538_b200 import workloads as W  # noqa: E402
+
+GIB = 1 << 30
+
+
+def darknet_mix(n: int, seed: int) -> list[W.Job]:
+    rng = random.Random(f"{seed}|darknet|{n}")
+    out = []
+    for i in range(n):
+        S = rng.choice([416, 608, 832, 1024])
+        B = rng.choice([1, 2, 4, 8, 16, 32, 64])
+        out.append(W.Job("yolo", n=S, m=B, iters=1, seed=seed * 1000 + i))
+    return out
+
+
+def summarize(res, solo=None) -> dict:
+    done = [r for r in res.records if r["state"] == "done"]
+    d = {
+        "jobs_per_s": round(res.completed / (res.makespan_ms / 1000.0), 4) if res.makespan_ms else 0.0,
+        "makespan_ms": round(res.makespan_ms, 1),
+        "mean_turnaround_ms": round(statistics.fmean(r["turnaround_ms"] for r in done), 1) if done else None,
+        "mean_wait_ms": round(statistics.fmean(r["wait_ms"] for r in done), 1) if done else None,
+        "completed": res.completed, "oom": res.oom, "crashed": res.crashed,
+    }
+    if solo:
+        sl = [(r["compute_ms"] / solo[i] - 1.0) * 100.0 for i, r in enumerate(res.records)
+              if r["state"] == "done" and solo[i] > 0]
+        d["kernel_slowdown_pct_mean"] = round(statistics.fmean(sl), 2) if sl else None
+        d["kernel_slowdown_pct_median"] = round(statistics.median(sl), 2) if sl else None
+    return d
+
+
+def cfg2(args):
+    jobs = darknet_mix(args.jobs, args.seed)
+    foot = sum(C.host_footprint(j) for j in jobs)
+    for policy in ("mgb-warps", "cg:4", "sa"):
+        res = W.run_jobs(jobs, policy=policy, workers=args.workers)
+        line = {"config": "cfg2 darknet yolov3-tiny mix", "policy": policy, "jobs": len(jobs),
+                "sum_footprint_gib": round(foot / GIB, 1), **summarize(res)}
+        print(json.dumps(line), flush=True)
+
+
+def cfg3(args):
+    rod = [m.job for m in C.gen_mix("3:1", args.jobs // 2, seed=args.seed)]
+    dk = darknet_mix(args.jobs - len(rod), args.seed + 1)
+    rng = random.Random(f"{args.seed}|cfg3|{args.jobs}")
+    jobs = rod + dk
+    rng.shuffle(jobs)
+    # isolated device time of every job (the slowdown baseline) and the
+    # solo service rate the offered load is measured against
+    solo = []
+    for j in jobs:
+        _, rec = W.run_solo(j)
+        solo.append(rec.compute_ms)
+    W.run_solo(jobs[0])
+    mean_service_ms = statistics.fmean(solo)
+    lam = args.load / mean_service_ms  # jobs per ms
+    t, arrivals = 0.0, []
+    for _ in jobs:
+        t += rng.expovariate(lam)
+        arrivals.append(t)
+    for policy in ("mgb-warps", "sa"):
+        res = W.run_jobs(jobs, policy=policy, workers=args.workers, arrivals_ms=arrivals)
+        line = {"config": "cfg3 poisson rodinia+darknet stream", "policy": policy, "jobs": len(jobs),
+                "offered_load": args.load, "mean_solo_ms": round(mean_service_ms, 2),
+                "arrival_span_ms": round(arrivals[-1], 1), **summarize(res, solo)}
+        print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", type=int, choices=[2, 3], required=True)
+    ap.add_argument("--jobs", type=int, default=None)
+    ap.add_argument("--seed", type=int, default=1)
+    ap.add_argument("--workers", type=int, default=8)
+    ap.add_argument("--load", type=float, default=0.7)
+    args = ap.parse_args()
+    if args.jobs is None:
+        args.jobs = 32 if args.config == 2 else 128
+    (cfg2 if args.config == 2 else cfg3)(args)
+
+
+if __name__ == "__main__":
+    main()
