@@ -146,7 +146,9 @@ __global__ void __launch_bounds__(128, 1) gemm_bf16_tc(const __grid_constant__ C
 #pragma unroll
           for (int i = 0; i < 32; i += 4) *reinterpret_cast<float4 *>(o + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
         } else {
-          for (int i = 0; i < 32 && col0 + i < g.n; ++i) o[i] = v[i];
+#pragma unroll
+          for (int i = 0; i < 32; ++i)
+            if (col0 + i < g.n) o[i] = v[i];
         }
       } else {
         __nv_bfloat16 *o = reinterpret_cast<__nv_bfloat16 *>(g.out) + (int64_t)row * g.ldo + col0;
@@ -163,7 +165,9 @@ __global__ void __launch_bounds__(128, 1) gemm_bf16_tc(const __grid_constant__ C
             *reinterpret_cast<uint4 *>(o + i) = q;
           }
         } else {
-          for (int i = 0; i < 32 && col0 + i < g.n; ++i) o[i] = __float2bfloat16_rn(v[i]);
+#pragma unroll
+          for (int i = 0; i < 32; ++i)
+            if (col0 + i < g.n) o[i] = __float2bfloat16_rn(v[i]);
         }
       }
     }

@@ -1083,6 +1083,10 @@ __device__ void exec_cmd(const KParams &p, Smem &S, int *dyn, const Cmd &c, gs_d
 __device__ void writeback(const KParams &p, int *dyn, Smem &S, int lane) {
   led_to_stage(p, dyn, S, lane);
   stage(p, dyn, S, false, lane);
+  // every lane must have read the dirty flags (inside stage) before any lane
+  // clears them — otherwise a fast lane 0 clears device d's flag while other
+  // lanes still have d's chunks to write and they skip them
+  __syncwarp();
   const int nw = sizeof(SchedState) / 4;
   for (int i = lane; i < nw; i += 32)
     reinterpret_cast<int32_t *>(p.st)[i] = reinterpret_cast<const int32_t *>(&S.st)[i];
