@@ -139,7 +139,7 @@ std::vector<Shape> job_launches(const gs_job_desc &j) {
     case GS_JOB_NEEDLE:
       return {{(const void *)needle_bands, needle_grid(j), 32 * kNwWarps}};
     case GS_JOB_LUD:
-      return {{(const void *)lud_diagonal, 1, BS}, {(const void *)lud_perimeter, (int)(j.n / BS), 2 * BS},
+      return {{(const void *)lud_panel, (int)(j.n / BS), 2 * BS},
               {(const void *)lud_internal, g, 256}};
     case GS_JOB_YOLO:
       return gemm_launches(j);
@@ -334,12 +334,12 @@ int run_kernels(const gs_job_desc &j, std::vector<void *> &buf, cudaStream_t st,
     case GS_JOB_LUD: {
       float *a = (float *)buf[0];
       for (int o = 0; o < n; o += BS) {
-        lud_diagonal<<<1, BS, 0, st>>>(a, (int)n, o);
+        const int panels = (int)((n - o) / BS - 1);
+        lud_panel<<<panels > 0 ? panels : 1, 2 * BS, 0, st>>>(a, (int)n, o);
         ++launches;
         if (o + BS >= n) break;
-        lud_perimeter<<<(int)((n - o) / BS - 1), 2 * BS, 0, st>>>(a, (int)n, o);
         lud_internal<<<g, 256, 0, st>>>(a, (int)n, o);
-        launches += 2;
+        ++launches;
       }
       *out_idx = 0;
       break;

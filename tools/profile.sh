@@ -7,7 +7,7 @@
 set -u
 TAG=${1:-r01}
 shift || true
-WANT=${*:-"hotspot srad kmeans bfs needle lud bpfwd bpadj gemm decide launches"}
+WANT=${*:-"hotspot srad kmeans bfs needle lud ludp bpfwd bpadj gemm decide launches"}
 OUT=gpurun_out
 mkdir -p $OUT
 export GS_NO_RING=1   # ncu serializes kernels: use one decision launch per call
@@ -24,6 +24,7 @@ cap kmeans kmeans_assign 2 python tools/debug_job.py kmeans 8000000 4 34
 cap bfs bfs_expand 8 python tools/debug_job.py bfs 48000000
 cap needle needle_bands 0 python tools/debug_job.py needle 16384
 cap lud lud_internal 20 python tools/debug_job.py lud 6144
+cap ludp lud_panel 20 python tools/debug_job.py lud 6144
 cap bpfwd bp_forward 1 python tools/debug_job.py backprop 32000000 2 16
 cap bpadj bp_adjust 1 python tools/debug_job.py backprop 32000000 2 16
 cap gemm gemm_bf16_tc 12 python tools/debug_job.py yolo 416 1 32
