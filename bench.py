@@ -38,6 +38,14 @@ METRIC = "job-mix jobs/s + mean turnaround at 1/2/4/8 B200 vs one-job-per-GPU; O
 UNIT = "jobs/s"
 
 
+_T0 = time.time()
+
+
+def log(msg: str) -> None:
+    """Progress on stderr (the JSON line stays the only stdout output)."""
+    print(f"[bench +{time.time() - _T0:7.1f}s] {msg}", file=sys.stderr, flush=True)
+
+
 def peaks() -> dict:
     try:
         with open(os.path.join(REPO, "MEASURED_PEAKS.json")) as f:
@@ -91,8 +99,9 @@ class Clocks:
 
 def run_steps(W, jobs, policy, device, workers, mode, steps, warmup, torch):
     """W warm-up + K timed steps; device-timed with CUDA events."""
-    for _ in range(warmup):
-        W.run_jobs(jobs, policy=policy, devices=[device], workers=workers, mode=mode)
+    for w in range(warmup):
+        r = W.run_jobs(jobs, policy=policy, devices=[device], workers=workers, mode=mode)
+        log(f"warmup {w} {policy} mode={mode}: {r.makespan_ms:.1f} ms, {r.completed} done, {r.oom} oom")
     times, results = [], []
     for _ in range(steps):
         torch.cuda.synchronize()
@@ -104,6 +113,7 @@ def run_steps(W, jobs, policy, device, workers, mode, steps, warmup, torch):
         torch.cuda.synchronize()
         times.append(e0.elapsed_time(e1))
         results.append(res)
+        log(f"step {policy} mode={mode}: {times[-1]:.1f} ms, {res.completed} done, {res.oom} oom")
     return times, results
 
 
@@ -131,6 +141,7 @@ def kernel_rooflines(W, C, jobs, device, pk):
         seen.setdefault(mj.job.kind, mj.job)
     hbm = pk["hbm_gbs"]
     for kind, job in seen.items():
+        log(f"solo {kind} n={job.n}")
         W.run_solo(job, device)  # warm-up
         recs = [W.run_solo(job, device)[1] for _ in range(2)]
         ms = min(r.compute_ms for r in recs)
@@ -263,6 +274,7 @@ def main() -> int:
     device = local
 
     # ---- device mode: inputs staged in HBM before the timed region ----
+    log(f"staging {len(jobs)} jobs (device mode)")
     W.stage(jobs, [device], W.MODE_DEVICE)
     if dist:
         dist.barrier()
@@ -280,6 +292,7 @@ def main() -> int:
     # ---- e2e mode: pinned host inputs, H2D + D2H inside the timed region ----
     e2e = sa_e2e = None
     if not args.skip_e2e:
+        log("staging (e2e mode: pinned host inputs)")
         W.stage(jobs, [device], W.MODE_E2E)
         et, er = run_steps(W, jobs, args.policy, device, args.workers, W.MODE_E2E, args.steps, 1, torch)
         e2e = summarize(er, et)

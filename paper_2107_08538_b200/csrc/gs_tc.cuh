@@ -20,15 +20,26 @@ __device__ __forceinline__ void fence_mbar_init() { asm volatile("fence.mbarrier
 __device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
 }
+// Wait for the phase with parity `phase` to complete.  A watchdog traps
+// after ~2 s so a protocol bug fails the launch instead of hanging the GPU.
 __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t phase) {
   const uint32_t a = smem_u32(bar);
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, 1000000;\n\t"
-      "@!p bra WAIT_%=;\n\t}" ::"r"(a),
-      "r"(phase)
-      : "memory");
+  uint32_t done = 0;
+  unsigned long long t0 = 0;
+  for (int spin = 0;; ++spin) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, 100000;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(a), "r"(phase)
+        : "memory");
+    if (done) return;
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    if (spin == 0) t0 = t;
+    else if (t - t0 > 2000000000ull) __trap();
+  }
 }
 
 // ---- TMA -------------------------------------------------------------------------
