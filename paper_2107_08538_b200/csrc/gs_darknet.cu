@@ -295,7 +295,7 @@ std::vector<Shape> gemm_launches(const gs_job_desc &j) {
     if (L.type == CONV)
       bn_max = std::max(bn_max, gemm_pick_bn((int)((int64_t)L.in.n * L.in.h * L.in.w), L.cout));
   const int64_t pix0 = (int64_t)j.m * j.n * j.n;
-  Shape g{gemm_kernel_fn(bn_max), kSMs, 128};
+  Shape g{gemm_kernel_fn(bn_max), kSMs, gemm_block_threads()};
   g.dsmem = (int)gemm_smem_for(bn_max);
   return {g, {(const void *)im2row3, grid_for(pix0 * 4), kThr}, {(const void *)maxpool2, grid_for(pix0), kThr}};
 }

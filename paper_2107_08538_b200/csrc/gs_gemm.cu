@@ -46,6 +46,8 @@ constexpr size_t gemm_smem_bytes() {
   return (size_t)kGemmStages * (kGemmBM + BN) * kGemmBK * 2 + 1024 + 256;
 }
 
+constexpr int kGemmThreads = 192;  // warp 0 TMA, warp 1 MMA, warps 2-5 epilogue
+
 __device__ __forceinline__ float leaky(float v) { return v > 0.0f ? v : 0.1f * v; }
 // YOLO layer (Darknet yolo_layer forward): logistic on x, y, objectness and
 // class scores of each 85-channel anchor group; w, h (entries 2, 3) linear.
@@ -54,20 +56,71 @@ __device__ __forceinline__ float yolo_act(float v, int col) {
   return (e == 2 || e == 3) ? v : 1.0f / (1.0f + expf(-v));
 }
 
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(tc::smem_u32(bar)) : "memory");
+}
+
+// Bias + activation of one row's 32 columns, stored as bf16 or fp32.
+__device__ __forceinline__ void epilogue_store(const GemmArgs &g, int row, int col0, float (&v)[32]) {
+  if (row >= g.m || col0 >= g.n) return;
+#pragma unroll
+  for (int i = 0; i < 32; ++i) {
+    float x = v[i];
+    if (g.bias && col0 + i < g.n) x += __ldg(g.bias + col0 + i);
+    v[i] = g.act == 1 ? leaky(x) : (g.act == 2 ? yolo_act(x, col0 + i) : x);
+  }
+  const bool whole = col0 + 32 <= g.n;
+  if (g.out_f32) {
+    float *o = reinterpret_cast<float *>(g.out) + (int64_t)row * g.ldo + col0;
+    if (whole && ((reinterpret_cast<uintptr_t>(o) & 15) == 0)) {
+#pragma unroll
+      for (int i = 0; i < 32; i += 4) *reinterpret_cast<float4 *>(o + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+    } else {
+#pragma unroll
+      for (int i = 0; i < 32; ++i)
+        if (col0 + i < g.n) o[i] = v[i];
+    }
+  } else {
+    __nv_bfloat16 *o = reinterpret_cast<__nv_bfloat16 *>(g.out) + (int64_t)row * g.ldo + col0;
+    if (whole && ((reinterpret_cast<uintptr_t>(o) & 15) == 0)) {
+#pragma unroll
+      for (int i = 0; i < 32; i += 8) {
+        uint4 q;
+        __nv_bfloat162 p0 = __floats2bfloat162_rn(v[i], v[i + 1]), p1 = __floats2bfloat162_rn(v[i + 2], v[i + 3]);
+        __nv_bfloat162 p2 = __floats2bfloat162_rn(v[i + 4], v[i + 5]), p3 = __floats2bfloat162_rn(v[i + 6], v[i + 7]);
+        q.x = *reinterpret_cast<uint32_t *>(&p0);
+        q.y = *reinterpret_cast<uint32_t *>(&p1);
+        q.z = *reinterpret_cast<uint32_t *>(&p2);
+        q.w = *reinterpret_cast<uint32_t *>(&p3);
+        *reinterpret_cast<uint4 *>(o + i) = q;
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < 32; ++i)
+        if (col0 + i < g.n) o[i] = __float2bfloat16_rn(v[i]);
+    }
+  }
+}
+
+// Persistent, warp-specialized: tiles are strided over the grid; the TMA
+// producer runs ahead through the 4-stage ring across tile boundaries, the
+// MMA warp alternates between two TMEM accumulators, and the four epilogue
+// warps drain accumulator t while the MMAs of tile t+1 run.
 template <int BN>
-__global__ void __launch_bounds__(128, 1) gemm_bf16_tc(const __grid_constant__ CUtensorMap ta,
-                                                       const __grid_constant__ CUtensorMap tb, GemmArgs g) {
+__global__ void __launch_bounds__(kGemmThreads, 1) gemm_bf16_tc(const __grid_constant__ CUtensorMap ta,
+                                                                const __grid_constant__ CUtensorMap tb, GemmArgs g) {
   using namespace tc;
   constexpr uint32_t A_BYTES = kGemmBM * kGemmBK * 2, B_BYTES = BN * kGemmBK * 2;
-  constexpr uint32_t TM_COLS = BN < 32 ? 32 : BN;
+  constexpr uint32_t TM_COLS = 2 * BN < 32 ? 32 : 2 * BN;  // two accumulators
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t *sa = smem;
   uint8_t *sb = smem + kGemmStages * A_BYTES;
   uint64_t *full = reinterpret_cast<uint64_t *>(sb + kGemmStages * B_BYTES);
   uint64_t *empty = full + kGemmStages;
-  uint64_t *done = empty + kGemmStages;
-  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(done + 1);
+  uint64_t *acc_full = empty + kGemmStages;  // [2]
+  uint64_t *acc_empty = acc_full + 2;        // [2]
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(acc_empty + 2);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   if (warp == 0 && lane == 0) {
@@ -77,7 +130,10 @@ __global__ void __launch_bounds__(128, 1) gemm_bf16_tc(const __grid_constant__ C
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
-    mbar_init(done, 1);
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&acc_full[a], 1);
+      mbar_init(&acc_empty[a], 4);  // one arrival per epilogue warp
+    }
     fence_mbar_init();
   }
   if (warp == 1) tmem_alloc<TM_COLS>(tmem_slot);
@@ -86,95 +142,72 @@ __global__ void __launch_bounds__(128, 1) gemm_bf16_tc(const __grid_constant__ C
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   constexpr uint32_t idesc = idesc_bf16_f32(kGemmBM, BN);
-
-  uint32_t stage = 0, phase = 0, tile_phase = 0;
   const int tiles = g.m_tiles * g.n_tiles;
-  for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
-    const int mt = tile / g.n_tiles, nt = tile % g.n_tiles;
-    if (warp == 0 && lane == 0) {
-      // TMA producer
-      for (int kb = 0; kb < g.k_blocks; ++kb) {
-        mbar_wait(&empty[stage], phase ^ 1);
-        mbar_expect_tx(&full[stage], A_BYTES + B_BYTES);
-        tma_load_2d(sa + stage * A_BYTES, &ta, &full[stage], kb * kGemmBK, mt * kGemmBM);
-        tma_load_2d(sb + stage * B_BYTES, &tb, &full[stage], kb * kGemmBK, nt * BN);
-        if (++stage == kGemmStages) {
-          stage = 0;
-          phase ^= 1;
-        }
-      }
-    } else if (warp == 1 && lane == 0) {
-      // MMA issuer
-      for (int kb = 0; kb < g.k_blocks; ++kb) {
-        mbar_wait(&full[stage], phase);
-        tc_fence_after();
-        const uint64_t ad = sdesc_k_sw128(sa + stage * A_BYTES);
-        const uint64_t bd = sdesc_k_sw128(sb + stage * B_BYTES);
-#pragma unroll
-        for (int k = 0; k < kGemmBK / 16; ++k)
-          mma_bf16(tmem, ad + 2 * k, bd + 2 * k, idesc, (kb | k) != 0);
-        mma_commit(&empty[stage]);  // frees the smem slot when these MMAs finish
-        if (++stage == kGemmStages) {
-          stage = 0;
-          phase ^= 1;
-        }
-      }
-      mma_commit(done);
-    }
-    __syncwarp();
-    // epilogue: TMEM lane = tile row; this warp owns lanes 32*warp .. +31
-    mbar_wait(done, tile_phase);
-    tile_phase ^= 1;
-    tc_fence_after();
-    const int row = mt * kGemmBM + warp * 32 + lane;
-#pragma unroll 1
-    for (int c0 = 0; c0 < BN; c0 += 32) {
-      float v[32];
-      tmem_ld32(tmem + ((uint32_t)(warp * 32) << 16) + c0, v);
-      const int col0 = nt * BN + c0;
-      if (row >= g.m || col0 >= g.n) continue;
-#pragma unroll
-      for (int i = 0; i < 32; ++i) {
-        float x = v[i];
-        if (g.bias && col0 + i < g.n) x += g.bias[col0 + i];
-        v[i] = g.act == 1 ? leaky(x) : (g.act == 2 ? yolo_act(x, col0 + i) : x);
-      }
-      const bool whole = col0 + 32 <= g.n;
-      if (g.out_f32) {
-        float *o = reinterpret_cast<float *>(g.out) + (int64_t)row * g.ldo + col0;
-        if (whole && ((reinterpret_cast<uintptr_t>(o) & 15) == 0)) {
-#pragma unroll
-          for (int i = 0; i < 32; i += 4) *reinterpret_cast<float4 *>(o + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
-        } else {
-#pragma unroll
-          for (int i = 0; i < 32; ++i)
-            if (col0 + i < g.n) o[i] = v[i];
-        }
-      } else {
-        __nv_bfloat16 *o = reinterpret_cast<__nv_bfloat16 *>(g.out) + (int64_t)row * g.ldo + col0;
-        if (whole && ((reinterpret_cast<uintptr_t>(o) & 15) == 0)) {
-#pragma unroll
-          for (int i = 0; i < 32; i += 8) {
-            uint4 q;
-            __nv_bfloat162 p0 = __floats2bfloat162_rn(v[i], v[i + 1]), p1 = __floats2bfloat162_rn(v[i + 2], v[i + 3]);
-            __nv_bfloat162 p2 = __floats2bfloat162_rn(v[i + 4], v[i + 5]), p3 = __floats2bfloat162_rn(v[i + 6], v[i + 7]);
-            q.x = *reinterpret_cast<uint32_t *>(&p0);
-            q.y = *reinterpret_cast<uint32_t *>(&p1);
-            q.z = *reinterpret_cast<uint32_t *>(&p2);
-            q.w = *reinterpret_cast<uint32_t *>(&p3);
-            *reinterpret_cast<uint4 *>(o + i) = q;
+
+  if (warp == 0) {
+    if (lane == 0) {  // TMA producer
+      uint32_t stage = 0, phase = 0;
+      for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+        const int mt = tile / g.n_tiles, nt = tile % g.n_tiles;
+        for (int kb = 0; kb < g.k_blocks; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          mbar_expect_tx(&full[stage], A_BYTES + B_BYTES);
+          tma_load_2d(sa + stage * A_BYTES, &ta, &full[stage], kb * kGemmBK, mt * kGemmBM);
+          tma_load_2d(sb + stage * B_BYTES, &tb, &full[stage], kb * kGemmBK, nt * BN);
+          if (++stage == kGemmStages) {
+            stage = 0;
+            phase ^= 1;
           }
-        } else {
-#pragma unroll
-          for (int i = 0; i < 32; ++i)
-            if (col0 + i < g.n) o[i] = __float2bfloat16_rn(v[i]);
         }
       }
     }
-    tc_fence_before();
-    __syncthreads();  // TMEM is free for the next tile's MMAs
-    tc_fence_after();
+  } else if (warp == 1) {
+    if (lane == 0) {  // MMA issuer
+      uint32_t stage = 0, phase = 0;
+      int t = 0;
+      for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x, ++t) {
+        const int acc = t & 1;
+        mbar_wait(&acc_empty[acc], ((t >> 1) & 1) ^ 1);  // epilogue drained this accumulator
+        tc_fence_after();
+        const uint32_t d = tmem + acc * BN;
+        for (int kb = 0; kb < g.k_blocks; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint64_t ad = sdesc_k_sw128(sa + stage * A_BYTES);
+          const uint64_t bd = sdesc_k_sw128(sb + stage * B_BYTES);
+#pragma unroll
+          for (int k = 0; k < kGemmBK / 16; ++k) mma_bf16(d, ad + 2 * k, bd + 2 * k, idesc, (kb | k) != 0);
+          mma_commit(&empty[stage]);  // frees the smem slot when these MMAs finish
+          if (++stage == kGemmStages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        mma_commit(&acc_full[acc]);  // accumulator ready for the epilogue
+      }
+    }
+  } else {
+    // epilogue warps 2..5: TMEM lane quarter (warp % 4) = tile rows 32q .. 32q+31
+    const int q = warp & 3;
+    int t = 0;
+    for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x, ++t) {
+      const int mt = tile / g.n_tiles, nt = tile % g.n_tiles;
+      const int acc = t & 1;
+      mbar_wait(&acc_full[acc], (t >> 1) & 1);
+      tc_fence_after();
+      const int row = mt * kGemmBM + q * 32 + lane;
+#pragma unroll 1
+      for (int c0 = 0; c0 < BN; c0 += 32) {
+        float v[32];
+        tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + acc * BN + c0, v);
+        epilogue_store(g, row, nt * BN + c0, v);
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&acc_empty[acc]);
+    }
   }
+  __syncthreads();
   if (warp == 1) tmem_dealloc<TM_COLS>(tmem);
 }
 
@@ -229,7 +262,7 @@ static int launch_bn(const CUtensorMap &ta, const CUtensorMap &tb, GemmArgs g, i
   g.n_tiles = (g.n + BN - 1) / BN;
   const int tiles = g.m_tiles * g.n_tiles;
   const int grid = tiles < max_ctas ? tiles : max_ctas;
-  gemm_bf16_tc<BN><<<grid, 128, gemm_smem_bytes<BN>(), st>>>(ta, tb, g);
+  gemm_bf16_tc<BN><<<grid, kGemmThreads, gemm_smem_bytes<BN>(), st>>>(ta, tb, g);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return err(GS_ERR_CUDA, std::string("gemm launch: ") + cudaGetErrorString(e));
   return GS_OK;
@@ -274,6 +307,8 @@ int gemm_bf16(const void *A, int64_t lda, const void *B, int64_t ldb, const floa
     default: return launch_bn<256>(ta, tb, g, max_ctas, st);
   }
 }
+
+int gemm_block_threads() { return kGemmThreads; }
 
 size_t gemm_smem_for(int bn) {
   switch (bn) {
