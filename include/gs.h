@@ -216,7 +216,7 @@ int gs_sched_job_state(gs_sched *s, int32_t *sa_owner, int32_t *cg_counts,
  * its devices become ring commands (no launch, no wait for a free SM).
  * Capacities (pending queue, task handles, job handles) are fixed at start;
  * the host must not write the ledgers while the ring runs.  An idle
- * watchdog retires the kernel after 20 s; the next call relaunches it. */
+ * watchdog retires the kernel after 200 ms idle; the next call relaunches it. */
 int gs_sched_ring_start(gs_sched *s, int32_t max_pending, int32_t max_handles, int32_t max_jobs);
 int gs_sched_ring_stop(gs_sched *s);
 /* Decisions served so far (kernel-launched commands + ring commands). */

@@ -486,6 +486,7 @@ int gs_exec_run_arrivals(const gs_job_desc *jobs, int32_t n_jobs, const double *
   std::vector<std::thread> pool;
   for (int w = 0; w < workers; ++w) pool.emplace_back(worker, w);
   for (auto &t : pool) t.join();
+  gs_sched_ring_stop(sched);  // retire the resident decision kernel before draining the devices
   for (int d = 0; d < n_devices; ++d) {
     cudaSetDevice(cuda_devices[d]);
     cudaDeviceSynchronize();

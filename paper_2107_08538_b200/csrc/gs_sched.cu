@@ -1924,7 +1924,9 @@ int gs_sched_ring_start(gs_sched *s, int32_t max_pending, int32_t max_handles, i
   rc = sched_params(s, L);
   if (rc) return rc;
   s->ring_params = L.p;
-  s->ring_params.ring_idle_ns = 20LL * 1000 * 1000 * 1000;  // idle watchdog: 20 s
+  // idle watchdog: an idle ring retires after 200 ms (the next call relaunches
+  // it in ~10 us), so a resident decision kernel never pins the device for long
+  s->ring_params.ring_idle_ns = 200LL * 1000 * 1000;
   s->ring_smem = L.smem;
   if (!s->ring_stream) {
     int lo = 0, hi = 0;
