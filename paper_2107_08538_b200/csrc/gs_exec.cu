@@ -152,13 +152,15 @@ int run_job(const gs_job_desc &j, const Staged *stg, int mode, cudaStream_t st, 
       return err(GS_ERR_CUDA, std::string("cudaMallocAsync: ") + cudaGetErrorString(e));
     }
   }
-  if (cudaMallocAsync((void **)&dsum, 8, st) != cudaSuccess) {
+  // 32 B of job control: [0] the output digest, [1..] the kernels' tile tickets
+  if (cudaMallocAsync((void **)&dsum, 32, st) != cudaSuccess) {
     cudaGetLastError();
     dsum = nullptr;
     release();
     *oom = true;
     return GS_OK;
   }
+  CUE(cudaMemsetAsync(dsum, 0, 32, st));
   // inputs in
   for (size_t i = 0; i < bufs.size(); ++i) {
     if (bufs[i].role == IN || bufs[i].role == INOUT) {
@@ -186,7 +188,7 @@ int run_job(const gs_job_desc &j, const Staged *stg, int mode, cudaStream_t st, 
   CUE(cudaEventRecord(e0, st));
   int out_idx = 0;
   int64_t launches = 0;
-  int rc = run_kernels(j, buf, st, &out_idx, &launches, host_scalar);
+  int rc = run_kernels(j, buf, st, &out_idx, &launches, host_scalar, reinterpret_cast<unsigned *>(dsum + 1));
   if (rc) return rc;
   CUE(cudaEventRecord(e1, st));
   rec.n_kernels = (int32_t)launches;

@@ -68,7 +68,7 @@ std::vector<Buf> job_buffers(const gs_job_desc &j) {
       break;
     case GS_JOB_BACKPROP:
       b = {{(n + 1) * 4, IN}, {j.m * (n + 1) * 4, INOUT}, {j.m * (n + 1) * 4, SCR}, {80 * 4, INOUT},
-           {(int64_t)kSMs * 8 * kMaxHid * 8, SCR}};
+           {((n + 1 + kBpTile - 1) / kBpTile) * kMaxHid * 8, SCR}};  // one partial per tile
       break;
     case GS_JOB_NEEDLE:  // ref, score, band tickets + progress flags
       b = {{(n + 1) * (n + 1) * 4, IN}, {(n + 1) * (n + 1) * 4, INOUT}, {(n / 32 + 1) * 4, SCR}};
@@ -237,7 +237,7 @@ int generate_inputs(const gs_job_desc &j, const std::vector<void *> &dst, cudaSt
 // index of the buffer holding the primary output in *out_idx (hotspot and
 // srad ping-pong).  `kernels` counts launches.
 int run_kernels(const gs_job_desc &j, std::vector<void *> &buf, cudaStream_t st, int *out_idx, int64_t *kernels,
-                int32_t *host_scalar) {
+                int32_t *host_scalar, unsigned *tk) {
   const int g = job_grid(j);
   const int64_t n = j.n;
   int64_t launches = 0;
@@ -254,7 +254,7 @@ int run_kernels(const gs_job_desc &j, std::vector<void *> &buf, cudaStream_t st,
       int32_t n_in = 1;
       for (int32_t depth = 0; n_in > 0; ++depth) {
         CUW(cudaMemsetAsync(cnt, 0, 4, st));
-        bfs_expand<<<g, kThreads, 0, st>>>(row, col, level, vis, qa, n_in, qb, cnt, depth + 1);
+        bfs_expand<<<g, kThreads, 0, st>>>(row, col, level, vis, qa, n_in, qb, cnt, depth + 1, tk);
         ++launches;
         // Rodinia-style host round trip per level (the frontier size)
         CUW(cudaMemcpyAsync(host_scalar, cnt, 4, cudaMemcpyDeviceToHost, st));
@@ -270,7 +270,7 @@ int run_kernels(const gs_job_desc &j, std::vector<void *> &buf, cudaStream_t st,
       gs_hotspot_coeffs(&cc, &rx1, &ry1, &rz1);
       float *t = (float *)buf[0], *p = (float *)buf[1], *t2 = (float *)buf[2];
       for (int it = 0; it < j.iters; ++it) {
-        hotspot_step<<<g, dim3(32, 8), 0, st>>>(t, p, t2, (int)n, cc, rx1, ry1, rz1);
+        hotspot_step<<<g, dim3(32, 8), 0, st>>>(t, p, t2, (int)n, cc, rx1, ry1, rz1, tk);
         ++launches;
         std::swap(t, t2);
       }
@@ -282,7 +282,7 @@ int run_kernels(const gs_job_desc &j, std::vector<void *> &buf, cudaStream_t st,
       const int roi = n < 128 ? (int)n : 128;
       for (int it = 0; it < j.iters; ++it) {
         srad_stats<<<1, kThreads, 0, st>>>(J, (int)n, roi, q0);
-        srad_fused<<<g, dim3(32, 8), 0, st>>>(J, J2, (int)n, q0);
+        srad_fused<<<g, dim3(32, 8), 0, st>>>(J, J2, (int)n, q0, tk);
         launches += 2;
         std::swap(J, J2);
       }
@@ -301,7 +301,7 @@ int run_kernels(const gs_job_desc &j, std::vector<void *> &buf, cudaStream_t st,
         CUW(cudaMemcpy2DAsync(cent + f, nf * 4, x + (int64_t)f * n, 4, 4, GS_KMEANS_K, cudaMemcpyDeviceToDevice,
                               st));
       for (int it = 0; it < j.iters; ++it) {
-        kmeans_assign_fn(nf)<<<g, kThreads, 0, st>>>(x, n, nf, cent, mem, sumq, cnt);
+        kmeans_assign_fn(nf)<<<g, kThreads, 0, st>>>(x, n, nf, cent, mem, sumq, cnt, tk);
         kmeans_recenter<<<1, kThreads, 0, st>>>(cent, sumq, cnt, nf);
         launches += 2;
       }
@@ -315,9 +315,10 @@ int run_kernels(const gs_job_desc &j, std::vector<void *> &buf, cudaStream_t st,
       const int nh = (int)j.m;
       CUW(cudaMemsetAsync(ow1, 0, (size_t)nh * (n + 1) * 4, st));
       for (int it = 0; it < j.iters; ++it) {
-        bp_forward<<<g, kThreads, 0, st>>>(x, w1, n + 1, nh, partial);
-        bp_output<<<1, 32, 0, st>>>(partial, g, nh, state);
-        bp_adjust<<<g, kThreads, 0, st>>>(x, w1, ow1, n + 1, nh, state);
+        const int ntiles = (int)((n + 1 + kBpTile - 1) / kBpTile);
+        bp_forward<<<g, kThreads, 0, st>>>(x, w1, n + 1, nh, partial, tk);
+        bp_output<<<1, 32, 0, st>>>(partial, ntiles, nh, state);
+        bp_adjust<<<g, kThreads, 0, st>>>(x, w1, ow1, n + 1, nh, state, tk);
         launches += 3;
       }
       *out_idx = 1;
@@ -338,7 +339,7 @@ int run_kernels(const gs_job_desc &j, std::vector<void *> &buf, cudaStream_t st,
         lud_panel<<<panels > 0 ? panels : 1, 2 * BS, 0, st>>>(a, (int)n, o);
         ++launches;
         if (o + BS >= n) break;
-        lud_internal<<<g, 256, 0, st>>>(a, (int)n, o);
+        lud_internal<<<g, 256, 0, st>>>(a, (int)n, o, tk);
         ++launches;
       }
       *out_idx = 0;
