@@ -137,6 +137,8 @@ struct KParams {
   const gs_probe *sweep_probes;
   Ring *ring;
   long long ring_idle_ns;
+  int ring_sleep_ns;  // poll interval of the idle decision warp
+  int pad2;
 };
 
 struct SLed {
@@ -1100,6 +1102,11 @@ __device__ __forceinline__ long long ld_acquire_sys(const long long *a) {
   asm volatile("ld.acquire.sys.global.b64 %0, [%1];" : "=l"(v) : "l"(a) : "memory");
   return v;
 }
+__device__ __forceinline__ long long ld_relaxed_sys(const long long *a) {
+  long long v;
+  asm volatile("ld.relaxed.sys.global.b64 %0, [%1];" : "=l"(v) : "l"(a) : "memory");
+  return v;
+}
 __device__ __forceinline__ void st_release_sys(long long *a, long long v) {
   asm volatile("st.release.sys.global.b64 [%0], %1;" ::"l"(a), "l"(v) : "memory");
 }
@@ -1153,14 +1160,17 @@ __global__ void __launch_bounds__(kThreads, 1) gs_interp_kernel(KParams p) {
       long long t = 0;
       if (lane == 0) {
         const unsigned long long t0 = globaltimer();
-        while ((t = ld_acquire_sys(&ring->tail)) <= processed) {
-          __nanosleep(256);
+        // relaxed polling (no per-poll acquire fence); one acquire once the
+        // tail moved orders the command reads after it
+        while ((t = ld_relaxed_sys(&ring->tail)) <= processed) {
+          __nanosleep(p.ring_sleep_ns);
           if (globaltimer() - t0 > (unsigned long long)p.ring_idle_ns) {
             t = -1;
             break;
           }
         }
       }
+      if (lane == 0 && t >= 0) t = ld_acquire_sys(&ring->tail);
       t = __shfl_sync(kFull, t, 0);
       if (t < 0) break;  // idle watchdog: the host relaunches on demand
       const int slot = (int)(processed % kRingSlots);
@@ -1927,11 +1937,16 @@ int gs_sched_ring_start(gs_sched *s, int32_t max_pending, int32_t max_handles, i
   // idle watchdog: an idle ring retires after 200 ms (the next call relaunches
   // it in ~10 us), so a resident decision kernel never pins the device for long
   s->ring_params.ring_idle_ns = 200LL * 1000 * 1000;
+  {
+    const char *sl = getenv("GS_RING_SLEEP_NS");
+    s->ring_params.ring_sleep_ns = sl ? atoi(sl) : 1000;
+  }
   s->ring_smem = L.smem;
   if (!s->ring_stream) {
     int lo = 0, hi = 0;
     CU(cudaDeviceGetStreamPriorityRange(&lo, &hi));
-    CU(cudaStreamCreateWithPriority(&s->ring_stream, cudaStreamNonBlocking, hi));
+    const char *pr = getenv("GS_RING_PRIO");  // experiment knob: 0 = default priority
+    CU(cudaStreamCreateWithPriority(&s->ring_stream, cudaStreamNonBlocking, (pr && pr[0] == '0') ? lo : hi));
   }
   memset(s->ring.h, 0, sizeof(Ring));
   rc = ring_launch(s);

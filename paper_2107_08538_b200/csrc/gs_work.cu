@@ -52,9 +52,9 @@ std::vector<Buf> job_buffers(const gs_job_desc &j) {
   const int64_t n = j.n;
   switch (j.kind) {
     case GS_JOB_BFS:
-      // row_ptr, col, level, frontier queues, counter, visited bitmap
-      b = {{(n + 1) * 4, IN}, {n * GS_BFS_DEGREE * 4, IN}, {n * 4, OUT}, {n * 4, SCR}, {n * 4, SCR}, {16, SCR},
-           {(n / 32 + 1) * 4, SCR}};
+      // row_ptr, col, level, then the frontier / visited / snapshot bitmaps and the counter
+      b = {{(n + 1) * 4, IN}, {n * GS_BFS_DEGREE * 4, IN}, {n * 4, OUT}, {(n / 32 + 1) * 4, SCR},
+           {(n / 32 + 1) * 4, SCR}, {(n / 32 + 1) * 4, SCR}, {16, SCR}};
       break;
     case GS_JOB_HOTSPOT:
       b = {{n * n * 4, INOUT}, {n * n * 4, IN}, {n * n * 4, SCR}};
@@ -70,8 +70,8 @@ std::vector<Buf> job_buffers(const gs_job_desc &j) {
       b = {{(n + 1) * 4, IN}, {j.m * (n + 1) * 4, INOUT}, {j.m * (n + 1) * 4, SCR}, {80 * 4, INOUT},
            {((n + 1 + kBpTile - 1) / kBpTile) * kMaxHid * 8, SCR}};  // one partial per tile
       break;
-    case GS_JOB_NEEDLE:  // ref, score, band tickets + progress flags
-      b = {{(n + 1) * (n + 1) * 4, IN}, {(n + 1) * (n + 1) * 4, INOUT}, {(n / 32 + 1) * 4, SCR}};
+    case GS_JOB_NEEDLE:  // ref, score, band edge rows (2 slots x n tagged words)
+      b = {{(n + 1) * (n + 1) * 4, IN}, {(n + 1) * (n + 1) * 4, INOUT}, {2 * n * 8, SCR}};
       break;
     case GS_JOB_LUD:
       b = {{n * n * 4, INOUT}};
@@ -126,7 +126,7 @@ std::vector<Shape> job_launches(const gs_job_desc &j) {
   const int g = job_grid(j);
   switch (j.kind) {
     case GS_JOB_BFS:
-      return {{(const void *)bfs_expand, g, kThreads}};
+      return {{(const void *)bfs_expand, g, kThreads}, {(const void *)bfs_commit, g, kThreads}};
     case GS_JOB_HOTSPOT:
       return {{(const void *)hotspot_step, g, kThreads}};
     case GS_JOB_SRAD:
@@ -243,24 +243,23 @@ int run_kernels(const gs_job_desc &j, std::vector<void *> &buf, cudaStream_t st,
   int64_t launches = 0;
   switch (j.kind) {
     case GS_JOB_BFS: {
-      int32_t *row = (int32_t *)buf[0], *col = (int32_t *)buf[1], *level = (int32_t *)buf[2];
-      int32_t *qa = (int32_t *)buf[3], *qb = (int32_t *)buf[4], *cnt = (int32_t *)buf[5];
-      uint32_t *vis = (uint32_t *)buf[6];
+      const int32_t *row = (const int32_t *)buf[0], *col = (const int32_t *)buf[1];
+      int32_t *level = (int32_t *)buf[2];
+      uint32_t *F = (uint32_t *)buf[3], *V = (uint32_t *)buf[4], *S = (uint32_t *)buf[5];
+      auto *cnt = (unsigned long long *)buf[6];
+      const int64_t nwords = n / 32 + 1;
       CUW(cudaMemsetAsync(level, 0xff, n * 4, st));
       CUW(cudaMemsetAsync(level, 0, 4, st));
-      CUW(cudaMemsetAsync(qa, 0, 4, st));
-      CUW(cudaMemsetAsync(vis, 0, (n / 32 + 1) * 4, st));
-      CUW(cudaMemsetAsync(vis, 1, 1, st));  // source vertex 0
-      int32_t n_in = 1;
-      for (int32_t depth = 0; n_in > 0; ++depth) {
-        CUW(cudaMemsetAsync(cnt, 0, 4, st));
-        bfs_expand<<<g, kThreads, 0, st>>>(row, col, level, vis, qa, n_in, qb, cnt, depth + 1, tk);
-        ++launches;
-        // Rodinia-style host round trip per level (the frontier size)
-        CUW(cudaMemcpyAsync(host_scalar, cnt, 4, cudaMemcpyDeviceToHost, st));
+      for (uint32_t *bm : {F, V, S}) CUW(cudaMemsetAsync(bm, 1, 1, st));  // source vertex 0 (bitmaps zeroed)
+      for (int32_t depth = 0;; ++depth) {
+        CUW(cudaMemsetAsync(cnt, 0, 8, st));
+        bfs_expand<<<g, kThreads, 0, st>>>(row, col, F, V, nwords, tk);
+        bfs_commit<<<g, kThreads, 0, st>>>(V, S, F, level, n, nwords, depth + 1, cnt, tk);
+        launches += 2;
+        // Rodinia-style host round trip per level (new-vertex count)
+        CUW(cudaMemcpyAsync(host_scalar, cnt, 8, cudaMemcpyDeviceToHost, st));
         CUW(cudaStreamSynchronize(st));
-        n_in = *host_scalar;
-        std::swap(qa, qb);
+        if (*reinterpret_cast<unsigned long long *>(host_scalar) == 0) break;
       }
       *out_idx = 2;
       break;
@@ -325,9 +324,8 @@ int run_kernels(const gs_job_desc &j, std::vector<void *> &buf, cudaStream_t st,
       break;
     }
     case GS_JOB_NEEDLE: {
-      CUW(cudaMemsetAsync(buf[2], 0, (n / 32 + 1) * 4, st));
-      needle_bands<<<needle_grid(j), 32 * kNwWarps, 0, st>>>((int32_t *)buf[1], (const int32_t *)buf[0], (int)n,
-                                                            (int32_t *)buf[2]);
+      needle_bands<<<needle_grid(j), 32 * kNwWarps, 0, st>>>((int32_t *)buf[1], (const int32_t *)buf[0], (int)n, tk,
+                                                            (unsigned long long *)buf[2]);
       ++launches;
       *out_idx = 1;
       break;
