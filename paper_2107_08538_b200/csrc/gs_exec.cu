@@ -344,11 +344,13 @@ int gs_exec_run_arrivals(const gs_job_desc *jobs, int32_t n_jobs, const double *
   if (rc) return err(rc, gs_last_error());
   rc = gs_engine_reserve_handles(eng, n_jobs + 1);
   if (rc) return err(rc, gs_last_error());
-  // the resident decision warp serves every placement call of this run
-  // (GS_NO_RING=1 falls back to one decision launch per call, e.g. under
-  // ncu, which serializes kernels and would starve a persistent one)
-  const char *no_ring = getenv("GS_NO_RING");
-  if (!(no_ring && no_ring[0] == '1')) {
+  // Placement calls: one decision launch per call by default.  GS_RING=1
+  // serves them from the resident decision warp over the host-mapped command
+  // ring instead (lower decision latency, but measured 2-3x slower job
+  // mixes: the resident kernel delays co-located jobs' kernels — see
+  // DESIGN.md §4); never under ncu, which serializes kernels.
+  const char *ring_env = getenv("GS_RING");
+  if (ring_env && ring_env[0] == '1') {
     rc = gs_sched_ring_start(sched, n_jobs + 1, n_jobs + 1, n_jobs + 1);
     if (rc) return err(rc, gs_last_error());
   }

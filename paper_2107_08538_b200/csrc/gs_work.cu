@@ -96,6 +96,7 @@ int validate(const gs_job_desc &j) {
     case GS_JOB_NEEDLE:
     case GS_JOB_LUD:
       if (j.n % 32) return err(GS_ERR_CONFIG, "needle / lud sizes must be multiples of 32");
+      if (j.kind == GS_JOB_NEEDLE && j.n % 128) return err(GS_ERR_CONFIG, "needle sizes must be multiples of 128");
       break;
     case GS_JOB_KMEANS:
       if (j.m < 1 || j.m > kMaxF) return err(GS_ERR_CONFIG, "kmeans features must be 1..64");
@@ -119,7 +120,7 @@ int job_grid(const gs_job_desc &) { return 2 * kSMs; }
 // needle: one warp per 32-row band in flight, at most the job's SM share
 int needle_grid(const gs_job_desc &j) {
   const int bands = (int)(j.n / 32);
-  return std::min((bands + kNwWarps - 1) / kNwWarps, 2 * kSMs);
+  return std::min(bands, 4 * kSMs);
 }
 
 std::vector<Shape> job_launches(const gs_job_desc &j) {
@@ -137,7 +138,7 @@ std::vector<Shape> job_launches(const gs_job_desc &j) {
       return {{(const void *)bp_forward, g, kThreads}, {(const void *)bp_output, 1, 32},
               {(const void *)bp_adjust, g, kThreads}};
     case GS_JOB_NEEDLE:
-      return {{(const void *)needle_bands, needle_grid(j), 32 * kNwWarps}};
+      return {{(const void *)needle_bands, needle_grid(j), 32}};
     case GS_JOB_LUD:
       return {{(const void *)lud_panel, (int)(j.n / BS), 2 * BS},
               {(const void *)lud_internal, g, 256}};
@@ -324,8 +325,8 @@ int run_kernels(const gs_job_desc &j, std::vector<void *> &buf, cudaStream_t st,
       break;
     }
     case GS_JOB_NEEDLE: {
-      needle_bands<<<needle_grid(j), 32 * kNwWarps, 0, st>>>((int32_t *)buf[1], (const int32_t *)buf[0], (int)n, tk,
-                                                            (unsigned long long *)buf[2]);
+      needle_bands<<<needle_grid(j), 32, 0, st>>>((int32_t *)buf[1], (const int32_t *)buf[0], (int)n, tk,
+                                                  (unsigned long long *)buf[2]);
       ++launches;
       *out_idx = 1;
       break;

@@ -21,8 +21,8 @@ CASES = [
     ("srad", dict(n=512, iters=5, seed=4), 1e-5),
     ("kmeans", dict(n=200_000, m=34, iters=5, seed=6), "exact"),
     ("backprop", dict(n=300_000, m=16, iters=2, seed=7), 1e-5),
-    ("needle", dict(n=32, seed=2), "exact"),      # one band, one chunk
-    ("needle", dict(n=96, seed=3), "exact"),      # odd chunk count
+    ("needle", dict(n=128, seed=2), "exact"),     # one chunk, 4 bands
+    ("needle", dict(n=384, seed=3), "exact"),     # odd chunk count
     ("needle", dict(n=512, seed=1), "exact"),
     ("needle", dict(n=1024, seed=9), "exact"),
     ("needle", dict(n=4096, seed=4), "exact"),    # 128 bands in a wavefront

@@ -1,7 +1,7 @@
 """Executor timeline of one cfg-1 mix run: per job pull / admit / end and
 device time, to see where a step's wall time goes.
 
-    GS_NO_RING=0|1 python tools/exec_timeline.py [policy] [jobs] [workers]
+    GS_RING=0|1 python tools/exec_timeline.py [policy] [jobs] [workers]
 """
 
 import os
@@ -22,7 +22,7 @@ W.stage(jobs, [0], W.MODE_DEVICE)
 for rep in range(2):
     t = time.time()
     res = W.run_jobs(jobs, policy=policy, workers=workers)
-    print(f"run {rep} {policy} ring={os.environ.get('GS_NO_RING', '0') != '1'}: makespan {res.makespan_ms:.1f} ms "
+    print(f"run {rep} {policy} ring={os.environ.get('GS_RING', '0') == '1'}: makespan {res.makespan_ms:.1f} ms "
           f"wall {time.time() - t:.2f} s decision_ms {res.decision_ms:.1f} launches {res.decision_launches}",
           flush=True)
 for m, r in zip(mix, res.records):

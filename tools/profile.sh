@@ -10,7 +10,7 @@ shift || true
 WANT=${*:-"hotspot srad kmeans bfs needle lud ludp bpfwd bpadj gemm decide launches"}
 OUT=gpurun_out
 mkdir -p $OUT
-export GS_NO_RING=1   # ncu serializes kernels: use one decision launch per call
+unset GS_RING   # ncu serializes kernels: one decision launch per call (the default)
 NCU="ncu --set full --clock-control none --import-source on"
 cap() {  # name regex skip cmd...
   local name=$1 rx=$2 skip=$3; shift 3
