@@ -388,10 +388,17 @@ int gs_exec_run_arrivals(const gs_job_desc *jobs, int32_t n_jobs, const double *
   };
 
   auto worker = [&](int wid) {
-    std::vector<cudaStream_t> streams(n_devices, nullptr);
+    // two streams per device: latency-chain jobs (many dependent launches or
+    // a wavefront: bfs, lud, needle) run at high stream priority so their
+    // next kernel is not queued behind co-located streaming kernels; the
+    // bandwidth-bound kinds run at normal priority
+    std::vector<cudaStream_t> streams(n_devices, nullptr), hi_streams(n_devices, nullptr);
+    int prio_lo = 0, prio_hi = 0;
+    cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi);
     for (int d = 0; d < n_devices; ++d) {
       cudaSetDevice(cuda_devices[d]);
       cudaStreamCreateWithFlags(&streams[d], cudaStreamNonBlocking);
+      cudaStreamCreateWithPriority(&hi_streams[d], cudaStreamNonBlocking, prio_hi);
     }
     void *host_out = nullptr;
     if (out_cap) cudaHostAlloc(&host_out, out_cap, cudaHostAllocPortable);
@@ -462,7 +469,9 @@ int gs_exec_run_arrivals(const gs_job_desc *jobs, int32_t n_jobs, const double *
         stg = find_staged(jobs[j]);
       }
       bool oom = false;
-      int r = run_job(jobs[j], stg, mode, streams[dev], rec, &oom, host_out, out_cap, scalar, &kernels, hsum,
+      const bool chain = jobs[j].kind == GS_JOB_BFS || jobs[j].kind == GS_JOB_LUD || jobs[j].kind == GS_JOB_NEEDLE;
+      int r = run_job(jobs[j], stg, mode, chain ? hi_streams[dev] : streams[dev], rec, &oom, host_out, out_cap, scalar,
+                      &kernels, hsum,
                       cuda_devices[dev]);
       rec.end_ms = ms_since(t0);
       rec.state = oom ? 1 : 0;
@@ -482,6 +491,7 @@ int gs_exec_run_arrivals(const gs_job_desc *jobs, int32_t n_jobs, const double *
       redrive();
     }
     for (cudaStream_t s : streams) cudaStreamDestroy(s);
+    for (cudaStream_t s : hi_streams) cudaStreamDestroy(s);
     if (host_out) cudaFreeHost(host_out);
     cudaFreeHost(scalar);
     cudaFreeHost(hsum);

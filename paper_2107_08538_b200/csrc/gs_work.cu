@@ -39,6 +39,7 @@ int err(int code, const std::string &m) {
     if (e_ != cudaSuccess) return err(GS_ERR_CUDA, std::string(#call ": ") + cudaGetErrorString(e_)); \
   } while (0)
 
+constexpr int kBfsBatch = 4;                // bfs levels launched per host round trip
 constexpr int64_t kGranule = 2 << 20;       // device-pool allocation granule
 constexpr int64_t kHeap = 8 << 20;          // per-task heap (task_builder.py:29)
 constexpr int kThreads = 256;
@@ -54,7 +55,7 @@ std::vector<Buf> job_buffers(const gs_job_desc &j) {
     case GS_JOB_BFS:
       // row_ptr, col, level, then the frontier / visited / snapshot bitmaps and the counter
       b = {{(n + 1) * 4, IN}, {n * GS_BFS_DEGREE * 4, IN}, {n * 4, OUT}, {(n / 32 + 1) * 4, SCR},
-           {(n / 32 + 1) * 4, SCR}, {(n / 32 + 1) * 4, SCR}, {16, SCR}};
+           {(n / 32 + 1) * 4, SCR}, {(n / 32 + 1) * 4, SCR}, {8 * kBfsBatch, SCR}};
       break;
     case GS_JOB_HOTSPOT:
       b = {{n * n * 4, INOUT}, {n * n * 4, IN}, {n * n * 4, SCR}};
@@ -252,15 +253,19 @@ int run_kernels(const gs_job_desc &j, std::vector<void *> &buf, cudaStream_t st,
       CUW(cudaMemsetAsync(level, 0xff, n * 4, st));
       CUW(cudaMemsetAsync(level, 0, 4, st));
       for (uint32_t *bm : {F, V, S}) CUW(cudaMemsetAsync(bm, 1, 1, st));  // source vertex 0 (bitmaps zeroed)
-      for (int32_t depth = 0;; ++depth) {
-        CUW(cudaMemsetAsync(cnt, 0, 8, st));
-        bfs_expand<<<g, kThreads, 0, st>>>(row, col, F, V, nwords, tk);
-        bfs_commit<<<g, kThreads, 0, st>>>(V, S, F, level, n, nwords, depth + 1, cnt, tk);
-        launches += 2;
-        // Rodinia-style host round trip per level (new-vertex count)
-        CUW(cudaMemcpyAsync(host_scalar, cnt, 8, cudaMemcpyDeviceToHost, st));
+      // kBfsBatch levels per host round trip (Rodinia checks after every
+      // level): levels past the last one find an empty frontier and do no
+      // work, so a batch may overrun the depth harmlessly
+      for (int32_t depth = 0;; depth += kBfsBatch) {
+        CUW(cudaMemsetAsync(cnt, 0, 8 * kBfsBatch, st));
+        for (int q = 0; q < kBfsBatch; ++q) {
+          bfs_expand<<<g, kThreads, 0, st>>>(row, col, F, V, nwords, tk);
+          bfs_commit<<<g, kThreads, 0, st>>>(V, S, F, level, n, nwords, depth + q + 1, cnt + q, tk);
+        }
+        launches += 2 * kBfsBatch;
+        CUW(cudaMemcpyAsync(host_scalar, cnt + kBfsBatch - 1, 8, cudaMemcpyDeviceToHost, st));
         CUW(cudaStreamSynchronize(st));
-        if (*reinterpret_cast<unsigned long long *>(host_scalar) == 0) break;
+        if (*reinterpret_cast<unsigned long long *>(host_scalar) == 0) break;  // the batch's last level was empty
       }
       *out_idx = 2;
       break;
