@@ -252,12 +252,9 @@ static int make_tmap(CUtensorMap *m, const void *ptr, int64_t rows, int64_t k, i
 
 template <int BN>
 static int launch_bn(const CUtensorMap &ta, const CUtensorMap &tb, GemmArgs g, int max_ctas, cudaStream_t st) {
-  static std::once_flag once;
-  static cudaError_t attr_rc = cudaSuccess;
-  std::call_once(once, [] {
-    attr_rc = cudaFuncSetAttribute(gemm_bf16_tc<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)gemm_smem_bytes<BN>());
-  });
+  // per launch: the attribute is per device, and the executor may drive several
+  const cudaError_t attr_rc =
+      cudaFuncSetAttribute(gemm_bf16_tc<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gemm_smem_bytes<BN>());
   if (attr_rc != cudaSuccess) return err(GS_ERR_CUDA, std::string("gemm smem attribute: ") + cudaGetErrorString(attr_rc));
   g.n_tiles = (g.n + BN - 1) / BN;
   const int tiles = g.m_tiles * g.n_tiles;

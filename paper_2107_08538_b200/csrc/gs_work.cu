@@ -121,7 +121,7 @@ int job_grid(const gs_job_desc &) { return 2 * kSMs; }
 // needle: one warp per 32-row band in flight, at most the job's SM share
 int needle_grid(const gs_job_desc &j) {
   const int bands = (int)(j.n / 32);
-  return std::min(bands, 4 * kSMs);
+  return std::min(bands, 2 * kSMs);  // 96 KB of shared memory per band warp: 2 per SM
 }
 
 std::vector<Shape> job_launches(const gs_job_desc &j) {
@@ -139,7 +139,11 @@ std::vector<Shape> job_launches(const gs_job_desc &j) {
       return {{(const void *)bp_forward, g, kThreads}, {(const void *)bp_output, 1, 32},
               {(const void *)bp_adjust, g, kThreads}};
     case GS_JOB_NEEDLE:
-      return {{(const void *)needle_bands, needle_grid(j), 32}};
+    {
+      Shape sh{(const void *)needle_bands, needle_grid(j), 32};
+      sh.dsmem = kNwSmem;
+      return {sh};
+    }
     case GS_JOB_LUD:
       return {{(const void *)lud_panel, (int)(j.n / BS), 2 * BS},
               {(const void *)lud_internal, g, 256}};
@@ -330,8 +334,9 @@ int run_kernels(const gs_job_desc &j, std::vector<void *> &buf, cudaStream_t st,
       break;
     }
     case GS_JOB_NEEDLE: {
-      needle_bands<<<needle_grid(j), 32, 0, st>>>((int32_t *)buf[1], (const int32_t *)buf[0], (int)n, tk,
-                                                  (unsigned long long *)buf[2]);
+      CUW(cudaFuncSetAttribute(needle_bands, cudaFuncAttributeMaxDynamicSharedMemorySize, kNwSmem));  // per device
+      needle_bands<<<needle_grid(j), 32, kNwSmem, st>>>((int32_t *)buf[1], (const int32_t *)buf[0], (int)n, tk,
+                                                        (unsigned long long *)buf[2]);
       ++launches;
       *out_idx = 1;
       break;
