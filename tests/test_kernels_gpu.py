@@ -16,8 +16,10 @@ W = pytest.importorskip("paper_2107_08538_b200.workloads")
 CASES = [
     ("bfs", dict(n=200_000, seed=3), "exact"),
     ("bfs", dict(n=1_000_003, seed=8), "exact"),
-    ("hotspot", dict(n=512, iters=10, seed=2), 1e-5),
-    ("hotspot", dict(n=1024, iters=3, seed=5), 1e-5),
+    ("hotspot", dict(n=512, iters=10, seed=2), "exact"),   # 5 two-step passes
+    ("hotspot", dict(n=1024, iters=3, seed=5), "exact"),   # one two-step pass + one single step
+    ("hotspot", dict(n=128, iters=2, seed=6), "exact"),    # grid edges on every side of one tile column
+    ("hotspot", dict(n=256, iters=5, seed=7), "exact"),
     ("srad", dict(n=512, iters=5, seed=4), 1e-5),
     ("kmeans", dict(n=200_000, m=34, iters=5, seed=6), "exact"),
     ("backprop", dict(n=300_000, m=16, iters=2, seed=7), 1e-5),
