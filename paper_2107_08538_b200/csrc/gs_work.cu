@@ -116,7 +116,10 @@ int validate(const gs_job_desc &j) {
 // Grid of every workload kernel: the job's SM share (2 blocks of 256
 // threads per SM on all 148 SMs) — resident-sized, so a probe's
 // thread_blocks is a real placement demand for mgb-sm.
-int job_grid(const gs_job_desc &) { return 2 * kSMs; }
+int job_grid(const gs_job_desc &j) {
+  // srad's fused kernel is FP32-issue bound: 3 CTAs per SM (<= 85 registers)
+  return j.kind == GS_JOB_SRAD ? 3 * kSMs : 2 * kSMs;
+}
 
 // needle: one warp per 32-row band in flight, at most the job's SM share
 int needle_grid(const gs_job_desc &j) {
@@ -325,7 +328,7 @@ int run_kernels(const gs_job_desc &j, std::vector<void *> &buf, cudaStream_t st,
       float *w1 = (float *)buf[1], *ow1 = (float *)buf[2], *state = (float *)buf[3];
       double *partial = (double *)buf[4];
       const int nh = (int)j.m;
-      CUW(cudaMemsetAsync(ow1, 0, (size_t)nh * (n + 1) * 4, st));
+      // ow1 (momentum) is a SCR buffer: the executor zeroed it with the job's buffers
       for (int it = 0; it < j.iters; ++it) {
         const int ntiles = (int)((n + 1 + kBpTile - 1) / kBpTile);
         bp_forward<<<g, kThreads, 0, st>>>(x, w1, n + 1, nh, partial, tk);
