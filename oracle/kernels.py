@@ -68,7 +68,7 @@ def kmeans(n, nf, iters, seed):
 
 
 def backprop(n_in, n_hid, iters, seed):
-    w1 = np.zeros((n_hid, n_in + 1), np.float32)
+    w1 = np.zeros((n_in + 1, n_hid), np.float32)  # [input][hidden]
     w2 = np.zeros(n_hid + 1, np.float32)
     hid = np.zeros(n_hid + 1, np.float32)
     o = c_float()

@@ -228,7 +228,9 @@ void cpu_backprop(int64_t n_in, int32_t n_hid, int32_t iters, uint64_t seed, flo
     float ow2[64] = {0};
     float dh[64];
     for (int64_t i = 0; i < ni; ++i) x[i] = gs_bp_input(seed, (uint64_t)i);
-    for (int64_t i = 0; i < (int64_t)n_hid * ni; ++i) w1[i] = gs_bp_w1(seed, (uint64_t)i);
+    /* element-major [input][hidden] (Rodinia input_weights); value of (j, i) from index j * ni + i */
+    for (int j = 0; j < n_hid; ++j)
+        for (int64_t i = 0; i < ni; ++i) w1[i * n_hid + j] = gs_bp_w1(seed, (uint64_t)(j * ni + i));
     for (int j = 0; j <= n_hid; ++j) w2[j] = gs_bp_w2(seed, (uint64_t)j);
     float o = 0.0f;
     for (int32_t it = 0; it < iters; ++it) {
@@ -236,7 +238,7 @@ void cpu_backprop(int64_t n_in, int32_t n_hid, int32_t iters, uint64_t seed, flo
 #pragma omp parallel for
         for (int j = 0; j < n_hid; ++j) {
             double s = 0.0;
-            for (int64_t i = 0; i < ni; ++i) s += (double)w1[j * ni + i] * (double)x[i];
+            for (int64_t i = 0; i < ni; ++i) s += (double)w1[i * n_hid + j] * (double)x[i];
             hidden[j + 1] = squash((float)s);
         }
         float so = 0.0f;
@@ -256,9 +258,9 @@ void cpu_backprop(int64_t n_in, int32_t n_hid, int32_t iters, uint64_t seed, flo
             const float e = GS_BP_ETA * dh[j + 1];
             for (int64_t i = 0; i < ni; ++i) {
                 const float t1 = e * x[i];
-                const float nd = t1 + GS_BP_MOMENTUM * ow1[j * ni + i];
-                w1[j * ni + i] = w1[j * ni + i] + nd;
-                ow1[j * ni + i] = nd;
+                const float nd = t1 + GS_BP_MOMENTUM * ow1[i * n_hid + j];
+                w1[i * n_hid + j] = w1[i * n_hid + j] + nd;
+                ow1[i * n_hid + j] = nd;
             }
         }
     }

@@ -103,7 +103,7 @@ int validate(const gs_job_desc &j) {
       if (j.m < 1 || j.m > kMaxF) return err(GS_ERR_CONFIG, "kmeans features must be 1..64");
       break;
     case GS_JOB_BACKPROP:
-      if (j.m < 1 || j.m > kMaxHid) return err(GS_ERR_CONFIG, "backprop hidden units must be 1..16");
+      if (j.m < 4 || j.m > kMaxHid || j.m % 4) return err(GS_ERR_CONFIG, "backprop hidden units must be 4, 8, 12 or 16");
       break;
     case GS_JOB_YOLO:
       return gemm_validate(j);

@@ -108,7 +108,7 @@ def output_shape(job: Job) -> tuple[int, ...]:
     n = job.n
     if job.kind == "yolo":  # both YOLO heads, NHWC, 255 channels each
         return ((job.m * (n // 32) ** 2 + job.m * (n // 16) ** 2) * 255,)
-    return {"bfs": (n,), "hotspot": (n, n), "srad": (n, n), "kmeans": (n,), "backprop": (job.m, n + 1),
+    return {"bfs": (n,), "hotspot": (n, n), "srad": (n, n), "kmeans": (n,), "backprop": (n + 1, job.m),
             "needle": (n + 1, n + 1), "lud": (n, n)}.get(job.kind, (0,))
 
 

@@ -68,4 +68,5 @@ def test_backprop_forward_and_update():
     h = 1.0 / (1.0 + np.exp(-s.astype(np.float32).astype(np.float64)))
     np.testing.assert_allclose(hid[1:], h, rtol=1e-5)
     assert 0.0 < o < 1.0
-    assert not np.array_equal(w1, w1_0)  # weights moved
+    assert w1.shape == (4001, 16)  # [input][hidden], Rodinia's input_weights layout
+    assert not np.array_equal(w1, w1_0.T)  # weights moved
