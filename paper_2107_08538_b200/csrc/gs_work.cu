@@ -117,8 +117,9 @@ int validate(const gs_job_desc &j) {
 // threads per SM on all 148 SMs) — resident-sized, so a probe's
 // thread_blocks is a real placement demand for mgb-sm.
 int job_grid(const gs_job_desc &j) {
-  // srad's fused kernel is FP32-issue bound: 3 CTAs per SM (<= 85 registers)
-  return j.kind == GS_JOB_SRAD ? 3 * kSMs : 2 * kSMs;
+  // srad's fused kernel and kmeans' assignment are issue / latency bound:
+  // 3 CTAs per SM (<= 85 registers) hide more latency than 2
+  return (j.kind == GS_JOB_SRAD || j.kind == GS_JOB_KMEANS) ? 3 * kSMs : 2 * kSMs;
 }
 
 // needle: one warp per 32-row band in flight, at most the job's SM share
