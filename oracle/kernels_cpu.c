@@ -229,17 +229,32 @@ void cpu_backprop(int64_t n_in, int32_t n_hid, int32_t iters, uint64_t seed, flo
     float dh[64];
     for (int64_t i = 0; i < ni; ++i) x[i] = gs_bp_input(seed, (uint64_t)i);
     /* element-major [input][hidden] (Rodinia input_weights); value of (j, i) from index j * ni + i */
-    for (int j = 0; j < n_hid; ++j)
-        for (int64_t i = 0; i < ni; ++i) w1[i * n_hid + j] = gs_bp_w1(seed, (uint64_t)(j * ni + i));
+#pragma omp parallel for
+    for (int64_t i = 0; i < ni; ++i)
+        for (int j = 0; j < n_hid; ++j) w1[i * n_hid + j] = gs_bp_w1(seed, (uint64_t)(j * ni + i));
     for (int j = 0; j <= n_hid; ++j) w2[j] = gs_bp_w2(seed, (uint64_t)j);
     float o = 0.0f;
     for (int32_t it = 0; it < iters; ++it) {
         hidden[0] = 1.0f;
+        /* double dot products, summed in fixed chunks of inputs (cache-friendly
+         * over the element-major rows; deterministic chunk order) */
+        {
+            const int64_t chunk = 1 << 16;
+            const int64_t nch = (ni + chunk - 1) / chunk;
+            double *part = (double *)calloc((size_t)nch * n_hid, sizeof(double));
 #pragma omp parallel for
-        for (int j = 0; j < n_hid; ++j) {
-            double s = 0.0;
-            for (int64_t i = 0; i < ni; ++i) s += (double)w1[i * n_hid + j] * (double)x[i];
-            hidden[j + 1] = squash((float)s);
+            for (int64_t c = 0; c < nch; ++c) {
+                double *pc = part + c * n_hid;
+                const int64_t i1 = (c + 1) * chunk < ni ? (c + 1) * chunk : ni;
+                for (int64_t i = c * chunk; i < i1; ++i)
+                    for (int j = 0; j < n_hid; ++j) pc[j] += (double)w1[i * n_hid + j] * (double)x[i];
+            }
+            for (int j = 0; j < n_hid; ++j) {
+                double s = 0.0;
+                for (int64_t c = 0; c < nch; ++c) s += part[c * n_hid + j];
+                hidden[j + 1] = squash((float)s);
+            }
+            free(part);
         }
         float so = 0.0f;
         for (int j = 0; j <= n_hid; ++j) so = fmaf(w2[j], hidden[j], so);
@@ -253,16 +268,16 @@ void cpu_backprop(int64_t n_in, int32_t n_hid, int32_t iters, uint64_t seed, flo
             w2[j] = w2[j] + nd;
             ow2[j] = nd;
         }
+        float e[64];
+        for (int j = 0; j < n_hid; ++j) e[j] = GS_BP_ETA * dh[j + 1];
 #pragma omp parallel for
-        for (int j = 0; j < n_hid; ++j) {
-            const float e = GS_BP_ETA * dh[j + 1];
-            for (int64_t i = 0; i < ni; ++i) {
-                const float t1 = e * x[i];
+        for (int64_t i = 0; i < ni; ++i)
+            for (int j = 0; j < n_hid; ++j) {
+                const float t1 = e[j] * x[i];
                 const float nd = t1 + GS_BP_MOMENTUM * ow1[i * n_hid + j];
                 w1[i * n_hid + j] = w1[i * n_hid + j] + nd;
                 ow1[i * n_hid + j] = nd;
             }
-        }
     }
     *output = o;
     free(x);
