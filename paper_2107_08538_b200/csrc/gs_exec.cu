@@ -388,20 +388,19 @@ int gs_exec_run_arrivals(const gs_job_desc *jobs, int32_t n_jobs, const double *
   };
 
   auto worker = [&](int wid) {
-    // three stream-priority classes per device (shortest-job-first-like):
-    // latency-chain jobs (bfs, lud, needle: many dependent launches or a
-    // wavefront) and short jobs (< 3 ms solo) run at the highest priority so
-    // their next kernel is not queued behind co-located long streaming
-    // kernels; < 15 ms at the middle one; the rest at the default
-    std::vector<cudaStream_t> streams(n_devices, nullptr), mid_streams(n_devices, nullptr),
-        hi_streams(n_devices, nullptr);
+    // two streams per device: latency-chain jobs (bfs, lud, needle: many
+    // dependent launches or a wavefront) run at high stream priority so their
+    // next kernel is not queued behind co-located streaming kernels; the
+    // bandwidth-bound kinds at the default.  (A three-class shortest-job-first
+    // variant starved the long streaming jobs: cfg 3 turnaround 907 ms vs
+    // 106 ms, cfg 1 makespan 324-414 ms vs 285 ms.)
+    std::vector<cudaStream_t> streams(n_devices, nullptr), hi_streams(n_devices, nullptr);
     int prio_lo = 0, prio_hi = 0;
     cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi);
     for (int d = 0; d < n_devices; ++d) {
       cudaSetDevice(cuda_devices[d]);
       cudaStreamCreateWithFlags(&streams[d], cudaStreamNonBlocking);
       cudaStreamCreateWithPriority(&hi_streams[d], cudaStreamNonBlocking, prio_hi);
-      cudaStreamCreateWithPriority(&mid_streams[d], cudaStreamNonBlocking, (prio_hi + prio_lo) / 2);
     }
     void *host_out = nullptr;
     if (out_cap) cudaHostAlloc(&host_out, out_cap, cudaHostAllocPortable);
@@ -473,8 +472,7 @@ int gs_exec_run_arrivals(const gs_job_desc *jobs, int32_t n_jobs, const double *
       }
       bool oom = false;
       const bool chain = jobs[j].kind == GS_JOB_BFS || jobs[j].kind == GS_JOB_LUD || jobs[j].kind == GS_JOB_NEEDLE;
-      const double est = job_est_ms(jobs[j]);
-      cudaStream_t js = (chain || est < 3.0) ? hi_streams[dev] : (est < 15.0 ? mid_streams[dev] : streams[dev]);
+      cudaStream_t js = chain ? hi_streams[dev] : streams[dev];
       int r = run_job(jobs[j], stg, mode, js, rec, &oom, host_out, out_cap, scalar, &kernels, hsum,
                       cuda_devices[dev]);
       rec.end_ms = ms_since(t0);
@@ -496,7 +494,6 @@ int gs_exec_run_arrivals(const gs_job_desc *jobs, int32_t n_jobs, const double *
     }
     for (cudaStream_t s : streams) cudaStreamDestroy(s);
     for (cudaStream_t s : hi_streams) cudaStreamDestroy(s);
-    for (cudaStream_t s : mid_streams) cudaStreamDestroy(s);
     if (host_out) cudaFreeHost(host_out);
     cudaFreeHost(scalar);
     cudaFreeHost(hsum);

@@ -46,21 +46,6 @@ constexpr int kThreads = 256;
 
 int64_t round_granule(int64_t b) { return (b + kGranule - 1) / kGranule * kGranule; }
 
-double job_est_ms(const gs_job_desc &j) {
-  const double n = (double)j.n, m = (double)j.m, it = j.iters > 0 ? j.iters : 1;
-  switch (j.kind) {  // algorithmic work / rate measured solo on B200
-    case GS_JOB_BFS: return 37.0 * n / 0.30e9;
-    case GS_JOB_HOTSPOT: return 12.0 * n * n * it / 5.5e9;
-    case GS_JOB_SRAD: return 8.0 * n * n * it / 1.15e9;
-    case GS_JOB_KMEANS: return (4.0 * n * m + 4.0 * n) * it / 2.5e9;
-    case GS_JOB_BACKPROP: return 16.0 * (n + 1) * (m + 1) * it / 4.4e9;
-    case GS_JOB_NEEDLE: return 8.0 * (n + 1) * (n + 1) / 0.22e9;
-    case GS_JOB_LUD: return 2.0 / 3.0 * n * n * n / 13e9;
-    case GS_JOB_YOLO: return 5.6e9 * (n / 416.0) * (n / 416.0) * m * it / 50e9;
-  }
-  return 1.0;
-}
-
 // Buffers of each kind.  role: IN staged input, INOUT staged input that is
 // also an output, OUT output, SCR scratch (zeroed).
 std::vector<Buf> job_buffers(const gs_job_desc &j) {

@@ -42,9 +42,6 @@ int run_kernels(const gs_job_desc &j, std::vector<void *> &buf, cudaStream_t st,
                 int32_t *host_scalar, unsigned *tk);
 int digest(const void *p, int64_t bytes, unsigned long long *dsum, cudaStream_t st);
 int64_t round_granule(int64_t b);
-// Rough solo device time of a job (ms) from its algorithmic work and the
-// kind's measured B200 rate; the executor's stream-priority class uses it.
-double job_est_ms(const gs_job_desc &j);
 
 // Darknet-style layer stacks on tcgen05 (gs_gemm.cu)
 std::vector<Buf> gemm_buffers(const gs_job_desc &j);
