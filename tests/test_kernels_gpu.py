@@ -20,7 +20,9 @@ CASES = [
     ("hotspot", dict(n=1024, iters=3, seed=5), "exact"),   # one two-step pass + one single step
     ("hotspot", dict(n=128, iters=2, seed=6), "exact"),    # grid edges on every side of one tile column
     ("hotspot", dict(n=256, iters=5, seed=7), "exact"),
-    ("srad", dict(n=512, iters=5, seed=4), 1e-5),
+    ("srad", dict(n=512, iters=5, seed=4), "exact"),
+    ("srad", dict(n=128, iters=3, seed=8), "exact"),     # one tile: every halo is a grid edge
+    ("srad", dict(n=384, iters=2, seed=9), "exact"),
     ("kmeans", dict(n=200_000, m=34, iters=5, seed=6), "exact"),
     ("backprop", dict(n=300_000, m=16, iters=2, seed=7), 1e-5),
     ("needle", dict(n=128, seed=2), "exact"),     # one chunk, 4 bands
