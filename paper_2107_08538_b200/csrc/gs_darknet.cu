@@ -267,11 +267,91 @@ __global__ void __launch_bounds__(kThr) upsample2(ViewArgs in, __nv_bfloat16 *ou
   }
 }
 
+// Direct 3x3 convolution (stride 1, pad 1) for the thin first layers
+// (C_in = 3 -> 16, 16 -> 32: K = 27 / 144, N = 16 / 32): an im2row matrix
+// and a tensor-core GEMM with N <= 32 move far more bytes than the math
+// needs (measured 4.2 ms of a 7.5 ms job at 608^2 x 32 for layer 0), so
+// these run on the CUDA cores: one thread per output pixel, all C_out
+// accumulators in registers (fp32 FMAs on the same bf16 inputs / filters),
+// filters in shared memory as fp32, bias + leaky fused, 16-byte stores.
+template <int CIN, int COUT>
+__global__ void __launch_bounds__(kThr) conv3x3_direct(ViewArgs in, const __nv_bfloat16 *__restrict__ w, int kpad,
+                                                       const float *__restrict__ bias, __nv_bfloat16 *out, int opitch) {
+  __shared__ __align__(16) float sW[9 * CIN][COUT];
+  __shared__ float sb[COUT];
+  for (int i = threadIdx.x; i < 9 * CIN * COUT; i += blockDim.x) {
+    const int k = i / COUT, co = i % COUT;
+    sW[k][co] = __bfloat162float(w[(int64_t)co * kpad + k]);
+  }
+  if (threadIdx.x < COUT) sb[threadIdx.x] = bias[threadIdx.x];
+  __syncthreads();
+  const int64_t pix = (int64_t)in.n * in.h * in.w;
+  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < pix; p += (int64_t)gridDim.x * blockDim.x) {
+    const int x = (int)(p % in.w), y = (int)((p / in.w) % in.h);
+    const int64_t b = p / ((int64_t)in.w * in.h);
+    float acc[COUT];
+#pragma unroll
+    for (int co = 0; co < COUT; ++co) acc[co] = 0.0f;
+#pragma unroll
+    for (int tap = 0; tap < 9; ++tap) {
+      const int iy = y + tap / 3 - 1, ix = x + tap % 3 - 1;
+      if (iy < 0 || iy >= in.h || ix < 0 || ix >= in.w) continue;
+      const __nv_bfloat16 *src = in.p + ((b * in.h + iy) * in.w + ix) * in.pitch;
+      float v[CIN];
+      if constexpr (CIN % 8 == 0) {
+#pragma unroll
+        for (int q = 0; q < CIN / 8; ++q) {
+          const uint4 u = *reinterpret_cast<const uint4 *>(src + 8 * q);
+          const __nv_bfloat162 *h = reinterpret_cast<const __nv_bfloat162 *>(&u);
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const float2 f = __bfloat1622float2(h[e]);
+            v[8 * q + 2 * e] = f.x;
+            v[8 * q + 2 * e + 1] = f.y;
+          }
+        }
+      } else {
+#pragma unroll
+        for (int c = 0; c < CIN; ++c) v[c] = __bfloat162float(src[c]);
+      }
+#pragma unroll
+      for (int c = 0; c < CIN; ++c) {
+        const float4 *wr = reinterpret_cast<const float4 *>(&sW[tap * CIN + c][0]);
+#pragma unroll
+        for (int q = 0; q < COUT / 4; ++q) {
+          const float4 ww = wr[q];
+          acc[4 * q] = fmaf(v[c], ww.x, acc[4 * q]);
+          acc[4 * q + 1] = fmaf(v[c], ww.y, acc[4 * q + 1]);
+          acc[4 * q + 2] = fmaf(v[c], ww.z, acc[4 * q + 2]);
+          acc[4 * q + 3] = fmaf(v[c], ww.w, acc[4 * q + 3]);
+        }
+      }
+    }
+    __nv_bfloat16 *dst = out + p * opitch;
+#pragma unroll
+    for (int q = 0; q < COUT / 8; ++q) {
+      __align__(16) __nv_bfloat162 o[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        float a0 = acc[8 * q + 2 * e] + sb[8 * q + 2 * e], a1 = acc[8 * q + 2 * e + 1] + sb[8 * q + 2 * e + 1];
+        a0 = a0 > 0.0f ? a0 : 0.1f * a0;
+        a1 = a1 > 0.0f ? a1 : 0.1f * a1;
+        o[e] = __floats2bfloat162_rn(a0, a1);
+      }
+      *reinterpret_cast<uint4 *>(dst + 8 * q) = *reinterpret_cast<const uint4 *>(o);
+    }
+  }
+}
+
 ViewArgs vargs(const TView &v, const std::vector<void *> &buf) {
   return {reinterpret_cast<const __nv_bfloat16 *>(buf[v.buf]) + v.off, v.n, v.h, v.w, v.c, v.pitch};
 }
 
-int grid_for(int64_t total) { return (int)std::min<int64_t>((total + kThr - 1) / kThr, 4 * kSMs); }
+// One CTA per SM for every kernel of the job: the GEMM's shared-memory ring
+// and the direct convolution's registers allow one CTA per SM, and mgb-sm
+// places a job by its widest launch under the most demanding kernel's
+// occupancy (task_builder.py:272-289 aggregation), so no grid may exceed 148.
+int grid_for(int64_t total) { return (int)std::min<int64_t>((total + kThr - 1) / kThr, kSMs); }
 
 }  // namespace
 
@@ -297,7 +377,9 @@ std::vector<Shape> gemm_launches(const gs_job_desc &j) {
   const int64_t pix0 = (int64_t)j.m * j.n * j.n;
   Shape g{gemm_kernel_fn(bn_max), kSMs, gemm_block_threads()};
   g.dsmem = (int)gemm_smem_for(bn_max);
-  return {g, {(const void *)im2row3, grid_for(pix0 * 4), kThr}, {(const void *)maxpool2, grid_for(pix0), kThr}};
+  return {g, {(const void *)im2row3, grid_for(pix0 * 4), kThr}, {(const void *)maxpool2, grid_for(pix0), kThr},
+          {(const void *)conv3x3_direct<3, 16>, grid_for(pix0), kThr},
+          {(const void *)conv3x3_direct<16, 32>, grid_for(pix0), kThr}};
 }
 
 int gemm_generate(const gs_job_desc &j, const std::vector<void *> &dst, cudaStream_t st) {
@@ -336,6 +418,18 @@ int gemm_run(const gs_job_desc &j, std::vector<void *> &buf, cudaStream_t st, in
         continue;
       }
       const int64_t pix = (int64_t)L.in.n * L.in.h * L.in.w;
+      if (L.k == 3 && L.act == 1 && !L.out.f32 && L.out.off % 8 == 0 && L.out.pitch % 8 == 0 &&
+          ((L.in.c == 3 && L.cout == 16) || (L.in.c == 16 && L.cout == 32 && L.in.pitch % 8 == 0))) {
+        const __nv_bfloat16 *w = (const __nv_bfloat16 *)buf[B_W] + L.woff;
+        const float *bias = (const float *)buf[B_BIAS] + L.boff;
+        __nv_bfloat16 *o = (__nv_bfloat16 *)buf[L.out.buf] + L.out.off;
+        if (L.in.c == 3)
+          conv3x3_direct<3, 16><<<grid_for(pix), kThr, 0, st>>>(in, w, L.kpad, bias, o, L.out.pitch);
+        else
+          conv3x3_direct<16, 32><<<grid_for(pix), kThr, 0, st>>>(in, w, L.kpad, bias, o, L.out.pitch);
+        ++*launches;
+        continue;
+      }
       const void *A;
       int64_t lda;
       if (L.k == 1 && L.in.pitch % 8 == 0 && L.in.off % 8 == 0) {
