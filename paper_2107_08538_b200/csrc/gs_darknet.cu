@@ -275,7 +275,7 @@ __global__ void __launch_bounds__(kThr) upsample2(ViewArgs in, __nv_bfloat16 *ou
 // accumulators in registers (fp32 FMAs on the same bf16 inputs / filters),
 // filters in shared memory as fp32, bias + leaky fused, 16-byte stores.
 template <int CIN, int COUT>
-__global__ void __launch_bounds__(kThr) conv3x3_direct(ViewArgs in, const __nv_bfloat16 *__restrict__ w, int kpad,
+__global__ void __launch_bounds__(kThr, 2) conv3x3_direct(ViewArgs in, const __nv_bfloat16 *__restrict__ w, int kpad,
                                                        const float *__restrict__ bias, __nv_bfloat16 *out, int opitch) {
   __shared__ __align__(16) float sW[9 * CIN][COUT];
   __shared__ float sb[COUT];
@@ -347,11 +347,12 @@ ViewArgs vargs(const TView &v, const std::vector<void *> &buf) {
   return {reinterpret_cast<const __nv_bfloat16 *>(buf[v.buf]) + v.off, v.n, v.h, v.w, v.c, v.pitch};
 }
 
-// One CTA per SM for every kernel of the job: the GEMM's shared-memory ring
-// and the direct convolution's registers allow one CTA per SM, and mgb-sm
-// places a job by its widest launch under the most demanding kernel's
-// occupancy (task_builder.py:272-289 aggregation), so no grid may exceed 148.
-int grid_for(int64_t total) { return (int)std::min<int64_t>((total + kThr - 1) / kThr, kSMs); }
+// Two CTAs per SM for every kernel of the job: the GEMM's shared-memory ring
+// (<= 99 KB) and the direct convolution's registers (<= 128) allow two, and
+// mgb-sm places a job by its widest launch under the most demanding
+// kernel's occupancy (task_builder.py:272-289 aggregation), so no grid may
+// exceed 2 x 148.
+int grid_for(int64_t total) { return (int)std::min<int64_t>((total + kThr - 1) / kThr, 2 * kSMs); }
 
 }  // namespace
 
@@ -375,7 +376,7 @@ std::vector<Shape> gemm_launches(const gs_job_desc &j) {
     if (L.type == CONV)
       bn_max = std::max(bn_max, gemm_pick_bn((int)((int64_t)L.in.n * L.in.h * L.in.w), L.cout));
   const int64_t pix0 = (int64_t)j.m * j.n * j.n;
-  Shape g{gemm_kernel_fn(bn_max), kSMs, gemm_block_threads()};
+  Shape g{gemm_kernel_fn(bn_max), 2 * kSMs, gemm_block_threads()};
   g.dsmem = (int)gemm_smem_for(bn_max);
   return {g, {(const void *)im2row3, grid_for(pix0 * 4), kThr}, {(const void *)maxpool2, grid_for(pix0), kThr},
           {(const void *)conv3x3_direct<3, 16>, grid_for(pix0), kThr},
@@ -444,7 +445,7 @@ int gemm_run(const gs_job_desc &j, std::vector<void *> &buf, cudaStream_t st, in
       void *out = L.out.f32 ? (void *)((float *)buf[L.out.buf] + L.out.off)
                             : (void *)((__nv_bfloat16 *)buf[L.out.buf] + L.out.off);
       int rc = gemm_bf16(A, lda, (const __nv_bfloat16 *)buf[B_W] + L.woff, L.kpad, (const float *)buf[B_BIAS] + L.boff,
-                         out, L.out.pitch, (int)pix, L.cout, L.kpad, L.out.f32 ? 1 : 0, L.act, kSMs, st);
+                         out, L.out.pitch, (int)pix, L.cout, L.kpad, L.out.f32 ? 1 : 0, L.act, 2 * kSMs, st);
       if (rc) return rc;
       ++*launches;
     }

@@ -39,7 +39,10 @@ struct GemmArgs {
   int act;               // 0 linear, 1 leaky (0.1), 2 YOLO logistic
 };
 
-constexpr int kGemmBM = 128, kGemmBK = 64, kGemmStages = 4;
+// 3 stages x (16 KB A + <= 16 KB B) <= 99 KB: two CTAs per SM, so one CTA's
+// epilogue overlaps the other's mainloop and a Darknet job's kernels all
+// fit a 2 x 148 grid (the mgb-sm probe rule, see gs_darknet.cu grid_for)
+constexpr int kGemmBM = 128, kGemmBK = 64, kGemmStages = 3;
 
 template <int BN>
 constexpr size_t gemm_smem_bytes() {
@@ -107,7 +110,7 @@ __device__ __forceinline__ void epilogue_store(const GemmArgs &g, int row, int c
 // MMA warp alternates between two TMEM accumulators, and the four epilogue
 // warps drain accumulator t while the MMAs of tile t+1 run.
 template <int BN>
-__global__ void __launch_bounds__(kGemmThreads, 1) gemm_bf16_tc(const __grid_constant__ CUtensorMap ta,
+__global__ void __launch_bounds__(kGemmThreads, 2) gemm_bf16_tc(const __grid_constant__ CUtensorMap ta,
                                                                 const __grid_constant__ CUtensorMap tb, GemmArgs g) {
   using namespace tc;
   constexpr uint32_t A_BYTES = kGemmBM * kGemmBK * 2, B_BYTES = BN * kGemmBK * 2;
@@ -266,10 +269,9 @@ static int launch_bn(const CUtensorMap &ta, const CUtensorMap &tb, GemmArgs g, i
 }
 
 int gemm_pick_bn(int m, int n) {
+  (void)m;
   if (n <= 32) return 32;
   if (n <= 64) return 64;
-  const int m_tiles = (m + kGemmBM - 1) / kGemmBM;
-  if (n >= 256 && (int64_t)m_tiles * ((n + 255) / 256) >= 2 * kSMs) return 256;
   return 128;
 }
 
@@ -296,7 +298,7 @@ int gemm_bf16(const void *A, int64_t lda, const void *B, int64_t ldb, const floa
   g.ldo = ldo;
   g.out_f32 = out_f32;
   g.act = act;
-  if (max_ctas <= 0) max_ctas = kSMs;
+  if (max_ctas <= 0) max_ctas = 2 * kSMs;
   switch (bn) {
     case 32: return launch_bn<32>(ta, tb, g, max_ctas, st);
     case 64: return launch_bn<64>(ta, tb, g, max_ctas, st);
