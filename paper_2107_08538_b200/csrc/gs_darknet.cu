@@ -267,13 +267,13 @@ __global__ void __launch_bounds__(kThr) upsample2(ViewArgs in, __nv_bfloat16 *ou
   }
 }
 
-// Direct 3x3 convolution (stride 1, pad 1) for the thin first layers
-// (C_in = 3 -> 16, 16 -> 32: K = 27 / 144, N = 16 / 32): an im2row matrix
-// and a tensor-core GEMM with N <= 32 move far more bytes than the math
-// needs (measured 4.2 ms of a 7.5 ms job at 608^2 x 32 for layer 0), so
-// these run on the CUDA cores: one thread per output pixel, all C_out
-// accumulators in registers (fp32 FMAs on the same bf16 inputs / filters),
-// filters in shared memory as fp32, bias + leaky fused, 16-byte stores.
+// Direct 3x3 convolution (stride 1, pad 1) for the thin first layer
+// (C_in = 3 -> 16: K = 27, N = 16): an im2row matrix and a tensor-core GEMM
+// with N = 16 move far more bytes than the math needs (measured 4.2 ms of a
+// 7.5 ms job at 608^2 x 32), so it runs on the CUDA cores: one thread per
+// output pixel, all C_out accumulators in registers (fp32 FMAs on the same
+// bf16 inputs / filters), filters in shared memory as fp32, bias + leaky
+// fused, 16-byte stores.
 template <int CIN, int COUT>
 __global__ void __launch_bounds__(kThr, 2) conv3x3_direct(ViewArgs in, const __nv_bfloat16 *__restrict__ w, int kpad,
                                                        const float *__restrict__ bias, __nv_bfloat16 *out, int opitch) {
@@ -379,8 +379,7 @@ std::vector<Shape> gemm_launches(const gs_job_desc &j) {
   Shape g{gemm_kernel_fn(bn_max), 2 * kSMs, gemm_block_threads()};
   g.dsmem = (int)gemm_smem_for(bn_max);
   return {g, {(const void *)im2row3, grid_for(pix0 * 4), kThr}, {(const void *)maxpool2, grid_for(pix0), kThr},
-          {(const void *)conv3x3_direct<3, 16>, grid_for(pix0), kThr},
-          {(const void *)conv3x3_direct<16, 32>, grid_for(pix0), kThr}};
+          {(const void *)conv3x3_direct<3, 16>, grid_for(pix0), kThr}};
 }
 
 int gemm_generate(const gs_job_desc &j, const std::vector<void *> &dst, cudaStream_t st) {
@@ -419,15 +418,13 @@ int gemm_run(const gs_job_desc &j, std::vector<void *> &buf, cudaStream_t st, in
         continue;
       }
       const int64_t pix = (int64_t)L.in.n * L.in.h * L.in.w;
-      if (L.k == 3 && L.act == 1 && !L.out.f32 && L.out.off % 8 == 0 && L.out.pitch % 8 == 0 &&
-          ((L.in.c == 3 && L.cout == 16) || (L.in.c == 16 && L.cout == 32 && L.in.pitch % 8 == 0))) {
-        const __nv_bfloat16 *w = (const __nv_bfloat16 *)buf[B_W] + L.woff;
-        const float *bias = (const float *)buf[B_BIAS] + L.boff;
-        __nv_bfloat16 *o = (__nv_bfloat16 *)buf[L.out.buf] + L.out.off;
-        if (L.in.c == 3)
-          conv3x3_direct<3, 16><<<grid_for(pix), kThr, 0, st>>>(in, w, L.kpad, bias, o, L.out.pitch);
-        else
-          conv3x3_direct<16, 32><<<grid_for(pix), kThr, 0, st>>>(in, w, L.kpad, bias, o, L.out.pitch);
+      if (L.k == 3 && L.act == 1 && !L.out.f32 && L.out.off % 8 == 0 && L.out.pitch % 8 == 0 && L.in.c == 3 &&
+          L.cout == 16) {
+        // layer 0 (K = 27): direct convolution (measured 0.6 ms vs 4.2 ms for
+        // im2row + GEMM at 608^2 x 32; for 16 -> 32 the GEMM path is faster)
+        conv3x3_direct<3, 16><<<grid_for(pix), kThr, 0, st>>>(in, (const __nv_bfloat16 *)buf[B_W] + L.woff, L.kpad,
+                                                              (const float *)buf[B_BIAS] + L.boff,
+                                                              (__nv_bfloat16 *)buf[L.out.buf] + L.out.off, L.out.pitch);
         ++*launches;
         continue;
       }
