@@ -27,7 +27,7 @@ cap lud lud_internal 20 python tools/debug_job.py lud 6144
 cap ludp lud_panel 20 python tools/debug_job.py lud 6144
 cap bpfwd bp_forward 1 python tools/debug_job.py backprop 32000000 2 16
 cap bpadj bp_adjust 1 python tools/debug_job.py backprop 32000000 2 16
-cap gemm gemm_bf16_tc 12 python tools/debug_job.py yolo 416 1 32
+cap gemm gemm_bf16_tc 4 python tools/debug_job.py yolo 608 1 32
 cap decide gs_interp 0 python -c "import __graft_entry__ as g; g.smoke()"
 case " $WANT " in *" launches "*)
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 6000 --csv \
