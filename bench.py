@@ -133,44 +133,69 @@ def summarize(results, times):
 
 
 def kernel_rooflines(W, C, jobs, device, pk):
-    """Each kind's kernels alone on the device (CUDA events around its
-    kernels): algorithmic work / kernel time vs the measured peak."""
-    out = {}
-    seen = {}
+    """Every distinct job of the mix alone on the device (CUDA events on the
+    job's stream around its kernels).  Returns (per-kind roofline of the
+    kind's largest job: algorithmic work / kernel time vs the measured peak,
+    per-template solo ms)."""
+    solo_ms, first = {}, {}
     for mj in jobs:
-        seen.setdefault(mj.job.kind, mj.job)
+        if mj.template in solo_ms:
+            continue
+        log(f"solo {mj.template} n={mj.job.n}")
+        W.run_solo(mj.job, device)  # warm-up
+        solo_ms[mj.template] = min(W.run_solo(mj.job, device)[1].compute_ms for _ in range(2))
+        j = mj.job
+        if j.kind not in first or j.n * max(j.m, 1) > first[j.kind][0].n * max(first[j.kind][0].m, 1):
+            first[j.kind] = (j, mj.template)
+    out = {}
     hbm = pk["hbm_gbs"]
-    for kind, job in seen.items():
-        log(f"solo {kind} n={job.n}")
-        W.run_solo(job, device)  # warm-up
-        recs = [W.run_solo(job, device)[1] for _ in range(2)]
-        ms = min(r.compute_ms for r in recs)
+    for kind, (job, tpl) in first.items():
+        ms = solo_ms[tpl]
         work, unit = C.algorithmic_work(job)
+        _, rec = W.run_solo(job, device)
         if unit == "B":
             ach = work / (ms * 1e-3) / 1e9
             out[kind] = {"bound": "hbm", "achieved": round(ach, 1), "peak": hbm, "unit": "GB/s",
-                         "frac": round(ach / hbm, 4), "ms": round(ms, 3), "launches": recs[0].n_kernels,
+                         "frac": round(ach / hbm, 4), "ms": round(ms, 3), "launches": rec.n_kernels,
                          "job": {"n": job.n, "iters": job.iters, "m": job.m}}
         elif unit == "TC_FLOP":
             ach = work / (ms * 1e-3) / 1e12
             pkt = pk["bf16_tflops"]
             out[kind] = {"bound": "tensor", "achieved": round(ach, 1), "peak": pkt, "unit": "TFLOP/s",
-                         "frac": round(ach / pkt, 4), "ms": round(ms, 3), "launches": recs[0].n_kernels,
+                         "frac": round(ach / pkt, 4), "ms": round(ms, 3), "launches": rec.n_kernels,
                          "job": {"n": job.n, "batch": job.m}}
         else:
             ach = work / (ms * 1e-3) / 1e12
             out[kind] = {"bound": "fp32", "achieved": round(ach, 2), "peak": round(FP32_TFLOPS_NOMINAL, 1),
                          "unit": "TFLOP/s", "frac": round(ach / FP32_TFLOPS_NOMINAL, 4), "ms": round(ms, 3),
-                         "launches": recs[0].n_kernels, "job": {"n": job.n}}
-    return out
+                         "launches": rec.n_kernels, "job": {"n": job.n}}
+    return out, solo_ms
 
 
 def traffic_from_profiles(kind: str):
+    """ncu DRAM bytes of one launch of the kind's main kernel (profiles/traffic.json)."""
     try:
         with open(os.path.join(REPO, "profiles", "traffic.json")) as f:
             return json.load(f).get(kind)
     except (OSError, ValueError):
         return None
+
+
+def pcie_h2d_gbps(torch) -> float:
+    """Measured pinned host -> device copy bandwidth (the e2e ceiling)."""
+    n = 1 << 28  # 1 GiB of float32
+    h = torch.empty(n, dtype=torch.float32, pin_memory=True)
+    d = torch.empty(n, dtype=torch.float32, device="cuda")
+    best = 1e9
+    for _ in range(3):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        d.copy_(h, non_blocking=True)
+        e1.record()
+        torch.cuda.synchronize()
+        best = min(best, e0.elapsed_time(e1))
+    del h, d
+    return 4.0 * n / (best * 1e-3) / 1e9
 
 
 def cpu_sample(jobs, budget_s: float):
@@ -287,7 +312,7 @@ def main() -> int:
         st, sr = run_steps(W, jobs, "sa", device, args.workers, W.MODE_DEVICE, args.steps, 1, torch)
         sa = summarize(sr, st)
     W.unstage()
-    kern = kernel_rooflines(W, C, mix, device, pk)
+    kern, solo_ms = kernel_rooflines(W, C, mix, device, pk)
 
     # ---- e2e mode: pinned host inputs, H2D + D2H inside the timed region ----
     e2e = sa_e2e = None
@@ -312,14 +337,17 @@ def main() -> int:
     value = whole_job_rate(len(jobs), world, ms_step)
 
     # dominant kernel: the kind with the largest share of device time in the mix
+    # dominant kind: the largest share of the mix's solo device time
     share = {}
-    for r in results[-1].records:
-        share[r["kind"]] = share.get(r["kind"], 0.0) + r["compute_ms"]
+    for mj in mix:
+        share[mj.job.kind] = share.get(mj.job.kind, 0.0) + solo_ms[mj.template]
     dom = max(share, key=share.get)
     kd = kern[dom]
+    tr = traffic_from_profiles(dom) or {}
     roof = {"kernel": dom, "bound": kd["bound"], "achieved": kd["achieved"], "peak": kd["peak"],
-            "unit": kd["unit"], "frac": kd["frac"], "traffic": traffic_from_profiles(dom),
-            "share_of_mix_device_time": round(share[dom] / sum(share.values()), 3),
+            "unit": kd["unit"], "frac": kd["frac"], "traffic": tr.get("dram_bytes_per_launch"),
+            "traffic_kernel": tr.get("kernel"), "algorithmic_bytes_per_launch": tr.get("algorithmic_bytes_per_launch"),
+            "share_of_mix_solo_device_time": round(share[dom] / sum(share.values()), 3),
             "peak_source": "MEASURED_PEAKS.json hbm_gbs (burst copy)" if kd["bound"] == "hbm"
             else "nominal FP32 (148 SMs x 128 FMA x 1.965 GHz)"}
     # aggregate HBM roofline fraction of the whole mix
@@ -351,9 +379,13 @@ def main() -> int:
         line["speedup_vs_sa"] = round(value / sa_value, 3)
         line["turnaround_speedup_vs_sa"] = round(sa["mean_turnaround_ms"] / max(ours["mean_turnaround_ms"], 1e-9), 3)
     if e2e:
+        pcie = pcie_h2d_gbps(torch)
+        h2d_rate = e2e["h2d"] / (e2e_ms / 1000.0) / 1e9
         line["e2e"] = {"value": round(n_total / (e2e_ms / 1000.0), 4), "unit": UNIT,
                        "h2d_bytes_per_step": e2e["h2d"], "d2h_bytes_per_step": e2e["d2h"],
-                       "mean_turnaround_ms": round(e2e["mean_turnaround_ms"], 2), "oom": e2e["oom"]}
+                       "mean_turnaround_ms": round(e2e["mean_turnaround_ms"], 2), "oom": e2e["oom"],
+                       "pcie_h2d_achieved_GBps": round(h2d_rate, 1), "pcie_h2d_peak_GBps": round(pcie, 1),
+                       "pcie_h2d_frac": round(h2d_rate / pcie, 3)}
         if sa_e2e:
             sv = n_total / (sa_e2e["ms_per_step"] / 1000.0)
             line["e2e"]["sa_value"] = round(sv, 4)
