@@ -134,7 +134,11 @@ std::vector<Shape> job_launches(const gs_job_desc &j) {
     case GS_JOB_BFS:
       return {{(const void *)bfs_expand, g, kThreads}, {(const void *)bfs_commit, g, kThreads}};
     case GS_JOB_HOTSPOT:
-      return {{(const void *)hotspot_step, g, kThreads}};
+    {
+      Shape s2{(const void *)hotspot_step2, g, kThreads};
+      s2.dsmem = kHs2Smem;
+      return {s2, {(const void *)hotspot_step, g, kThreads}};
+    }
     case GS_JOB_SRAD:
       return {{(const void *)srad_stats, 1, kThreads}, {(const void *)srad_fused, g, kThreads}};
     case GS_JOB_KMEANS:
@@ -282,10 +286,17 @@ int run_kernels(const gs_job_desc &j, std::vector<void *> &buf, cudaStream_t st,
       float cc, rx1, ry1, rz1;
       gs_hotspot_coeffs(&cc, &rx1, &ry1, &rz1);
       float *t = (float *)buf[0], *p = (float *)buf[1], *t2 = (float *)buf[2];
-      // one pass per time step: the single-step kernel runs at 80-93 % of HBM;
-      // a two-step temporally blocked variant (6 B/cell-step) measured 27 ms
-      // vs 21.5 ms here (FP32-issue bound: 2.5 cell updates per output)
-      for (int it = 0; it < j.iters; ++it) {
+      // two time steps per pass through shared memory (~6.5 B/cell-step);
+      // an odd step count ends with one single-step pass.  (A register-only
+      // two-step variant was FP32-issue bound: 2.5 updates per output.)
+      CUW(cudaFuncSetAttribute(hotspot_step2, cudaFuncAttributeMaxDynamicSharedMemorySize, kHs2Smem));
+      int it = 0;
+      for (; it + 1 < j.iters; it += 2) {
+        hotspot_step2<<<g, 256, kHs2Smem, st>>>(t, p, t2, (int)n, cc, rx1, ry1, rz1, tk);
+        ++launches;
+        std::swap(t, t2);
+      }
+      if (it < j.iters) {
         hotspot_step<<<g, dim3(32, 8), 0, st>>>(t, p, t2, (int)n, cc, rx1, ry1, rz1, tk);
         ++launches;
         std::swap(t, t2);
