@@ -131,8 +131,8 @@ def algorithmic_work(job: Job) -> tuple[float, str]:
     """(work, unit) per job run — SURVEY.md §8d's per-unit figures times the
     units a run processes: bytes for HBM-bound kernels, flops for lud."""
     n, it, m = job.n, max(job.iters, 1), job.m
-    if job.kind == "hotspot":
-        return 12.0 * n * n * it, "B"
+    if job.kind == "hotspot":  # two steps per pass: read T and P, write T once per pass
+        return 12.0 * n * n * (it // 2 + it % 2), "B"
     if job.kind == "srad":  # fused coefficient + update: read J, write J
         return 8.0 * n * n * it, "B"
     if job.kind == "bfs":
