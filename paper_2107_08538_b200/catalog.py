@@ -120,7 +120,7 @@ def host_footprint(job: Job) -> int:
         "srad": [n * n * 4] * 2 + [16],
         "kmeans": [n * m * 4, n * 4, 5 * m * 4, 5 * m * 8, 40],
         "backprop": [(n + 1) * 4, m * (n + 1) * 4, m * (n + 1) * 4, 320, -(-(n + 1) // 8192) * 16 * 8],
-        "needle": [(n + 1) * (n + 1) * 4] * 2 + [2 * n * 8],
+        "needle": [n * n * 4, (n + 1) * (n + 4) * 4, 2 * n * 8],
         "lud": [n * n * 4],
         "yolo": yolo_buffers(n, m) if job.kind == "yolo" else [],
     }[job.kind]

@@ -71,8 +71,8 @@ std::vector<Buf> job_buffers(const gs_job_desc &j) {
       b = {{(n + 1) * 4, IN}, {j.m * (n + 1) * 4, INOUT}, {j.m * (n + 1) * 4, SCR}, {80 * 4, INOUT},
            {((n + 1 + kBpTile - 1) / kBpTile) * kMaxHid * 8, SCR}};  // one partial per tile
       break;
-    case GS_JOB_NEEDLE:  // ref, score, band edge rows (2 slots x n tagged words)
-      b = {{(n + 1) * (n + 1) * 4, IN}, {(n + 1) * (n + 1) * 4, INOUT}, {2 * n * 8, SCR}};
+    case GS_JOB_NEEDLE:  // ref (n x n interior), score ((n+1) x (n+4) aligned), band edge rows
+      b = {{n * n * 4, IN}, {(n + 1) * (n + 4) * 4, INOUT}, {2 * n * 8, SCR}};
       break;
     case GS_JOB_LUD:
       b = {{n * n * 4, INOUT}};
@@ -124,8 +124,8 @@ int job_grid(const gs_job_desc &j) {
 
 // needle: one warp per 32-row band in flight, at most the job's SM share
 int needle_grid(const gs_job_desc &j) {
-  const int bands = (int)(j.n / 32);
-  return std::min(bands, 2 * kSMs);  // 96 KB of shared memory per band warp: 2 per SM
+  const int bands = (int)(j.n / 64);
+  return std::min(bands, 4 * kSMs);
 }
 
 std::vector<Shape> job_launches(const gs_job_desc &j) {
@@ -147,11 +147,7 @@ std::vector<Shape> job_launches(const gs_job_desc &j) {
       return {{(const void *)bp_forward, g, kThreads}, {(const void *)bp_output, 1, 32},
               {(const void *)bp_adjust, g, kThreads}};
     case GS_JOB_NEEDLE:
-    {
-      Shape sh{(const void *)needle_bands, needle_grid(j), 32};
-      sh.dsmem = kNwSmem;
-      return {sh};
-    }
+      return {{(const void *)needle_bands, needle_grid(j), 32}};
     case GS_JOB_LUD:
       return {{(const void *)lud_panel, (int)(j.n / BS), 2 * BS},
               {(const void *)lud_internal, g, 256}};
@@ -352,8 +348,7 @@ int run_kernels(const gs_job_desc &j, std::vector<void *> &buf, cudaStream_t st,
       break;
     }
     case GS_JOB_NEEDLE: {
-      CUW(cudaFuncSetAttribute(needle_bands, cudaFuncAttributeMaxDynamicSharedMemorySize, kNwSmem));  // per device
-      needle_bands<<<needle_grid(j), 32, kNwSmem, st>>>((int32_t *)buf[1], (const int32_t *)buf[0], (int)n, tk,
+      needle_bands<<<needle_grid(j), 32, 0, st>>>((int32_t *)buf[1], (const int32_t *)buf[0], (int)n, tk,
                                                         (unsigned long long *)buf[2]);
       ++launches;
       *out_idx = 1;
