@@ -74,19 +74,13 @@ void cpu_hotspot(int64_t n, int32_t iters, uint64_t seed, float *out) {
             for (int64_t c = 0; c < n; ++c) {
                 const int64_t cw = c > 0 ? c - 1 : 0, ce = c < n - 1 ? c + 1 : n - 1;
                 const float tc = t[r * n + c];
-                float a = t[rs * n + c] + t[rn * n + c];
-                a = a - 2.0f * tc;
-                a = a * ry1;
-                float b = t[r * n + ce] + t[r * n + cw];
-                b = b - 2.0f * tc;
-                b = b * rx1;
-                float e = GS_HOTSPOT_AMB - tc;
-                e = e * rz1;
-                float d = p[r * n + c] + a;
-                d = d + b;
-                d = d + e;
-                d = cc * d;
-                t2[r * n + c] = tc + d;
+                const float a = fmaf(-2.0f, tc, t[rs * n + c] + t[rn * n + c]);
+                const float b = fmaf(-2.0f, tc, t[r * n + ce] + t[r * n + cw]);
+                const float e = GS_HOTSPOT_AMB - tc;
+                float d = fmaf(a, ry1, p[r * n + c]);
+                d = fmaf(b, rx1, d);
+                d = fmaf(e, rz1, d);
+                t2[r * n + c] = fmaf(cc, d, tc);
             }
         }
         float *x = t;

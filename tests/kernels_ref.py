@@ -65,13 +65,13 @@ def hotspot(n: int, iters: int, seed: int) -> np.ndarray:
     rn, rs = np.maximum(r - 1, 0), np.minimum(r + 1, n - 1)
     for _ in range(iters):
         tc = t
-        a = (t[rs, :] + t[rn, :]) - np.float32(2.0) * tc
-        a = a * ry1
-        b = (t[:, rs] + t[:, rn]) - np.float32(2.0) * tc
-        b = b * rx1
-        e = (np.float32(80.0) - tc) * rz1
-        d = ((p + a) + b) + e
-        t = tc + cc * d
+        a = fmaf(np.float32(-2.0), tc, t[rs, :] + t[rn, :])
+        b = fmaf(np.float32(-2.0), tc, t[:, rs] + t[:, rn])
+        e = np.float32(80.0) - tc
+        d = fmaf(a, ry1, p)
+        d = fmaf(b, rx1, d)
+        d = fmaf(e, rz1, d)
+        t = fmaf(cc, d, tc)
     return t
 
 
