@@ -32,7 +32,8 @@ extern "C" {
 #define GS_JOB_NEEDLE 5
 #define GS_JOB_LUD 6
 #define GS_JOB_YOLO 7      /* Darknet YOLOv3-tiny inference (bf16 im2col + tcgen05 GEMM) */
-#define GS_JOB_KINDS 8
+#define GS_JOB_RESNET 8    /* ResNet-50 inference (same layers: im2col + tcgen05 GEMM, fused shortcut) */
+#define GS_JOB_KINDS 9
 
 /* executor modes */
 #define GS_MODE_DEVICE 0   /* inputs pre-staged in HBM, D2D into the job's buffers */
@@ -40,9 +41,9 @@ extern "C" {
 
 typedef struct gs_job_desc {
     int32_t kind;
-    int32_t iters;        /* iterations (hotspot/srad/kmeans/backprop), forward passes (yolo) */
+    int32_t iters;        /* iterations (hotspot/srad/kmeans/backprop), forward passes (yolo/resnet) */
     int64_t n;            /* problem size: nodes / grid edge / points / inputs / matrix edge / image edge */
-    int64_t m;            /* secondary size: features (kmeans), hidden (backprop), batch (yolo) */
+    int64_t m;            /* secondary size: features (kmeans), hidden (backprop), batch (yolo/resnet) */
     uint64_t seed;
 } gs_job_desc;
 

@@ -30,6 +30,7 @@ RODINIA = {
 # Darknet YOLOv3-tiny inference jobs (BASELINE cfg 2): image edge, batch
 DARKNET = {
     "yolo": (dict(n=416, m=8), dict(n=608, m=32)),
+    "resnet": (dict(n=224, m=8), dict(n=224, m=64)),
 }
 
 # the 8-job CPU-runnable mix of cfg 0 (2x bfs, hotspot, srad, kmeans, repeated)
@@ -108,6 +109,55 @@ def yolo_flops(S: int, N: int) -> float:
     return float(sum(2 * N * (S // d) ** 2 * k * k * cin * cout for d, cin, cout, k in YOLO_CONVS))
 
 
+def resnet50_convs(S: int) -> list[tuple[int, int, int, int, int, str]]:
+    """ResNet-50 convolutions in plan order (csrc/gs_darknet.cu resnet50_plan):
+    (in_hw, cin, cout, k, stride, out_buffer) with out_buffer "act" (a new
+    resident activation) or "det" (the logits)."""
+    out = [(S, 3, 64, 7, 2, "act")]
+    hw = S // 4
+    cin = 64
+    for mid, blocks in ((64, 3), (128, 4), (256, 6), (512, 3)):
+        for bi in range(blocks):
+            stride = 2 if (mid != 64 and bi == 0) else 1
+            out.append((hw, cin, mid, 1, 1, "act"))
+            out.append((hw, mid, mid, 3, stride, "act"))
+            if bi == 0:
+                out.append((hw, cin, 4 * mid, 1, stride, "act"))
+            out.append((hw // stride, mid, 4 * mid, 1, 1, "act"))
+            hw //= stride
+            cin = 4 * mid
+    out.append((1, 2048, 1000, 1, 1, "det"))
+    return out
+
+
+def resnet_buffers(S: int, N: int) -> list[int]:
+    """Byte sizes of the ResNet-50 job's buffers (resnet50_plan order)."""
+    w = b = ws = 0
+    acts = []
+    for hw, cin, cout, k, stride, kind in resnet50_convs(S):
+        kdim = k * k * cin
+        kpad = (kdim + 7) // 8 * 8
+        w = (w + cout * kpad + 7) // 8 * 8
+        b += cout
+        ohw = hw // stride if kind == "act" else 1
+        if not (k == 1 and stride == 1):
+            ws = max(ws, N * ohw * ohw * kpad * 2)
+        if kind == "act":
+            acts.append(N * ohw * ohw * cout * 2)
+            if len(acts) == 1:  # the stem is followed by the 3x3/2 max-pool
+                acts.append(N * (S // 4) ** 2 * 64 * 2)
+    acts.append(N * 2048 * 2)  # global average pool
+    return [N * S * S * 3 * 2, w * 2, b * 4, N * 1000 * 4, max(ws, 16)] + acts
+
+
+def resnet_flops(S: int, N: int) -> float:
+    tot = 0
+    for hw, cin, cout, k, stride, kind in resnet50_convs(S):
+        ohw = hw // stride if kind == "act" else 1
+        tot += 2 * N * ohw * ohw * k * k * cin * cout
+    return float(tot)
+
+
 def host_footprint(job: Job) -> int:
     """The probe's mem_bytes computed on the host alone (same rule as
     gs_job_probe: buffers rounded to 2 MiB + the 8 MiB task heap) — used by
@@ -123,6 +173,7 @@ def host_footprint(job: Job) -> int:
         "needle": [n * n * 4, (n + 1) * (n + 4) * 4, 2 * n * 8],
         "lud": [n * n * 4],
         "yolo": yolo_buffers(n, m) if job.kind == "yolo" else [],
+        "resnet": resnet_buffers(n, m) if job.kind == "resnet" else [],
     }[job.kind]
     return (8 << 20) + sum((s + g - 1) // g * g for s in sizes)
 
@@ -147,4 +198,6 @@ def algorithmic_work(job: Job) -> tuple[float, str]:
         return 2.0 / 3.0 * n ** 3, "FLOP"
     if job.kind == "yolo":
         return yolo_flops(n, m) * it, "TC_FLOP"
+    if job.kind == "resnet":
+        return resnet_flops(n, m) * it, "TC_FLOP"
     return 0.0, "B"

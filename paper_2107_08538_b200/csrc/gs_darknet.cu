@@ -16,6 +16,13 @@
 // bias + leaky (or YOLO logistic) epilogue fused; route/concat is free (the
 // producing GEMM writes into a channel slice of the concat tensor) and the
 // 2x upsample writes straight into its slice.
+//
+// The same layer machinery runs ResNet-50 (BASELINE cfg 2's other network:
+// 7x7/2 stem, 3x3/2 max-pool, 16 bottleneck blocks with 1x1 / 3x3 / 1x1
+// convolutions and identity or strided-projection shortcuts, global average
+// pool, 1000-way fully connected layer; batch-norm folded into the bias):
+// strided convolutions are im2row with a stride, and each block's residual
+// add + ReLU is fused into the last GEMM's epilogue.
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <math.h>
@@ -33,7 +40,8 @@ namespace gsw {
 namespace {
 
 constexpr int kThr = 256;
-enum LType { CONV = 0, MAXPOOL = 1, UPSAMPLE = 2 };
+enum LType { CONV = 0, MAXPOOL = 1, UPSAMPLE = 2, AVGPOOL = 3 };
+enum Act { LINEAR = 0, LEAKY = 1, YOLO = 2, RELU = 3 };
 
 // A tensor view: NHWC with a per-pixel pitch and a channel offset inside buffer `buf`.
 struct TView {
@@ -45,8 +53,8 @@ struct TView {
 
 struct LPlan {
   int type;
-  TView in, out;
-  int k, stride, cout, act;  // act: 0 linear, 1 leaky, 2 yolo
+  TView in, out, res;        // res.buf < 0: no residual
+  int k, stride, pad, cout, act;
   int kdim, kpad;            // im2row width (k*k*cin) and its 8-aligned pitch
   int64_t woff, boff;        // weight (bf16 elements) / bias (floats) offsets
 };
@@ -54,7 +62,6 @@ struct LPlan {
 struct NetPlan {
   std::vector<Buf> bufs;
   std::vector<LPlan> layers;
-  int out_buf = 3;
   int64_t flops = 0;
 };
 
@@ -62,27 +69,33 @@ constexpr int B_IMG = 0, B_W = 1, B_BIAS = 2, B_DET = 3, B_WS = 4;
 
 int64_t elems(const TView &v) { return (int64_t)v.n * v.h * v.w * v.pitch; }
 
-NetPlan yolo_plan(const gs_job_desc &j) {
+// Layer-by-layer plan builder: every layer output is its own resident buffer
+// (Darknet's l.output), weights / biases are packed into one buffer each.
+struct NetBuilder {
   NetPlan P;
-  const int S = (int)j.n, N = (int)j.m;
-  P.bufs.resize(5);
-  P.bufs[B_IMG] = {(int64_t)N * S * S * 3 * 2, IN};
-  int64_t wcount = 0, bcount = 0;
-  auto new_act = [&](int h, int w, int c, bool f32 = false) {
+  int N;
+  int64_t wcount = 0, bcount = 0, ws = 0;
+  explicit NetBuilder(int batch, int64_t img_elems) : N(batch) {
+    P.bufs.resize(5);
+    P.bufs[B_IMG] = {img_elems * 2, IN};
+  }
+  TView act(int h, int w, int c, bool f32 = false) {
     TView v{(int)P.bufs.size(), 0, N, h, w, c, c, f32};
     P.bufs.push_back({elems(v) * (f32 ? 4 : 2), WRK});
     return v;
-  };
-  int64_t ws = 0;
-  auto conv = [&](const TView &in, TView out, int k, int cout, int act) {
+  }
+  static TView none() { return TView{-1, 0, 0, 0, 0, 0, 0, false}; }
+  TView conv(const TView &in, TView out, int k, int stride, int cout, int a, TView res = none()) {
     LPlan L{};
     L.type = CONV;
     L.in = in;
     L.out = out;
+    L.res = res;
     L.k = k;
-    L.stride = 1;
+    L.stride = stride;
+    L.pad = k / 2;
     L.cout = cout;
-    L.act = act;
+    L.act = a;
     L.kdim = k * k * in.c;
     L.kpad = (L.kdim + 7) / 8 * 8;
     L.woff = wcount;
@@ -90,51 +103,72 @@ NetPlan yolo_plan(const gs_job_desc &j) {
     wcount += (int64_t)cout * L.kpad;
     wcount = (wcount + 7) / 8 * 8;  // 16-byte aligned next layer
     bcount += cout;
-    const int64_t pix = (int64_t)in.n * in.h * in.w;
-    if (!(k == 1 && in.pitch % 8 == 0 && in.off % 8 == 0)) ws = std::max(ws, pix * L.kpad * 2);
-    P.flops += 2 * pix * (int64_t)L.kdim * cout;
+    const int64_t opix = (int64_t)out.n * out.h * out.w;
+    if (!direct_gemm(L)) ws = std::max(ws, opix * L.kpad * 2);
+    P.flops += 2 * opix * (int64_t)L.kdim * cout;
     P.layers.push_back(L);
     return out;
-  };
-  auto pool = [&](const TView &in, int stride) {
-    const int ho = stride == 2 ? in.h / 2 : in.h, wo = stride == 2 ? in.w / 2 : in.w;
-    TView out = new_act(ho, wo, in.c);
+  }
+  // a 1x1 / stride-1 convolution reads the activation itself as the GEMM's A
+  static bool direct_gemm(const LPlan &L) {
+    return L.k == 1 && L.stride == 1 && L.in.pitch % 8 == 0 && L.in.off % 8 == 0;
+  }
+  TView pool(const TView &in, int k, int stride, int pad, int ho, int wo) {
+    TView out = act(ho, wo, in.c);
     LPlan L{};
     L.type = MAXPOOL;
     L.in = in;
     L.out = out;
-    L.k = 2;
+    L.res = none();
+    L.k = k;
     L.stride = stride;
+    L.pad = pad;
     P.layers.push_back(L);
     return out;
+  }
+  void finish(int64_t det_bytes) {
+    P.bufs[B_W] = {wcount * 2, IN};
+    P.bufs[B_BIAS] = {bcount * 4, IN};
+    P.bufs[B_DET] = {det_bytes, OUT};
+    P.bufs[B_WS] = {std::max<int64_t>(ws, 16), WRK};
+  }
+};
+
+NetPlan yolo_plan(const gs_job_desc &j) {
+  const int S = (int)j.n, N = (int)j.m;
+  NetBuilder B(N, (int64_t)N * S * S * 3);
+  // Darknet maxpool size 2: stride 2 halves the map, stride 1 keeps it
+  // (window [i, i+1] clipped at the edge: Darknet's pad = size - 1, offset 0)
+  auto pool2 = [&](const TView &in, int stride) {
+    return B.pool(in, 2, stride, 0, stride == 2 ? in.h / 2 : in.h, stride == 2 ? in.w / 2 : in.w);
   };
   TView x{B_IMG, 0, N, S, S, 3, 3, false};
   // yolov3-tiny.cfg
-  x = conv(x, new_act(S, S, 16), 3, 16, 1);                      // 0
-  x = pool(x, 2);                                                // 1
-  x = conv(x, new_act(S / 2, S / 2, 32), 3, 32, 1);              // 2
-  x = pool(x, 2);                                                // 3
-  x = conv(x, new_act(S / 4, S / 4, 64), 3, 64, 1);              // 4
-  x = pool(x, 2);                                                // 5
-  x = conv(x, new_act(S / 8, S / 8, 128), 3, 128, 1);            // 6
-  x = pool(x, 2);                                                // 7
+  x = B.conv(x, B.act(S, S, 16), 3, 1, 16, LEAKY);                      // 0
+  x = pool2(x, 2);                                                      // 1
+  x = B.conv(x, B.act(S / 2, S / 2, 32), 3, 1, 32, LEAKY);              // 2
+  x = pool2(x, 2);                                                      // 3
+  x = B.conv(x, B.act(S / 4, S / 4, 64), 3, 1, 64, LEAKY);              // 4
+  x = pool2(x, 2);                                                      // 5
+  x = B.conv(x, B.act(S / 8, S / 8, 128), 3, 1, 128, LEAKY);            // 6
+  x = pool2(x, 2);                                                      // 7
   // route target: [upsampled layer 18 (128) | layer 8 (256)] at S/16
-  TView cat = new_act(S / 16, S / 16, 384);
+  TView cat = B.act(S / 16, S / 16, 384);
   TView l8 = cat;
   l8.off = 128;
   l8.c = 256;
-  x = conv(x, l8, 3, 256, 1);                                    // 8 -> concat[128:384]
-  x = pool(x, 2);                                                // 9
-  x = conv(x, new_act(S / 32, S / 32, 512), 3, 512, 1);          // 10
-  x = pool(x, 1);                                                // 11 (size 2, stride 1)
-  x = conv(x, new_act(S / 32, S / 32, 1024), 3, 1024, 1);        // 12
-  TView l13 = conv(x, new_act(S / 32, S / 32, 256), 1, 256, 1);  // 13
-  x = conv(l13, new_act(S / 32, S / 32, 512), 3, 512, 1);        // 14
+  x = B.conv(x, l8, 3, 1, 256, LEAKY);                                  // 8 -> concat[128:384]
+  x = pool2(x, 2);                                                      // 9
+  x = B.conv(x, B.act(S / 32, S / 32, 512), 3, 1, 512, LEAKY);          // 10
+  x = pool2(x, 1);                                                      // 11 (size 2, stride 1)
+  x = B.conv(x, B.act(S / 32, S / 32, 1024), 3, 1, 1024, LEAKY);        // 12
+  TView l13 = B.conv(x, B.act(S / 32, S / 32, 256), 1, 1, 256, LEAKY);  // 13
+  x = B.conv(l13, B.act(S / 32, S / 32, 512), 3, 1, 512, LEAKY);        // 14
   // 15 + 16: conv 255 linear, YOLO head 1 -> det[0 : N*(S/32)^2*255]
   TView det1{B_DET, 0, N, S / 32, S / 32, 255, 255, true};
-  conv(x, det1, 1, 255, 2);
+  B.conv(x, det1, 1, 1, 255, YOLO);
   // 17 route 13; 18 conv 128 1x1; 19 upsample -> concat[0:128]
-  TView l18 = conv(l13, new_act(S / 32, S / 32, 128), 1, 128, 1);
+  TView l18 = B.conv(l13, B.act(S / 32, S / 32, 128), 1, 1, 128, LEAKY);
   {
     TView up = cat;
     up.c = 128;
@@ -142,19 +176,56 @@ NetPlan yolo_plan(const gs_job_desc &j) {
     L.type = UPSAMPLE;
     L.in = l18;
     L.out = up;
+    L.res = NetBuilder::none();
     L.stride = 2;
-    P.layers.push_back(L);
+    B.P.layers.push_back(L);
   }
   // 20 route 19, 8 (= cat); 21 conv 256 3x3; 22 conv 255 linear; 23 YOLO head 2
-  x = conv(cat, new_act(S / 16, S / 16, 256), 3, 256, 1);        // 21
+  x = B.conv(cat, B.act(S / 16, S / 16, 256), 3, 1, 256, LEAKY);        // 21
   TView det2{B_DET, (int64_t)N * (S / 32) * (S / 32) * 255, N, S / 16, S / 16, 255, 255, true};
-  conv(x, det2, 1, 255, 2);                                      // 22 + 23
-  P.bufs[B_W] = {wcount * 2, IN};
-  P.bufs[B_BIAS] = {bcount * 4, IN};
-  P.bufs[B_DET] = {((int64_t)N * (S / 32) * (S / 32) + (int64_t)N * (S / 16) * (S / 16)) * 255 * 4, OUT};
-  P.bufs[B_WS] = {std::max<int64_t>(ws, 16), WRK};
-  return P;
+  B.conv(x, det2, 1, 1, 255, YOLO);                                     // 22 + 23
+  B.finish(((int64_t)N * (S / 32) * (S / 32) + (int64_t)N * (S / 16) * (S / 16)) * 255 * 4);
+  return B.P;
 }
+
+// ResNet-50 (v1.5: stride on the 3x3 of the bottleneck), batch-norm folded
+NetPlan resnet50_plan(const gs_job_desc &j) {
+  const int S = (int)j.n, N = (int)j.m;
+  NetBuilder B(N, (int64_t)N * S * S * 3);
+  TView x{B_IMG, 0, N, S, S, 3, 3, false};
+  x = B.conv(x, B.act(S / 2, S / 2, 64), 7, 2, 64, RELU);      // stem 7x7/2
+  x = B.pool(x, 3, 2, 1, S / 4, S / 4);                        // max-pool 3x3/2, pad 1
+  const int mids[4] = {64, 128, 256, 512}, blocks[4] = {3, 4, 6, 3};
+  int hw = S / 4;
+  for (int st = 0; st < 4; ++st) {
+    const int mid = mids[st], outc = 4 * mid;
+    for (int bi = 0; bi < blocks[st]; ++bi) {
+      const int stride = (st > 0 && bi == 0) ? 2 : 1;
+      const int ohw = hw / stride;
+      TView a = B.conv(x, B.act(hw, hw, mid), 1, 1, mid, RELU);
+      TView b = B.conv(a, B.act(ohw, ohw, mid), 3, stride, mid, RELU);
+      TView sc = x;
+      if (bi == 0) sc = B.conv(x, B.act(ohw, ohw, outc), 1, stride, outc, LINEAR);  // projection
+      x = B.conv(b, B.act(ohw, ohw, outc), 1, 1, outc, RELU, sc);                  // + shortcut, ReLU
+      hw = ohw;
+    }
+  }
+  TView pooled = B.act(1, 1, 2048);
+  {
+    LPlan L{};
+    L.type = AVGPOOL;
+    L.in = x;
+    L.out = pooled;
+    L.res = NetBuilder::none();
+    B.P.layers.push_back(L);
+  }
+  TView logits{B_DET, 0, N, 1, 1, 1000, 1000, true};
+  B.conv(pooled, logits, 1, 1, 1000, LINEAR);                  // fully connected
+  B.finish((int64_t)N * 1000 * 4);
+  return B.P;
+}
+
+NetPlan net_plan(const gs_job_desc &j) { return j.kind == GS_JOB_RESNET ? resnet50_plan(j) : yolo_plan(j); }
 
 // ---- kernels ------------------------------------------------------------------
 
@@ -186,25 +257,26 @@ struct ViewArgs {
   int n, h, w, c, pitch;
 };
 
-// im2row, 3x3 / stride 1 / pad 1 (every yolov3-tiny conv with k > 1):
-// ws[pixel][(kh*3 + kw)*C + c], zero outside the image and in the pad columns.
-// 16-byte vectors when C % 8 == 0 (all layers but the first).
-__global__ void __launch_bounds__(kThr) im2row3(ViewArgs in, __nv_bfloat16 *ws, int kdim, int kpad) {
+// im2row for a k x k / stride / pad convolution: ws[out pixel][(kh*k + kw)*C
+// + c], zero outside the image and in the pad columns; 16-byte vectors when
+// C % 8 == 0 (all layers but the first).
+__global__ void __launch_bounds__(kThr) im2row(ViewArgs in, __nv_bfloat16 *ws, int k, int stride, int pad, int oh,
+                                               int ow, int kdim, int kpad) {
   const int C = in.c;
   const bool vec = (C % 8 == 0) && (in.pitch % 8 == 0);
-  const int64_t pix = (int64_t)in.n * in.h * in.w;
+  const int64_t pix = (int64_t)in.n * oh * ow;
   const int chunks = kpad / 8;
   const int64_t total = pix * chunks;
   for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
     const int64_t p = t / chunks;
     const int col0 = (int)(t % chunks) * 8;
-    const int ox = (int)(p % in.w), oy = (int)((p / in.w) % in.h), b = (int)(p / ((int64_t)in.w * in.h));
+    const int ox = (int)(p % ow), oy = (int)((p / ow) % oh), b = (int)(p / ((int64_t)ow * oh));
     uint4 out;
     if (vec) {
       out = make_uint4(0, 0, 0, 0);
       if (col0 < kdim) {
         const int tap = col0 / C, c = col0 % C;
-        const int iy = oy + tap / 3 - 1, ix = ox + tap % 3 - 1;
+        const int iy = oy * stride + tap / k - pad, ix = ox * stride + tap % k - pad;
         if (iy >= 0 && iy < in.h && ix >= 0 && ix < in.w)
           out = *reinterpret_cast<const uint4 *>(in.p + (((int64_t)b * in.h + iy) * in.w + ix) * in.pitch + c);
       }
@@ -216,7 +288,7 @@ __global__ void __launch_bounds__(kThr) im2row3(ViewArgs in, __nv_bfloat16 *ws, 
         float x = 0.0f;
         if (col < kdim) {
           const int tap = col / C, c = col % C;
-          const int iy = oy + tap / 3 - 1, ix = ox + tap % 3 - 1;
+          const int iy = oy * stride + tap / k - pad, ix = ox * stride + tap % k - pad;
           if (iy >= 0 && iy < in.h && ix >= 0 && ix < in.w)
             x = __bfloat162float(in.p[(((int64_t)b * in.h + iy) * in.w + ix) * in.pitch + c]);
         }
@@ -228,10 +300,10 @@ __global__ void __launch_bounds__(kThr) im2row3(ViewArgs in, __nv_bfloat16 *ws, 
   }
 }
 
-// Darknet maxpool, size 2: stride 2 halves the map; stride 1 keeps it
-// (window clipped at the bottom / right edge, Darknet's pad = size - 1).
-__global__ void __launch_bounds__(kThr) maxpool2(ViewArgs in, __nv_bfloat16 *out, int oh, int ow, int opitch,
-                                                 int stride) {
+// max-pool k x k / stride, window origin oy*stride - pad, taps outside the
+// map skipped (Darknet's size-2 pools: pad 0; ResNet's 3x3/2: pad 1)
+__global__ void __launch_bounds__(kThr) maxpool(ViewArgs in, __nv_bfloat16 *out, int oh, int ow, int opitch, int k,
+                                                int stride, int pad) {
   const int cv = in.c / 8;
   const int64_t total = (int64_t)in.n * oh * ow * cv;
   for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
@@ -240,10 +312,10 @@ __global__ void __launch_bounds__(kThr) maxpool2(ViewArgs in, __nv_bfloat16 *out
     const int ox = (int)(p % ow), oy = (int)((p / ow) % oh), b = (int)(p / ((int64_t)ow * oh));
     __nv_bfloat162 m[4];
     bool first = true;
-    for (int dy = 0; dy < 2; ++dy)
-      for (int dx = 0; dx < 2; ++dx) {
-        const int iy = oy * stride + dy, ix = ox * stride + dx;
-        if (iy >= in.h || ix >= in.w) continue;
+    for (int dy = 0; dy < k; ++dy)
+      for (int dx = 0; dx < k; ++dx) {
+        const int iy = oy * stride - pad + dy, ix = ox * stride - pad + dx;
+        if (iy < 0 || iy >= in.h || ix < 0 || ix >= in.w) continue;
         const uint4 v = *reinterpret_cast<const uint4 *>(in.p + (((int64_t)b * in.h + iy) * in.w + ix) * in.pitch + c);
         const __nv_bfloat162 *h = reinterpret_cast<const __nv_bfloat162 *>(&v);
 #pragma unroll
@@ -251,6 +323,20 @@ __global__ void __launch_bounds__(kThr) maxpool2(ViewArgs in, __nv_bfloat16 *out
         first = false;
       }
     *reinterpret_cast<uint4 *>(out + p * opitch + c) = *reinterpret_cast<uint4 *>(m);
+  }
+}
+
+// global average pool: [N, H, W, C] -> [N, 1, 1, C] (fp32 sums in pixel order)
+__global__ void __launch_bounds__(kThr) avgpool(ViewArgs in, __nv_bfloat16 *out, int opitch) {
+  const int64_t total = (int64_t)in.n * in.c;
+  const int hw = in.h * in.w;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+    const int c = (int)(t % in.c);
+    const int64_t b = t / in.c;
+    const __nv_bfloat16 *src = in.p + b * hw * in.pitch + c;
+    float s = 0.0f;
+    for (int q = 0; q < hw; ++q) s += __bfloat162float(src[(int64_t)q * in.pitch]);
+    out[b * opitch + c] = __float2bfloat16_rn(s / (float)hw);
   }
 }
 
@@ -359,31 +445,34 @@ int grid_for(int64_t total) { return (int)std::min<int64_t>((total + kThr - 1) /
 // ---- job hooks (gs_work_internal.h) ------------------------------------------
 
 int gemm_validate(const gs_job_desc &j) {
-  if (j.n < 32 || j.n % 32) return err(GS_ERR_CONFIG, "yolo input size must be a positive multiple of 32");
-  if (j.m < 1 || j.m > 1024) return err(GS_ERR_CONFIG, "yolo batch must be 1..1024");
-  if (j.iters < 1) return err(GS_ERR_CONFIG, "yolo needs at least one forward pass");
+  if (j.n < 32 || j.n % 32) return err(GS_ERR_CONFIG, "network input size must be a positive multiple of 32");
+  if (j.m < 1 || j.m > 1024) return err(GS_ERR_CONFIG, "network batch must be 1..1024");
+  if (j.iters < 1) return err(GS_ERR_CONFIG, "a network job needs at least one forward pass");
   return GS_OK;
 }
 
-std::vector<Buf> gemm_buffers(const gs_job_desc &j) { return yolo_plan(j).bufs; }
+std::vector<Buf> gemm_buffers(const gs_job_desc &j) { return net_plan(j).bufs; }
 
 // launch shapes for the probe: the widest launch (im2row / pool grids) and
 // the GEMM's dynamic shared memory (largest tile variant the net can pick)
 std::vector<Shape> gemm_launches(const gs_job_desc &j) {
-  const NetPlan P = yolo_plan(j);
+  const NetPlan P = net_plan(j);
   int bn_max = 32;
   for (const LPlan &L : P.layers)
     if (L.type == CONV)
-      bn_max = std::max(bn_max, gemm_pick_bn((int)((int64_t)L.in.n * L.in.h * L.in.w), L.cout));
+      bn_max = std::max(bn_max, gemm_pick_bn((int)((int64_t)L.out.n * L.out.h * L.out.w), L.cout));
   const int64_t pix0 = (int64_t)j.m * j.n * j.n;
   Shape g{gemm_kernel_fn(bn_max), 2 * kSMs, gemm_block_threads()};
   g.dsmem = (int)gemm_smem_for(bn_max);
-  return {g, {(const void *)im2row3, grid_for(pix0 * 4), kThr}, {(const void *)maxpool2, grid_for(pix0), kThr},
-          {(const void *)conv3x3_direct<3, 16>, grid_for(pix0), kThr}};
+  std::vector<Shape> v = {g, {(const void *)im2row, grid_for(pix0 * 4), kThr},
+                          {(const void *)maxpool, grid_for(pix0), kThr}};
+  if (j.kind == GS_JOB_YOLO) v.push_back({(const void *)conv3x3_direct<3, 16>, grid_for(pix0), kThr});
+  else v.push_back({(const void *)avgpool, grid_for(pix0), kThr});
+  return v;
 }
 
 int gemm_generate(const gs_job_desc &j, const std::vector<void *> &dst, cudaStream_t st) {
-  const NetPlan P = yolo_plan(j);
+  const NetPlan P = net_plan(j);
   const int64_t nimg = (int64_t)j.m * j.n * j.n * 3;
   gen_image<<<grid_for(nimg), kThr, 0, st>>>((__nv_bfloat16 *)dst[B_IMG], nimg, j.seed);
   int li = 0;
@@ -396,59 +485,66 @@ int gemm_generate(const gs_job_desc &j, const std::vector<void *> &dst, cudaStre
     ++li;
   }
   cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess) return err(GS_ERR_CUDA, std::string("yolo generate: ") + cudaGetErrorString(e));
+  if (e != cudaSuccess) return err(GS_ERR_CUDA, std::string("network generate: ") + cudaGetErrorString(e));
   return GS_OK;
 }
 
 int gemm_run(const gs_job_desc &j, std::vector<void *> &buf, cudaStream_t st, int *out_idx, int64_t *launches) {
-  const NetPlan P = yolo_plan(j);
+  const NetPlan P = net_plan(j);
   for (int pass = 0; pass < j.iters; ++pass) {
     for (const LPlan &L : P.layers) {
       const ViewArgs in = vargs(L.in, buf);
+      __nv_bfloat16 *obf = L.out.f32 ? nullptr : (__nv_bfloat16 *)buf[L.out.buf] + L.out.off;
       if (L.type == MAXPOOL) {
-        maxpool2<<<grid_for((int64_t)L.out.n * L.out.h * L.out.w * (L.in.c / 8)), kThr, 0, st>>>(
-            in, (__nv_bfloat16 *)buf[L.out.buf] + L.out.off, L.out.h, L.out.w, L.out.pitch, L.stride);
+        maxpool<<<grid_for((int64_t)L.out.n * L.out.h * L.out.w * (L.in.c / 8)), kThr, 0, st>>>(
+            in, obf, L.out.h, L.out.w, L.out.pitch, L.k, L.stride, L.pad);
         ++*launches;
         continue;
       }
       if (L.type == UPSAMPLE) {
-        upsample2<<<grid_for((int64_t)L.in.n * L.in.h * L.in.w * 4 * (L.in.c / 8)), kThr, 0, st>>>(
-            in, (__nv_bfloat16 *)buf[L.out.buf] + L.out.off, L.out.pitch);
+        upsample2<<<grid_for((int64_t)L.in.n * L.in.h * L.in.w * 4 * (L.in.c / 8)), kThr, 0, st>>>(in, obf,
+                                                                                                    L.out.pitch);
         ++*launches;
         continue;
       }
-      const int64_t pix = (int64_t)L.in.n * L.in.h * L.in.w;
-      if (L.k == 3 && L.act == 1 && !L.out.f32 && L.out.off % 8 == 0 && L.out.pitch % 8 == 0 && L.in.c == 3 &&
-          L.cout == 16) {
-        // layer 0 (K = 27): direct convolution (measured 0.6 ms vs 4.2 ms for
-        // im2row + GEMM at 608^2 x 32; for 16 -> 32 the GEMM path is faster)
-        conv3x3_direct<3, 16><<<grid_for(pix), kThr, 0, st>>>(in, (const __nv_bfloat16 *)buf[B_W] + L.woff, L.kpad,
-                                                              (const float *)buf[B_BIAS] + L.boff,
-                                                              (__nv_bfloat16 *)buf[L.out.buf] + L.out.off, L.out.pitch);
+      if (L.type == AVGPOOL) {
+        avgpool<<<grid_for((int64_t)L.in.n * L.in.c), kThr, 0, st>>>(in, obf, L.out.pitch);
+        ++*launches;
+        continue;
+      }
+      const int64_t opix = (int64_t)L.out.n * L.out.h * L.out.w;
+      if (L.k == 3 && L.stride == 1 && L.act == LEAKY && !L.out.f32 && L.out.off % 8 == 0 && L.out.pitch % 8 == 0 &&
+          L.in.c == 3 && L.cout == 16) {
+        // YOLO layer 0 (K = 27): direct convolution (measured 0.6 ms vs 4.2 ms
+        // for im2row + GEMM at 608^2 x 32; for 16 -> 32 the GEMM path is faster)
+        conv3x3_direct<3, 16><<<grid_for(opix), kThr, 0, st>>>(in, (const __nv_bfloat16 *)buf[B_W] + L.woff, L.kpad,
+                                                               (const float *)buf[B_BIAS] + L.boff, obf, L.out.pitch);
         ++*launches;
         continue;
       }
       const void *A;
       int64_t lda;
-      if (L.k == 1 && L.in.pitch % 8 == 0 && L.in.off % 8 == 0) {
+      if (NetBuilder::direct_gemm(L)) {
         A = in.p;  // 1x1 / stride 1: the activation is already the im2row matrix
         lda = L.in.pitch;
       } else {
-        im2row3<<<grid_for(pix * (L.kpad / 8)), kThr, 0, st>>>(in, (__nv_bfloat16 *)buf[B_WS], L.kdim, L.kpad);
+        im2row<<<grid_for(opix * (L.kpad / 8)), kThr, 0, st>>>(in, (__nv_bfloat16 *)buf[B_WS], L.k, L.stride, L.pad,
+                                                               L.out.h, L.out.w, L.kdim, L.kpad);
         ++*launches;
         A = buf[B_WS];
         lda = L.kpad;
       }
-      void *out = L.out.f32 ? (void *)((float *)buf[L.out.buf] + L.out.off)
-                            : (void *)((__nv_bfloat16 *)buf[L.out.buf] + L.out.off);
+      void *out = L.out.f32 ? (void *)((float *)buf[L.out.buf] + L.out.off) : (void *)obf;
+      const void *res = L.res.buf >= 0 ? (const void *)((const __nv_bfloat16 *)buf[L.res.buf] + L.res.off) : nullptr;
       int rc = gemm_bf16(A, lda, (const __nv_bfloat16 *)buf[B_W] + L.woff, L.kpad, (const float *)buf[B_BIAS] + L.boff,
-                         out, L.out.pitch, (int)pix, L.cout, L.kpad, L.out.f32 ? 1 : 0, L.act, 2 * kSMs, st);
+                         out, L.out.pitch, (int)opix, L.cout, L.kpad, L.out.f32 ? 1 : 0, L.act, 2 * kSMs, st, res,
+                         L.res.pitch);
       if (rc) return rc;
       ++*launches;
     }
   }
   cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess) return err(GS_ERR_CUDA, std::string("yolo run: ") + cudaGetErrorString(e));
+  if (e != cudaSuccess) return err(GS_ERR_CUDA, std::string("network run: ") + cudaGetErrorString(e));
   *out_idx = B_DET;
   return GS_OK;
 }

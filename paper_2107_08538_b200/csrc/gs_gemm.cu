@@ -36,7 +36,9 @@ struct GemmArgs {
   void *out;             // D + column offset
   int64_t ldo;           // row pitch of D (elements)
   int out_f32;           // 1: fp32 D, 0: bf16 D
-  int act;               // 0 linear, 1 leaky (0.1), 2 YOLO logistic
+  int act;               // 0 linear, 1 leaky (0.1), 2 YOLO logistic, 3 ReLU
+  const __nv_bfloat16 *res;  // residual added before the activation (bf16, pitch ldr) or nullptr
+  int64_t ldr;
 };
 
 // 3 stages x (16 KB A + <= 16 KB B) <= 99 KB: two CTAs per SM, so one CTA's
@@ -70,7 +72,32 @@ __device__ __forceinline__ void epilogue_store(const GemmArgs &g, int row, int c
   for (int i = 0; i < 32; ++i) {
     float x = v[i];
     if (g.bias && col0 + i < g.n) x += __ldg(g.bias + col0 + i);
-    v[i] = g.act == 1 ? leaky(x) : (g.act == 2 ? yolo_act(x, col0 + i) : x);
+    v[i] = x;
+  }
+  if (g.res) {  // ResNet shortcut: D = act(A.B^T + bias + R)
+    const __nv_bfloat16 *r = g.res + (int64_t)row * g.ldr + col0;
+    if (col0 + 32 <= g.n && ((reinterpret_cast<uintptr_t>(r) & 15) == 0)) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const uint4 u = *reinterpret_cast<const uint4 *>(r + 8 * q);
+        const __nv_bfloat162 *h = reinterpret_cast<const __nv_bfloat162 *>(&u);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const float2 f = __bfloat1622float2(h[e]);
+          v[8 * q + 2 * e] += f.x;
+          v[8 * q + 2 * e + 1] += f.y;
+        }
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < 32; ++i)
+        if (col0 + i < g.n) v[i] += __bfloat162float(r[i]);
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < 32; ++i) {
+    const float x = v[i];
+    v[i] = g.act == 1 ? leaky(x) : (g.act == 2 ? yolo_act(x, col0 + i) : (g.act == 3 ? fmaxf(x, 0.0f) : x));
   }
   const bool whole = col0 + 32 <= g.n;
   if (g.out_f32) {
@@ -278,7 +305,7 @@ int gemm_pick_bn(int m, int n) {
 // D = act(A . B^T + bias): A [m x k] (pitch lda), B [n x k] (pitch ldb), D
 // [m x n] at `out` (pitch ldo).  max_ctas bounds the grid (the job's SM share).
 int gemm_bf16(const void *A, int64_t lda, const void *B, int64_t ldb, const float *bias, void *out, int64_t ldo,
-              int m, int n, int k, int out_f32, int act, int max_ctas, cudaStream_t st) {
+              int m, int n, int k, int out_f32, int act, int max_ctas, cudaStream_t st, const void *res, int64_t ldr) {
   if (m <= 0 || n <= 0 || k <= 0) return err(GS_ERR_CONFIG, "gemm dims must be positive");
   if (k % 8) return err(GS_ERR_CONFIG, "gemm K must be a multiple of 8");
   const int bn = gemm_pick_bn(m, n);
@@ -298,6 +325,8 @@ int gemm_bf16(const void *A, int64_t lda, const void *B, int64_t ldb, const floa
   g.ldo = ldo;
   g.out_f32 = out_f32;
   g.act = act;
+  g.res = reinterpret_cast<const __nv_bfloat16 *>(res);
+  g.ldr = ldr;
   if (max_ctas <= 0) max_ctas = 2 * kSMs;
   switch (bn) {
     case 32: return launch_bn<32>(ta, tb, g, max_ctas, st);

@@ -78,6 +78,7 @@ std::vector<Buf> job_buffers(const gs_job_desc &j) {
       b = {{n * n * 4, INOUT}};
       break;
     case GS_JOB_YOLO:
+    case GS_JOB_RESNET:
       b = gemm_buffers(j);
       break;
     default:
@@ -106,6 +107,7 @@ int validate(const gs_job_desc &j) {
       if (j.m < 4 || j.m > kMaxHid || j.m % 4) return err(GS_ERR_CONFIG, "backprop hidden units must be 4, 8, 12 or 16");
       break;
     case GS_JOB_YOLO:
+    case GS_JOB_RESNET:
       return gemm_validate(j);
     default:
       break;
@@ -152,6 +154,7 @@ std::vector<Shape> job_launches(const gs_job_desc &j) {
       return {{(const void *)lud_panel, (int)(j.n / BS), 2 * BS},
               {(const void *)lud_internal, g, 256}};
     case GS_JOB_YOLO:
+    case GS_JOB_RESNET:
       return gemm_launches(j);
   }
   return {};
@@ -237,6 +240,7 @@ int generate_inputs(const gs_job_desc &j, const std::vector<void *> &dst, cudaSt
       gen_lud<<<g, kThreads, 0, st>>>((float *)dst[0], n, j.seed);
       break;
     case GS_JOB_YOLO:
+    case GS_JOB_RESNET:
       return gemm_generate(j, dst, st);
   }
   CUW(cudaGetLastError());
@@ -367,7 +371,8 @@ int run_kernels(const gs_job_desc &j, std::vector<void *> &buf, cudaStream_t st,
       *out_idx = 0;
       break;
     }
-    case GS_JOB_YOLO: {
+    case GS_JOB_YOLO:
+    case GS_JOB_RESNET: {
       int rc = gemm_run(j, buf, st, out_idx, &launches);
       if (rc) return rc;
       break;

@@ -53,6 +53,7 @@ size_t gemm_smem_for(int bn);
 int gemm_block_threads();
 const void *gemm_kernel_fn(int bn);
 int gemm_bf16(const void *A, int64_t lda, const void *B, int64_t ldb, const float *bias, void *out, int64_t ldo,
-              int m, int n, int k, int out_f32, int act, int max_ctas, cudaStream_t st);
+              int m, int n, int k, int out_f32, int act, int max_ctas, cudaStream_t st, const void *res = nullptr,
+              int64_t ldr = 0);
 
 }  // namespace gsw

@@ -18,7 +18,7 @@ import numpy as np
 
 from . import _native as nat
 
-KINDS = {"bfs": 0, "hotspot": 1, "srad": 2, "kmeans": 3, "backprop": 4, "needle": 5, "lud": 6, "yolo": 7}
+KINDS = {"bfs": 0, "hotspot": 1, "srad": 2, "kmeans": 3, "backprop": 4, "needle": 5, "lud": 6, "yolo": 7, "resnet": 8}
 KIND_NAMES = {v: k for k, v in KINDS.items()}
 MODE_DEVICE, MODE_E2E = 0, 1
 
@@ -101,13 +101,16 @@ def io_bytes(job: Job) -> tuple[int, int]:
 
 
 OUTPUT_DTYPES = {"bfs": np.int32, "hotspot": np.float32, "srad": np.float32, "kmeans": np.int32,
-                 "backprop": np.float32, "needle": np.int32, "lud": np.float32, "yolo": np.float32}
+                 "backprop": np.float32, "needle": np.int32, "lud": np.float32, "yolo": np.float32,
+                 "resnet": np.float32}
 
 
 def output_shape(job: Job) -> tuple[int, ...]:
     n = job.n
     if job.kind == "yolo":  # both YOLO heads, NHWC, 255 channels each
         return ((job.m * (n // 32) ** 2 + job.m * (n // 16) ** 2) * 255,)
+    if job.kind == "resnet":  # logits
+        return (job.m, 1000)
     return {"bfs": (n,), "hotspot": (n, n), "srad": (n, n), "kmeans": (n,), "backprop": (n + 1, job.m),
             "needle": (n + 1, n + 4), "lud": (n, n)}.get(job.kind, (0,))
 

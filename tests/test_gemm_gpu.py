@@ -89,3 +89,28 @@ def test_yolo_probe_matches_host_footprint_and_reports_gemm_smem():
     p = W.probe(job)
     assert p.mem_bytes == C.host_footprint(job)
     assert p.smem_per_block > 64 * 1024  # the tcgen05 GEMM's dynamic shared-memory ring is counted
+
+
+@pytest.mark.parametrize("S,N", [(64, 2), (96, 1)])
+def test_resnet50_job_matches_torch_reference(S, N):
+    """ResNet-50 job (im2row with strides + tcgen05 GEMM with the fused
+    shortcut + ReLU epilogue, max / average pools, FC) against torch fp32
+    with bf16 rounding at the same points.  Random He-init residual stacks
+    grow the activations, so the bar is relative to the largest logit:
+    max error < 5e-2, mean < 5e-3 of max |logit|."""
+    import yolo_ref
+
+    job = W.Job("resnet", n=S, m=N, iters=1, seed=13)
+    got, rec = W.run_solo(job)
+    assert rec.state == 0 and rec.n_kernels > 53
+    want = yolo_ref.resnet50_forward(S, N, 13).cpu().numpy()
+    scale = float(abs(want).max())
+    err = abs(got.reshape(-1).astype("float64") - want.astype("float64")) / scale
+    assert err.max() < 5e-2 and err.mean() < 5e-3, (err.max(), err.mean(), scale)
+
+
+def test_resnet_probe_matches_host_footprint():
+    from paper_2107_08538_b200 import catalog as C
+
+    job = W.Job("resnet", n=224, m=4, iters=1, seed=1)
+    assert W.probe(job).mem_bytes == C.host_footprint(job)

@@ -76,3 +76,48 @@ def forward(S: int, N: int, seed: int, device="cuda"):
     x = conv(cat, 11, "leaky")
     det2 = conv(x, 12, "yolo")
     return torch.cat([det1.permute(0, 2, 3, 1).reshape(-1), det2.permute(0, 2, 3, 1).reshape(-1)])
+
+
+def resnet50_forward(S: int, N: int, seed: int, device="cuda"):
+    """ResNet-50 (v1.5, folded batch-norm) job reference: same filters /
+    biases as csrc/gs_darknet.cu resnet50_plan (conv li from seed+100+li /
+    seed+200+li, plan order), bf16 rounding wherever the job stores bf16
+    (every activation, the pooled features); logits in fp32."""
+    import torch
+    import torch.nn.functional as F
+
+    from paper_2107_08538_b200.catalog import resnet50_convs
+
+    def bf(t):
+        return t.to(torch.bfloat16).float()
+
+    img = R.unit(seed, np.arange(N * S * S * 3, dtype=np.uint64)).reshape(N, S, S, 3)
+    x = bf(torch.from_numpy(img).to(device).permute(0, 3, 1, 2).contiguous())
+    convs = resnet50_convs(S)
+    params = []
+    for li, (_, cin, cout, k, stride, _) in enumerate(convs):
+        w, b = filters(seed, li, cin, cout, k)
+        params.append((bf(torch.from_numpy(w).to(device).permute(0, 3, 1, 2).contiguous()),
+                       torch.from_numpy(b).to(device), k, stride))
+    it = iter(range(len(convs)))
+
+    def conv(x, act="relu", res=None):
+        w, b, k, stride = params[next(it)]
+        y = F.conv2d(x, w, b, stride=stride, padding=k // 2)
+        if res is not None:
+            y = y + res
+        if act == "relu":
+            y = torch.relu(y)
+        return bf(y)
+
+    x = conv(x)                                      # stem 7x7/2
+    x = F.max_pool2d(x, 3, 2, 1)
+    for mid, blocks in ((64, 3), (128, 4), (256, 6), (512, 3)):
+        for bi in range(blocks):
+            a = conv(x)
+            b = conv(a)
+            sc = conv(x, act=None) if bi == 0 else x
+            x = conv(b, res=sc)
+    pooled = bf(x.mean(dim=(2, 3)))
+    w, b, _, _ = params[next(it)]
+    return (pooled @ w.view(w.shape[0], -1).T + b).reshape(-1)
