@@ -152,7 +152,7 @@ std::vector<Shape> job_launches(const gs_job_desc &j) {
       return {{(const void *)needle_bands, needle_grid(j), 32}};
     case GS_JOB_LUD:
       return {{(const void *)lud_panel, (int)(j.n / BS), 2 * BS},
-              {(const void *)lud_internal, g, 256}};
+              {(const void *)lud_internal, g, 256, kLudSmem2}};
     case GS_JOB_YOLO:
     case GS_JOB_RESNET:
       return gemm_launches(j);
@@ -359,14 +359,30 @@ int run_kernels(const gs_job_desc &j, std::vector<void *> &buf, cudaStream_t st,
       break;
     }
     case GS_JOB_LUD: {
+      // Steps in pairs with look-ahead: panel(o); update only block row and
+      // column o+32 with step o (what panel(o+32) reads); panel(o+32); then
+      // one pass applies steps o and o+32 to the rest of the trailing matrix
+      // (bit-identical to two passes, half the traffic).
       float *a = (float *)buf[0];
-      for (int o = 0; o < n; o += BS) {
-        const int panels = (int)((n - o) / BS - 1);
-        lud_panel<<<panels > 0 ? panels : 1, 2 * BS, 0, st>>>(a, (int)n, o);
+      const int N = (int)n;
+      CUW(cudaFuncSetAttribute(lud_internal, cudaFuncAttributeMaxDynamicSharedMemorySize, kLudSmem2));
+      auto panel = [&](int o) {
+        const int panels = (N - o) / BS - 1;
+        lud_panel<<<panels > 0 ? panels : 1, 2 * BS, 0, st>>>(a, N, o);
         ++launches;
-        if (o + BS >= n) break;
-        lud_internal<<<g, 256, 0, st>>>(a, (int)n, o, tk);
+      };
+      auto update = [&](int o, int rb, int re, int cb, int ce, int two) {
+        if (re <= rb || ce <= cb) return;
+        lud_internal<<<g, 256, kLudSmem2, st>>>(a, N, o, rb, re, cb, ce, two, tk);
         ++launches;
+      };
+      for (int o = 0; o < N; o += 2 * BS) {
+        panel(o);
+        if (o + BS >= N) break;
+        update(o, o + BS, o + 2 * BS, o + BS, N, 0);        // block row o+32 (incl. the diagonal block)
+        update(o, o + 2 * BS, N, o + BS, o + 2 * BS, 0);    // block column o+32 below it
+        panel(o + BS);
+        update(o, o + 2 * BS, N, o + 2 * BS, N, 1);         // the rest: steps o and o+32 in one pass
       }
       *out_idx = 0;
       break;
