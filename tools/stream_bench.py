@@ -3,8 +3,8 @@
     python tools/stream_bench.py --config 2 [--jobs 32] [--seed 1]
     python tools/stream_bench.py --config 3 [--jobs 128] [--seed 1] [--load 0.7]
 
-cfg 2  Darknet YOLOv3-tiny inference mix (random init, batch 32-64, image
-       edge 1280-1792: 8-33 GB per job) whose co-running footprint exceeds
+cfg 2  Darknet YOLOv3-tiny + ResNet-50 inference mix (random init, batch
+       32-64, large images: 7-33 GB per job) whose co-running footprint exceeds
        the device: run under mgb-warps (memory-safe), cg:8 (no memory
        check) and sa; reports jobs/s, mean turnaround and OOMs per policy.
 cfg 3  a 128-job stream mixing cfg 1's Rodinia jobs with cfg 2's Darknet
@@ -33,19 +33,24 @@ from paper_2107_08538_b200 import workloads as W  # noqa: E402
 GIB = 1 << 30
 
 
-def darknet_mix(n: int, seed: int, sizes=(416, 608, 832, 1024), batches=(1, 2, 4, 8, 16, 32, 64)) -> list[W.Job]:
+def darknet_mix(n: int, seed: int, sizes=(416, 608, 832, 1024), batches=(1, 2, 4, 8, 16, 32, 64),
+                resnet_sizes=(224, 448)) -> list[W.Job]:
+    """Half YOLOv3-tiny, half ResNet-50 inference jobs (BASELINE cfg 2)."""
     rng = random.Random(f"{seed}|darknet|{n}")
     out = []
     for i in range(n):
-        S = rng.choice(sizes)
         B = rng.choice(batches)
-        out.append(W.Job("yolo", n=S, m=B, iters=1, seed=seed * 1000 + i))
+        if rng.random() < 0.5:
+            out.append(W.Job("yolo", n=rng.choice(sizes), m=B, iters=1, seed=seed * 1000 + i))
+        else:
+            out.append(W.Job("resnet", n=rng.choice(resnet_sizes), m=B, iters=1, seed=seed * 1000 + i))
     return out
 
 
 # cfg 2: jobs large enough that 8 co-running ones exceed the device (Darknet
-# keeps every layer's output resident: 8-33 GB per job at these sizes)
-CFG2_SIZES, CFG2_BATCHES = (1280, 1536, 1792), (32, 64)
+# keeps every layer's output resident: 8-33 GB per YOLO job, 7-28 GB per
+# ResNet-50 job at these sizes)
+CFG2_SIZES, CFG2_BATCHES, CFG2_RESNET = (1280, 1536, 1792), (32, 64), (896, 1152)
 
 
 def summarize(res, solo=None) -> dict:
@@ -66,11 +71,11 @@ def summarize(res, solo=None) -> dict:
 
 
 def cfg2(args):
-    jobs = darknet_mix(args.jobs, args.seed, CFG2_SIZES, CFG2_BATCHES)
+    jobs = darknet_mix(args.jobs, args.seed, CFG2_SIZES, CFG2_BATCHES, CFG2_RESNET)
     foot = sum(C.host_footprint(j) for j in jobs)
     for policy in ("mgb-warps", "cg:8", "sa"):
         res = W.run_jobs(jobs, policy=policy, workers=args.workers)
-        line = {"config": "cfg2 darknet yolov3-tiny mix", "policy": policy, "jobs": len(jobs),
+        line = {"config": "cfg2 darknet yolov3-tiny + resnet-50 mix", "policy": policy, "jobs": len(jobs),
                 "sum_footprint_gib": round(foot / GIB, 1), **summarize(res)}
         print(json.dumps(line), flush=True)
 
