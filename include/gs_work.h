@@ -62,6 +62,12 @@ typedef struct gs_job_record {
     uint64_t checksum;    /* order-independent digest of the job's outputs */
     int32_t n_kernels;
     int32_t pad;
+    /* where a job's wall time goes (diagnostics): host time from admission
+     * to the inputs' launches returning, device time from the job's first
+     * queued op to its first kernel (input fill / generation, including
+     * waiting for an SM), and from its last kernel to the output digest's
+     * readback */
+    double setup_ms, gen_ms, tail_ms;
 } gs_job_record;
 
 typedef struct gs_exec_stats {

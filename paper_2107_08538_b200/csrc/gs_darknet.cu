@@ -489,7 +489,8 @@ int gemm_generate(const gs_job_desc &j, const std::vector<void *> &dst, cudaStre
   return GS_OK;
 }
 
-int gemm_run(const gs_job_desc &j, std::vector<void *> &buf, cudaStream_t st, int *out_idx, int64_t *launches) {
+int gemm_run(const gs_job_desc &j, std::vector<void *> &buf, cudaStream_t st, int *out_idx, int64_t *launches,
+             unsigned *tk) {
   const NetPlan P = net_plan(j);
   for (int pass = 0; pass < j.iters; ++pass) {
     for (const LPlan &L : P.layers) {
@@ -538,7 +539,7 @@ int gemm_run(const gs_job_desc &j, std::vector<void *> &buf, cudaStream_t st, in
       const void *res = L.res.buf >= 0 ? (const void *)((const __nv_bfloat16 *)buf[L.res.buf] + L.res.off) : nullptr;
       int rc = gemm_bf16(A, lda, (const __nv_bfloat16 *)buf[B_W] + L.woff, L.kpad, (const float *)buf[B_BIAS] + L.boff,
                          out, L.out.pitch, (int)opix, L.cout, L.kpad, L.out.f32 ? 1 : 0, L.act, 2 * kSMs, st, res,
-                         L.res.pitch);
+                         L.res.pitch, tk);
       if (rc) return rc;
       ++*launches;
     }

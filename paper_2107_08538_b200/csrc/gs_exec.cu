@@ -22,6 +22,7 @@
 #include <atomic>
 #include <chrono>
 #include <condition_variable>
+#include <functional>
 #include <mutex>
 #include <string>
 #include <thread>
@@ -42,6 +43,8 @@ using namespace gsw;
 namespace {
 
 using Clock = std::chrono::steady_clock;
+
+static const bool g_alloc_log = getenv("GS_ALLOC_LOG") != nullptr;
 
 double ms_since(Clock::time_point t0) {
   return std::chrono::duration<double, std::milli>(Clock::now() - t0).count();
@@ -130,6 +133,7 @@ int run_job(const gs_job_desc &j, const Staged *stg, int mode, cudaStream_t st, 
             void *host_out, int64_t host_out_bytes, int32_t *host_scalar, std::atomic<int64_t> *kernel_count,
             unsigned long long *host_sum, int device) {
   *oom = false;
+  const auto t_admit = Clock::now();
   const std::vector<Buf> bufs = job_buffers(j);
   std::vector<void *> buf(bufs.size(), nullptr);
   unsigned long long *dsum = nullptr;
@@ -140,7 +144,22 @@ int run_job(const gs_job_desc &j, const Staged *stg, int mode, cudaStream_t st, 
     cudaStreamSynchronize(st);
   };
   for (size_t i = 0; i < bufs.size(); ++i) {
+    const auto ta = Clock::now();
     cudaError_t e = cudaMallocAsync(&buf[i], bufs[i].bytes, st);
+    if (g_alloc_log && ms_since(ta) > 5.0)
+      fprintf(stderr, "[gs alloc] %.1f ms for %lld B (rc %d)\n", ms_since(ta), (long long)bufs[i].bytes, (int)e);
+    if (e == cudaErrorMemoryAllocation) {
+      // the pool may hold enough free memory in chunks too small for this
+      // buffer: give the unused chunks back and retry once
+      cudaGetLastError();
+      cudaMemPool_t pool;
+      const auto tt = Clock::now();
+      if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) cudaMemPoolTrimTo(pool, 0);
+      e = cudaMallocAsync(&buf[i], bufs[i].bytes, st);
+      if (g_alloc_log)
+        fprintf(stderr, "[gs alloc] trim+retry %.1f ms for %lld B (rc %d)\n", ms_since(tt), (long long)bufs[i].bytes,
+                (int)e);
+    }
     if (e != cudaSuccess) {
       cudaGetLastError();
       buf[i] = nullptr;
@@ -160,6 +179,12 @@ int run_job(const gs_job_desc &j, const Staged *stg, int mode, cudaStream_t st, 
     *oom = true;
     return GS_OK;
   }
+  cudaEvent_t es, e0, e1, ed;
+  CUE(cudaEventCreate(&es));
+  CUE(cudaEventCreate(&e0));
+  CUE(cudaEventCreate(&e1));
+  CUE(cudaEventCreate(&ed));
+  CUE(cudaEventRecord(es, st));
   CUE(cudaMemsetAsync(dsum, 0, 32, st));
   // inputs in
   for (size_t i = 0; i < bufs.size(); ++i) {
@@ -182,9 +207,7 @@ int run_job(const gs_job_desc &j, const Staged *stg, int mode, cudaStream_t st, 
     int rc = generate_inputs(j, buf, st);
     if (rc) return rc;
   }
-  cudaEvent_t e0, e1;
-  CUE(cudaEventCreate(&e0));
-  CUE(cudaEventCreate(&e1));
+  rec.setup_ms = ms_since(t_admit);
   CUE(cudaEventRecord(e0, st));
   int out_idx = 0;
   int64_t launches = 0;
@@ -216,13 +239,20 @@ int run_job(const gs_job_desc &j, const Staged *stg, int mode, cudaStream_t st, 
   }
   CUE(cudaMemcpyAsync(host_sum, dsum, 8, cudaMemcpyDeviceToHost, st));
   rec.d2h_bytes += 8;
+  CUE(cudaEventRecord(ed, st));
   CUE(cudaStreamSynchronize(st));
   float ms = 0;
   CUE(cudaEventElapsedTime(&ms, e0, e1));
   rec.compute_ms = ms;
+  CUE(cudaEventElapsedTime(&ms, es, e0));
+  rec.gen_ms = ms;
+  CUE(cudaEventElapsedTime(&ms, e1, ed));
+  rec.tail_ms = ms;
   rec.checksum = *host_sum;
+  cudaEventDestroy(es);
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
+  cudaEventDestroy(ed);
   release();
   return GS_OK;
 }
@@ -265,6 +295,38 @@ void gs_exec_unstage(void) {
   g_staged.clear();
 }
 
+// The device pool jobs allocate from.  Growing a stream-ordered pool maps
+// fresh physical memory (measured ~5.5 ms per GiB on B200) under a driver
+// lock every worker thread then waits on, and a pool grown piecemeal by
+// jobs of different sizes fragments.  So the pool never trims
+// (release threshold = max) and, before a run, it is grown ONCE, as one
+// chunk, to `need` bytes: the most the run can have allocated at a time.
+static void prepare_pool(int device, int64_t need) {
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, device) != cudaSuccess) return;
+  uint64_t thr = UINT64_MAX;
+  cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  uint64_t reserved = 0, used = 0;
+  cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &reserved);
+  cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &used);
+  if (need <= 0 || (int64_t)(reserved - used) >= need) return;
+  int prev = 0;
+  cudaGetDevice(&prev);
+  cudaSetDevice(device);
+  cudaStream_t st;
+  if (cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking) == cudaSuccess) {
+    const auto t = Clock::now();
+    if (used == 0) cudaMemPoolTrimTo(pool, 0);  // start from one clean chunk
+    void *p = nullptr;
+    if (cudaMallocAsync(&p, (size_t)need, st) == cudaSuccess) cudaFreeAsync(p, st);
+    cudaGetLastError();  // a pool that cannot grow that far still works, piecemeal
+    cudaStreamSynchronize(st);
+    cudaStreamDestroy(st);
+    if (g_alloc_log) fprintf(stderr, "[gs alloc] pool grown to %lld B in %.1f ms\n", (long long)need, ms_since(t));
+  }
+  cudaSetDevice(prev);
+}
+
 int gs_job_run_solo(const gs_job_desc *job, int cuda_device, int mode, void *host_out, int64_t host_out_bytes,
                     gs_job_record *rec) {
   int rc = validate(*job);
@@ -284,6 +346,10 @@ int gs_job_run_solo(const gs_job_desc *job, int cuda_device, int mode, void *hos
     stg = find_staged(*job);
   }
   bool oom = false;
+  {
+    gs_probe pr;
+    if (gs_job_probe(job, &pr) == GS_OK) prepare_pool(cuda_device, pr.mem_bytes);
+  }
   const auto t0 = Clock::now();
   rc = run_job(*job, stg, mode, st, *rec, &oom, host_out, host_out_bytes, scalar, &kc, hsum, cuda_device);
   rec->end_ms = ms_since(t0);
@@ -329,6 +395,12 @@ int gs_exec_run_arrivals(const gs_job_desc *jobs, int32_t n_jobs, const double *
     CUE(cudaDeviceGetDefaultMemPool(&pool, cuda_devices[d]));
     uint64_t thr = UINT64_MAX;
     CUE(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+    // memory an earlier run left mapped in the pool is free for this run's
+    // jobs: cudaMemGetInfo counts it as used
+    uint64_t reserved = 0, used = 0;
+    CUE(cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &reserved));
+    CUE(cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &used));
+    if (reserved > used) free_b += (size_t)(reserved - used);
     gs_spec spec;
     spec.sm_count = prop.multiProcessorCount;
     spec.mem_bytes = ledger_bytes > 0 ? ledger_bytes : (int64_t)free_b - (int64_t)(6ll << 30);
@@ -338,6 +410,19 @@ int gs_exec_run_arrivals(const gs_job_desc *jobs, int32_t n_jobs, const double *
     spec.smem_per_sm_bytes = (int64_t)prop.sharedMemPerMultiprocessor;
     rc = gs_device_create(eng, &spec, d, &ledgers[d]);
     if (rc) return err(rc, gs_last_error());
+    // at most `workers` jobs hold memory at once: the pool needs the sum of
+    // the largest `workers` footprints, capped by the ledger
+    std::vector<int64_t> foot;
+    foot.reserve(n_jobs);
+    for (int i = 0; i < n_jobs; ++i) {
+      gs_probe pr;
+      if (gs_job_probe(&jobs[i], &pr) == GS_OK) foot.push_back(pr.mem_bytes);
+    }
+    const size_t k = std::min(foot.size(), (size_t)std::max(workers, 1));
+    std::partial_sort(foot.begin(), foot.begin() + k, foot.end(), std::greater<int64_t>());
+    int64_t need = 0;
+    for (size_t i = 0; i < k; ++i) need += foot[i];
+    prepare_pool(cuda_devices[d], std::min(need, spec.mem_bytes));
   }
   gs_sched *sched = nullptr;
   rc = gs_sched_create(eng, ledgers.data(), n_devices, policy, cg_ratio, 1, &sched);

@@ -20,6 +20,7 @@
 #include <stdint.h>
 #include <string.h>
 
+#include <atomic>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -39,6 +40,7 @@ struct GemmArgs {
   int act;               // 0 linear, 1 leaky (0.1), 2 YOLO logistic, 3 ReLU
   const __nv_bfloat16 *res;  // residual added before the activation (bf16, pitch ldr) or nullptr
   int64_t ldr;
+  unsigned *tk;          // the job's tile tickets (gs_kernels.cuh grab_tile) or nullptr: static striding
 };
 
 // 3 stages x (16 KB A + <= 16 KB B) <= 99 KB: two CTAs per SM, so one CTA's
@@ -132,10 +134,29 @@ __device__ __forceinline__ void epilogue_store(const GemmArgs &g, int row, int c
   }
 }
 
-// Persistent, warp-specialized: tiles are strided over the grid; the TMA
-// producer runs ahead through the 4-stage ring across tile boundaries, the
-// MMA warp alternates between two TMEM accumulators, and the four epilogue
-// warps drain accumulator t while the MMAs of tile t+1 run.
+// The producer's next tile: a ticket from the job's counter (co-location
+// friendly: a CTA that starts late behind another job's kernel finds fewer
+// tiles left instead of owing a fixed share), or static striding without
+// one.  The retirement protocol is grab_tile's: the last CTA out resets the
+// counter for the next kernel on the job's stream.
+__device__ __forceinline__ int gemm_next_tile(const GemmArgs &g, int i, int tiles) {
+  if (!g.tk) return blockIdx.x + i * gridDim.x;
+  const unsigned t = atomicAdd(&g.tk[0], 1u);
+  if ((int64_t)t < tiles) return (int)t;
+  __threadfence();
+  if (atomicAdd(&g.tk[1], 1u) == gridDim.x - 1) {
+    atomicExch(&g.tk[0], 0u);
+    atomicExch(&g.tk[1], 0u);
+  }
+  return tiles;
+}
+
+// Persistent, warp-specialized: the TMA producer takes tiles (tickets or
+// static striding) and publishes each tile index through a 4-slot smem queue
+// to the MMA warp and the epilogue warps; it runs ahead through the 3-stage
+// operand ring across tile boundaries, the MMA warp alternates between two
+// TMEM accumulators, and the four epilogue warps drain accumulator t while
+// the MMAs of tile t+1 run.
 template <int BN>
 __global__ void __launch_bounds__(kGemmThreads, 2) gemm_bf16_tc(const __grid_constant__ CUtensorMap ta,
                                                                 const __grid_constant__ CUtensorMap tb, GemmArgs g) {
@@ -150,7 +171,10 @@ __global__ void __launch_bounds__(kGemmThreads, 2) gemm_bf16_tc(const __grid_con
   uint64_t *empty = full + kGemmStages;
   uint64_t *acc_full = empty + kGemmStages;  // [2]
   uint64_t *acc_empty = acc_full + 2;        // [2]
-  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(acc_empty + 2);
+  uint64_t *tq_full = acc_empty + 2;         // [4] tile index published
+  uint64_t *tq_empty = tq_full + 4;          // [4] read by the MMA thread and the 4 epilogue warps
+  volatile int *tq = reinterpret_cast<volatile int *>(tq_empty + 4);  // [4]
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tq_empty + 4) + 4;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   if (warp == 0 && lane == 0) {
@@ -163,6 +187,10 @@ __global__ void __launch_bounds__(kGemmThreads, 2) gemm_bf16_tc(const __grid_con
     for (int a = 0; a < 2; ++a) {
       mbar_init(&acc_full[a], 1);
       mbar_init(&acc_empty[a], 4);  // one arrival per epilogue warp
+    }
+    for (int s = 0; s < 4; ++s) {
+      mbar_init(&tq_full[s], 1);
+      mbar_init(&tq_empty[s], 5);
     }
     fence_mbar_init();
   }
@@ -177,7 +205,12 @@ __global__ void __launch_bounds__(kGemmThreads, 2) gemm_bf16_tc(const __grid_con
   if (warp == 0) {
     if (lane == 0) {  // TMA producer
       uint32_t stage = 0, phase = 0;
-      for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+      for (int i = 0;; ++i) {
+        mbar_wait(&tq_empty[i & 3], ((i >> 2) & 1) ^ 1);
+        const int tile = gemm_next_tile(g, i, tiles);
+        tq[i & 3] = tile;
+        mbar_arrive(&tq_full[i & 3]);
+        if (tile >= tiles) break;
         const int mt = tile / g.n_tiles, nt = tile % g.n_tiles;
         for (int kb = 0; kb < g.k_blocks; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
@@ -194,8 +227,11 @@ __global__ void __launch_bounds__(kGemmThreads, 2) gemm_bf16_tc(const __grid_con
   } else if (warp == 1) {
     if (lane == 0) {  // MMA issuer
       uint32_t stage = 0, phase = 0;
-      int t = 0;
-      for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x, ++t) {
+      for (int t = 0;; ++t) {
+        mbar_wait(&tq_full[t & 3], (t >> 2) & 1);
+        const int tile = tq[t & 3];
+        mbar_arrive(&tq_empty[t & 3]);
+        if (tile >= tiles) break;
         const int acc = t & 1;
         mbar_wait(&acc_empty[acc], ((t >> 1) & 1) ^ 1);  // epilogue drained this accumulator
         tc_fence_after();
@@ -219,8 +255,12 @@ __global__ void __launch_bounds__(kGemmThreads, 2) gemm_bf16_tc(const __grid_con
   } else {
     // epilogue warps 2..5: TMEM lane quarter (warp % 4) = tile rows 32q .. 32q+31
     const int q = warp & 3;
-    int t = 0;
-    for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x, ++t) {
+    for (int t = 0;; ++t) {
+      mbar_wait(&tq_full[t & 3], (t >> 2) & 1);
+      const int tile = tq[t & 3];
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tq_empty[t & 3]);
+      if (tile >= tiles) break;
       const int mt = tile / g.n_tiles, nt = tile % g.n_tiles;
       const int acc = t & 1;
       mbar_wait(&acc_full[acc], (t >> 1) & 1);
@@ -282,10 +322,20 @@ static int make_tmap(CUtensorMap *m, const void *ptr, int64_t rows, int64_t k, i
 
 template <int BN>
 static int launch_bn(const CUtensorMap &ta, const CUtensorMap &tb, GemmArgs g, int max_ctas, cudaStream_t st) {
-  // per launch: the attribute is per device, and the executor may drive several
-  const cudaError_t attr_rc =
-      cudaFuncSetAttribute(gemm_bf16_tc<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gemm_smem_bytes<BN>());
-  if (attr_rc != cudaSuccess) return err(GS_ERR_CUDA, std::string("gemm smem attribute: ") + cudaGetErrorString(attr_rc));
+  // the attribute is per device (the executor may drive several); set it on
+  // a device's first launch only -- a driver call per launch serializes the
+  // executor's worker threads on the context lock
+  static std::atomic<uint64_t> configured{0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const uint64_t bit = 1ull << (dev & 63);
+  if (!(configured.load(std::memory_order_acquire) & bit)) {
+    const cudaError_t attr_rc = cudaFuncSetAttribute(gemm_bf16_tc<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                     (int)gemm_smem_bytes<BN>());
+    if (attr_rc != cudaSuccess)
+      return err(GS_ERR_CUDA, std::string("gemm smem attribute: ") + cudaGetErrorString(attr_rc));
+    configured.fetch_or(bit, std::memory_order_acq_rel);
+  }
   g.n_tiles = (g.n + BN - 1) / BN;
   const int tiles = g.m_tiles * g.n_tiles;
   const int grid = tiles < max_ctas ? tiles : max_ctas;
@@ -305,7 +355,8 @@ int gemm_pick_bn(int m, int n) {
 // D = act(A . B^T + bias): A [m x k] (pitch lda), B [n x k] (pitch ldb), D
 // [m x n] at `out` (pitch ldo).  max_ctas bounds the grid (the job's SM share).
 int gemm_bf16(const void *A, int64_t lda, const void *B, int64_t ldb, const float *bias, void *out, int64_t ldo,
-              int m, int n, int k, int out_f32, int act, int max_ctas, cudaStream_t st, const void *res, int64_t ldr) {
+              int m, int n, int k, int out_f32, int act, int max_ctas, cudaStream_t st, const void *res, int64_t ldr,
+              unsigned *tk) {
   if (m <= 0 || n <= 0 || k <= 0) return err(GS_ERR_CONFIG, "gemm dims must be positive");
   if (k % 8) return err(GS_ERR_CONFIG, "gemm K must be a multiple of 8");
   const int bn = gemm_pick_bn(m, n);
@@ -327,6 +378,7 @@ int gemm_bf16(const void *A, int64_t lda, const void *B, int64_t ldb, const floa
   g.act = act;
   g.res = reinterpret_cast<const __nv_bfloat16 *>(res);
   g.ldr = ldr;
+  g.tk = tk;
   if (max_ctas <= 0) max_ctas = 2 * kSMs;
   switch (bn) {
     case 32: return launch_bn<32>(ta, tb, g, max_ctas, st);

@@ -389,7 +389,7 @@ int run_kernels(const gs_job_desc &j, std::vector<void *> &buf, cudaStream_t st,
     }
     case GS_JOB_YOLO:
     case GS_JOB_RESNET: {
-      int rc = gemm_run(j, buf, st, out_idx, &launches);
+      int rc = gemm_run(j, buf, st, out_idx, &launches, tk);
       if (rc) return rc;
       break;
     }

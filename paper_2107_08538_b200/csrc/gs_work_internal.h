@@ -47,13 +47,14 @@ int64_t round_granule(int64_t b);
 std::vector<Buf> gemm_buffers(const gs_job_desc &j);
 int gemm_validate(const gs_job_desc &j);
 int gemm_generate(const gs_job_desc &j, const std::vector<void *> &dst, cudaStream_t st);
-int gemm_run(const gs_job_desc &j, std::vector<void *> &buf, cudaStream_t st, int *out_idx, int64_t *launches);
+int gemm_run(const gs_job_desc &j, std::vector<void *> &buf, cudaStream_t st, int *out_idx, int64_t *launches,
+             unsigned *tk);
 int gemm_pick_bn(int m, int n);
 size_t gemm_smem_for(int bn);
 int gemm_block_threads();
 const void *gemm_kernel_fn(int bn);
 int gemm_bf16(const void *A, int64_t lda, const void *B, int64_t ldb, const float *bias, void *out, int64_t ldo,
               int m, int n, int k, int out_f32, int act, int max_ctas, cudaStream_t st, const void *res = nullptr,
-              int64_t ldr = 0);
+              int64_t ldr = 0, unsigned *tk = nullptr);
 
 }  // namespace gsw

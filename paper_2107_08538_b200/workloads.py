@@ -32,7 +32,8 @@ class GsJobRecord(ctypes.Structure):
                 ("admit_ms", c_double),
                 ("end_ms", c_double), ("wait_ms", c_double), ("compute_ms", c_double),
                 ("mem_bytes", c_int64), ("h2d_bytes", c_int64), ("d2h_bytes", c_int64),
-                ("checksum", c_uint64), ("n_kernels", c_int32), ("pad", c_int32)]
+                ("checksum", c_uint64), ("n_kernels", c_int32), ("pad", c_int32),
+                ("setup_ms", c_double), ("gen_ms", c_double), ("tail_ms", c_double)]
 
 
 class GsExecStats(ctypes.Structure):
@@ -195,6 +196,7 @@ def run_jobs(jobs: list[Job], policy: str = "mgb-warps", devices: list[int] = (0
                      "admit_ms": r.admit_ms, "end_ms": r.end_ms, "turnaround_ms": r.end_ms - r.arrival_ms,
                      "wait_ms": r.wait_ms, "compute_ms": r.compute_ms,
                      "mem_bytes": r.mem_bytes, "h2d_bytes": r.h2d_bytes, "d2h_bytes": r.d2h_bytes,
-                     "checksum": r.checksum, "n_kernels": r.n_kernels})
+                     "checksum": r.checksum, "n_kernels": r.n_kernels,
+                     "setup_ms": r.setup_ms, "gen_ms": r.gen_ms, "tail_ms": r.tail_ms})
     return ExecResult(rows, st.makespan_ms, st.completed, st.crashed, st.oom, st.rejected,
                       st.kernel_launches, st.decision_launches, st.decision_ms)
