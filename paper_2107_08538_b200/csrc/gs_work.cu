@@ -401,7 +401,9 @@ int run_kernels(const gs_job_desc &j, std::vector<void *> &buf, cudaStream_t st,
 
 int digest(const void *p, int64_t bytes, unsigned long long *dsum, cudaStream_t st) {
   CUW(cudaMemsetAsync(dsum, 0, 8, st));
-  checksum_words<<<2 * kSMs, kThreads, 0, st>>>((const uint32_t *)p, bytes / 4, dsum);
+  // dsum[1..] are the job's tile tickets (zero between kernels)
+  checksum_words<<<2 * kSMs, kThreads, 0, st>>>((const uint32_t *)p, bytes / 4, dsum,
+                                                reinterpret_cast<unsigned *>(dsum + 1));
   CUW(cudaGetLastError());
   return GS_OK;
 }
