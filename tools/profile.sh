@@ -18,7 +18,7 @@ cap() {  # name regex skip cmd...
   timeout 300 $NCU -k regex:$rx -s $skip -c 1 -o $OUT/prof_$name -f "$@" > $OUT/prof_$name.log 2>&1 \
     || echo "capture $name failed/timeout" >> $OUT/prof_errors.log
 }
-cap hotspot hotspot_step 5 python tools/debug_job.py hotspot 16384 8
+cap hotspot hotspot_step2 2 python tools/debug_job.py hotspot 16384 8
 cap srad srad_fused 3 python tools/debug_job.py srad 16384 5
 cap kmeans kmeans_assign 2 python tools/debug_job.py kmeans 8000000 4 34
 cap bfs bfs_expand 8 python tools/debug_job.py bfs 48000000
