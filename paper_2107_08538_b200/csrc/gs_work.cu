@@ -121,7 +121,8 @@ int validate(const gs_job_desc &j) {
 int job_grid(const gs_job_desc &j) {
   // srad's fused kernel and kmeans' assignment are issue / latency bound:
   // 3 CTAs per SM (<= 85 registers) hide more latency than 2
-  return (j.kind == GS_JOB_SRAD || j.kind == GS_JOB_KMEANS) ? 3 * kSMs : 2 * kSMs;
+  if (j.kind == GS_JOB_SRAD) return 4 * kSMs;
+  return j.kind == GS_JOB_KMEANS ? 3 * kSMs : 2 * kSMs;
 }
 
 // needle: one warp per 32-row band in flight, at most the job's SM share
