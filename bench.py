@@ -66,6 +66,8 @@ class Clocks:
         self.path = f"/tmp/gs_clocks_{os.getpid()}.csv"
 
     def __enter__(self):
+        if os.environ.get("GS_BENCH_NO_CLOCKS"):  # diagnostics only: the bench line then says "unsampled"
+            return self
         q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
@@ -113,7 +115,8 @@ def run_steps(W, jobs, policy, device, workers, mode, steps, warmup, torch):
         torch.cuda.synchronize()
         times.append(e0.elapsed_time(e1))
         results.append(res)
-        log(f"step {policy} mode={mode}: {times[-1]:.1f} ms, {res.completed} done, {res.oom} oom")
+        log(f"step {policy} mode={mode}: {times[-1]:.1f} ms (executor makespan {res.makespan_ms:.1f}), "
+            f"{res.completed} done, {res.oom} oom")
     return times, results
 
 

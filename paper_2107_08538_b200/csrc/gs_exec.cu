@@ -30,6 +30,7 @@
 
 #include "../../include/gs.h"
 #include "../../include/gs_work.h"
+#include "gs_cache.h"
 #include "gs_work_internal.h"
 
 using namespace gsw;
@@ -372,6 +373,10 @@ int gs_exec_run_arrivals(const gs_job_desc *jobs, int32_t n_jobs, const double *
                          int32_t cg_ratio, const int32_t *cuda_devices, int32_t n_devices, int32_t workers,
                          int32_t mode, int64_t ledger_bytes, gs_job_record *records, gs_exec_stats *stats) {
   if (n_jobs <= 0) return GS_OK;
+  const auto t_call = Clock::now();
+  auto phase = [&](const char *what) {
+    if (g_alloc_log) fprintf(stderr, "[gs exec] %8.1f ms %s\n", ms_since(t_call), what);
+  };
   if (n_devices < 1 || n_devices > GS_MAX_DEVICES) return err(GS_ERR_CONFIG, "1..32 devices");
   if (workers < 1) return err(GS_ERR_CONFIG, "need at least one worker");
   for (int i = 0; i < n_jobs; ++i) {
@@ -385,8 +390,7 @@ int gs_exec_run_arrivals(const gs_job_desc *jobs, int32_t n_jobs, const double *
   if (rc) return err(rc, gs_last_error());
   std::vector<gs_device *> ledgers(n_devices, nullptr);
   for (int d = 0; d < n_devices; ++d) {
-    cudaDeviceProp prop;
-    CUE(cudaGetDeviceProperties(&prop, cuda_devices[d]));
+    const cudaDeviceProp &prop = gscache::device_props(cuda_devices[d]);
     CUE(cudaSetDevice(cuda_devices[d]));
     size_t free_b = 0, total_b = 0;
     CUE(cudaMemGetInfo(&free_b, &total_b));
@@ -479,20 +483,22 @@ int gs_exec_run_arrivals(const gs_job_desc *jobs, int32_t n_jobs, const double *
     // bandwidth-bound kinds at the default.  (A three-class shortest-job-first
     // variant starved the long streaming jobs: cfg 3 turnaround 907 ms vs
     // 106 ms, cfg 1 makespan 324-414 ms vs 285 ms.)
+    // streams and pinned scratch come from process-lifetime caches
+    // (gs_cache.h): creating / freeing them per run stalled whole runs
     std::vector<cudaStream_t> streams(n_devices, nullptr), hi_streams(n_devices, nullptr);
     int prio_lo = 0, prio_hi = 0;
     cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi);
     for (int d = 0; d < n_devices; ++d) {
       cudaSetDevice(cuda_devices[d]);
-      cudaStreamCreateWithFlags(&streams[d], cudaStreamNonBlocking);
-      cudaStreamCreateWithPriority(&hi_streams[d], cudaStreamNonBlocking, prio_hi);
+      gscache::stream_get(&streams[d], 0);
+      gscache::stream_get(&hi_streams[d], prio_hi);
     }
     void *host_out = nullptr;
-    if (out_cap) cudaHostAlloc(&host_out, out_cap, cudaHostAllocPortable);
+    if (out_cap) gscache::host_alloc(&host_out, out_cap);
     int32_t *scalar = nullptr;
     unsigned long long *hsum = nullptr;
-    cudaHostAlloc((void **)&scalar, 16, cudaHostAllocPortable);
-    cudaHostAlloc((void **)&hsum, 16, cudaHostAllocPortable);
+    gscache::host_alloc((void **)&scalar, 16);
+    gscache::host_alloc((void **)&hsum, 16);
     for (;;) {
       const int j = next.fetch_add(1);
       if (j >= n_jobs) break;
@@ -577,21 +583,27 @@ int gs_exec_run_arrivals(const gs_job_desc *jobs, int32_t n_jobs, const double *
       decision_ms += ms_since(a);
       redrive();
     }
-    for (cudaStream_t s : streams) cudaStreamDestroy(s);
-    for (cudaStream_t s : hi_streams) cudaStreamDestroy(s);
-    if (host_out) cudaFreeHost(host_out);
-    cudaFreeHost(scalar);
-    cudaFreeHost(hsum);
-    (void)wid;
+    const auto tw = Clock::now();
+    for (int d = 0; d < n_devices; ++d) {
+      gscache::stream_put(streams[d], cuda_devices[d], 0);
+      gscache::stream_put(hi_streams[d], cuda_devices[d], prio_hi);
+    }
+    if (host_out) gscache::host_free(host_out, out_cap);
+    gscache::host_free(scalar, 16);
+    gscache::host_free(hsum, 16);
+    if (g_alloc_log) fprintf(stderr, "[gs exec] worker %d teardown %.1f ms (at %.1f)\n", wid, ms_since(tw), ms_since(t_call));
   };
+  phase("setup done");
   std::vector<std::thread> pool;
   for (int w = 0; w < workers; ++w) pool.emplace_back(worker, w);
   for (auto &t : pool) t.join();
+  phase("workers joined");
   gs_sched_ring_stop(sched);  // retire the resident decision kernel before draining the devices
   for (int d = 0; d < n_devices; ++d) {
     cudaSetDevice(cuda_devices[d]);
     cudaDeviceSynchronize();
   }
+  phase("devices drained");
   if (stats) {
     memset(stats, 0, sizeof(*stats));
     for (int i = 0; i < n_jobs; ++i) {
@@ -607,8 +619,11 @@ int gs_exec_run_arrivals(const gs_job_desc *jobs, int32_t n_jobs, const double *
   }
   gs_sched_ring_stop(sched);
   gs_sched_destroy(sched);
+  phase("sched destroyed");
   for (gs_device *d : ledgers) gs_device_destroy(d);
+  phase("ledgers destroyed");
   gs_engine_close(eng);
+  phase("engine closed");
   if (first_err) return err(first_err, first_msg);
   return GS_OK;
 }

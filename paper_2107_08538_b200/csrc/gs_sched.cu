@@ -37,9 +37,13 @@
 #include <stdlib.h>
 #include <limits.h>
 #include <chrono>
+#include <map>
 #include <mutex>
 #include <string>
+#include <tuple>
 #include <vector>
+
+#include "gs_cache.h"
 #include <algorithm>
 
 #include "../../include/gs.h"
@@ -1234,6 +1238,86 @@ namespace {
       return set_err(GS_ERR_CUDA, std::string(#call ": ") + cudaGetErrorString(e_)); \
   } while (0)
 
+}  // namespace (reopened below)
+
+namespace gscache {
+namespace {
+std::mutex g_mu;
+std::multimap<std::pair<int, size_t>, void *> g_host, g_dev;
+std::multimap<std::pair<int, int>, cudaStream_t> g_streams;
+}  // namespace
+
+cudaError_t host_alloc(void **p, size_t bytes) {
+  {
+    std::lock_guard<std::mutex> g(g_mu);
+    auto it = g_host.find({0, bytes});
+    if (it != g_host.end()) {
+      *p = it->second;
+      g_host.erase(it);
+      return cudaSuccess;
+    }
+  }
+  return cudaHostAlloc(p, bytes, cudaHostAllocMapped | cudaHostAllocPortable);
+}
+void host_free(void *p, size_t bytes) {
+  if (!p) return;
+  std::lock_guard<std::mutex> g(g_mu);
+  g_host.insert({{0, bytes}, p});
+}
+cudaError_t dev_alloc(void **p, size_t bytes) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  {
+    std::lock_guard<std::mutex> g(g_mu);
+    auto it = g_dev.find({dev, bytes});
+    if (it != g_dev.end()) {
+      *p = it->second;
+      g_dev.erase(it);
+      return cudaSuccess;
+    }
+  }
+  return cudaMalloc(p, bytes);
+}
+void dev_free(void *p, size_t bytes, int device) {
+  if (!p) return;
+  std::lock_guard<std::mutex> g(g_mu);
+  g_dev.insert({{device, bytes}, p});
+}
+cudaError_t stream_get(cudaStream_t *s, int prio) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  {
+    std::lock_guard<std::mutex> g(g_mu);
+    auto it = g_streams.find({dev, prio});
+    if (it != g_streams.end()) {
+      *s = it->second;
+      g_streams.erase(it);
+      return cudaSuccess;
+    }
+  }
+  return cudaStreamCreateWithPriority(s, cudaStreamNonBlocking, prio);
+}
+void stream_put(cudaStream_t s, int device, int prio) {
+  if (!s) return;
+  std::lock_guard<std::mutex> g(g_mu);
+  g_streams.insert({{device, prio}, s});
+}
+const cudaDeviceProp &device_props(int device) {
+  static std::map<int, cudaDeviceProp> props;
+  std::lock_guard<std::mutex> g(g_mu);
+  auto it = props.find(device);
+  if (it == props.end()) {
+    cudaDeviceProp p;
+    memset(&p, 0, sizeof p);
+    cudaGetDeviceProperties(&p, device);
+    it = props.emplace(device, p).first;
+  }
+  return it->second;
+}
+}  // namespace gscache
+
+namespace {
+
 template <class T>
 struct Mapped {
   T *h = nullptr;
@@ -1242,14 +1326,14 @@ struct Mapped {
   int alloc(size_t count) {
     release();
     if (count == 0) count = 1;
-    CU(cudaHostAlloc((void **)&h, count * sizeof(T), cudaHostAllocMapped | cudaHostAllocPortable));
+    CU(gscache::host_alloc((void **)&h, count * sizeof(T)));
     memset(h, 0, count * sizeof(T));
     CU(cudaHostGetDevicePointer((void **)&d, h, 0));
     n = count;
     return GS_OK;
   }
   void release() {
-    if (h) cudaFreeHost(h);
+    if (h) gscache::host_free(h, n * sizeof(T));
     h = d = nullptr;
     n = 0;
   }
@@ -1259,21 +1343,25 @@ template <class T>
 struct DevBuf {
   T *d = nullptr;
   size_t n = 0;
+  int dev = 0;
   int ensure(size_t count, cudaStream_t st, bool keep) {
     if (count <= n) return GS_OK;
     size_t nn = std::max(count, n * 2);
     T *nd = nullptr;
-    CU(cudaMalloc((void **)&nd, nn * sizeof(T)));
+    int cur = 0;
+    cudaGetDevice(&cur);
+    CU(gscache::dev_alloc((void **)&nd, nn * sizeof(T)));
     CU(cudaMemsetAsync(nd, 0, nn * sizeof(T), st));
     if (keep && d && n) CU(cudaMemcpyAsync(nd, d, n * sizeof(T), cudaMemcpyDeviceToDevice, st));
     CU(cudaStreamSynchronize(st));
-    if (d) cudaFree(d);
+    release();
     d = nd;
     n = nn;
+    dev = cur;
     return GS_OK;
   }
   void release() {
-    if (d) cudaFree(d);
+    if (d) gscache::dev_free(d, n * sizeof(T), dev);
     d = nullptr;
     n = 0;
   }
@@ -1284,6 +1372,7 @@ struct DevBuf {
 struct gs_engine {
   int cuda_dev = 0;
   cudaStream_t stream = nullptr;
+  int stream_prio = 0;
   std::recursive_mutex mu;
   int32_t res_cap = 0;
   std::vector<gs_device *> devices;
@@ -1541,13 +1630,16 @@ int ensure_jobs(gs_sched *s, int32_t job) {
   if (s->ring_active) return set_err(GS_ERR_NOMEM, "job capacity reserved at ring start exceeded");
   size_t nn = std::max<size_t>((size_t)job + 1, old * 2);
   int32_t *nd = nullptr;
-  CU(cudaMalloc((void **)&nd, nn * sizeof(int32_t)));
+  int cur = 0;
+  cudaGetDevice(&cur);
+  CU(gscache::dev_alloc((void **)&nd, nn * sizeof(int32_t)));
   CU(cudaMemsetAsync(nd, 0xff, nn * sizeof(int32_t), s->eng->stream));  // -1
   if (old) CU(cudaMemcpyAsync(nd, s->claims.d, old * sizeof(int32_t), cudaMemcpyDeviceToDevice, s->eng->stream));
   CU(cudaStreamSynchronize(s->eng->stream));
-  if (s->claims.d) cudaFree(s->claims.d);
+  s->claims.release();
   s->claims.d = nd;
   s->claims.n = nn;
+  s->claims.dev = cur;
   return GS_OK;
 }
 
@@ -1574,8 +1666,7 @@ int gs_engine_open(int cuda_device, gs_engine **out) {
     return set_err(GS_ERR_CUDA, "no CUDA device visible: libgs has no CPU fallback");
   if (cuda_device < 0 || cuda_device >= count) return set_err(GS_ERR_CONFIG, "bad CUDA device index");
   CU(cudaSetDevice(cuda_device));
-  cudaDeviceProp prop;
-  CU(cudaGetDeviceProperties(&prop, cuda_device));
+  const cudaDeviceProp &prop = gscache::device_props(cuda_device);
   if (prop.major < 10) return set_err(GS_ERR_CUDA, "libgs is built for sm_100a (B200)");
   auto *eng = new gs_engine();
   eng->cuda_dev = cuda_device;
@@ -1585,7 +1676,8 @@ int gs_engine_open(int cuda_device, gs_engine **out) {
     // decisions preempt workload blocks at the block scheduler
     int lo = 0, hi = 0;
     CU(cudaDeviceGetStreamPriorityRange(&lo, &hi));
-    CU(cudaStreamCreateWithPriority(&eng->stream, cudaStreamNonBlocking, hi));
+    CU(gscache::stream_get(&eng->stream, hi));
+    eng->stream_prio = hi;
   }
   int rc = eng->cmds.alloc(64);
   if (!rc) rc = eng->results.alloc(64);
@@ -1609,7 +1701,7 @@ void gs_engine_close(gs_engine *eng) {
   eng->plan_io.release();
   eng->dummy_state.release();
   eng->dcmds.release();
-  cudaStreamDestroy(eng->stream);
+  gscache::stream_put(eng->stream, eng->cuda_dev, eng->stream_prio);
   delete eng;
 }
 

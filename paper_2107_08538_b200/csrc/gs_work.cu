@@ -13,6 +13,7 @@
 #include <string.h>
 
 #include <algorithm>
+#include <map>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -177,8 +178,20 @@ extern "C" int gs_job_probe(const gs_job_desc *job, gs_probe *out) {
   // maxima over the job's kernels (task_builder.py:272-289)
   int64_t best = -1;
   for (const Shape &s : job_launches(*job)) {
+    // a kernel's attributes never change: query the driver once per kernel
+    static std::mutex mu;
+    static std::map<const void *, cudaFuncAttributes> cache;
     cudaFuncAttributes a;
-    if (cudaFuncGetAttributes(&a, s.fn) != cudaSuccess) return err(GS_ERR_CUDA, "cudaFuncGetAttributes failed");
+    {
+      std::lock_guard<std::mutex> g(mu);
+      auto it = cache.find(s.fn);
+      if (it == cache.end()) {
+        if (cudaFuncGetAttributes(&a, s.fn) != cudaSuccess) return err(GS_ERR_CUDA, "cudaFuncGetAttributes failed");
+        cache.emplace(s.fn, a);
+      } else {
+        a = it->second;
+      }
+    }
     const int wpb = (s.block + 31) / 32;
     if ((int64_t)s.grid * wpb > best) {
       best = (int64_t)s.grid * wpb;
