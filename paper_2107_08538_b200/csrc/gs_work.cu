@@ -40,7 +40,7 @@ int err(int code, const std::string &m) {
     if (e_ != cudaSuccess) return err(GS_ERR_CUDA, std::string(#call ": ") + cudaGetErrorString(e_)); \
   } while (0)
 
-constexpr int kBfsBatch = 4;                // bfs levels launched per host round trip
+constexpr int kBfsBatch = 8;                // bfs levels launched per host round trip
 constexpr int64_t kGranule = 2 << 20;       // device-pool allocation granule
 constexpr int64_t kHeap = 8 << 20;          // per-task heap (task_builder.py:29)
 constexpr int kThreads = 256;
@@ -280,13 +280,14 @@ int run_kernels(const gs_job_desc &j, std::vector<void *> &buf, cudaStream_t st,
       CUW(cudaMemsetAsync(level, 0, 4, st));
       for (uint32_t *bm : {F, V, S}) CUW(cudaMemsetAsync(bm, 1, 1, st));  // source vertex 0 (bitmaps zeroed)
       // kBfsBatch levels per host round trip (Rodinia checks after every
-      // level): levels past the last one find an empty frontier and do no
-      // work, so a batch may overrun the depth harmlessly
+      // level): a level whose predecessor found nothing returns at once, so
+      // a batch overruns the depth for the price of empty launches
       for (int32_t depth = 0;; depth += kBfsBatch) {
         CUW(cudaMemsetAsync(cnt, 0, 8 * kBfsBatch, st));
         for (int q = 0; q < kBfsBatch; ++q) {
-          bfs_expand<<<g, kThreads, 0, st>>>(row, col, F, V, nwords, tk);
-          bfs_commit<<<g, kThreads, 0, st>>>(V, S, F, level, n, nwords, depth + q + 1, cnt + q, tk);
+          const unsigned long long *prev = q ? cnt + q - 1 : nullptr;
+          bfs_expand<<<g, kThreads, 0, st>>>(row, col, F, V, nwords, prev, tk);
+          bfs_commit<<<g, kThreads, 0, st>>>(V, S, F, level, n, nwords, depth + q + 1, prev, cnt + q, tk);
         }
         launches += 2 * kBfsBatch;
         CUW(cudaMemcpyAsync(host_scalar, cnt + kBfsBatch - 1, 8, cudaMemcpyDeviceToHost, st));
