@@ -426,7 +426,11 @@ int gs_exec_run_arrivals(const gs_job_desc *jobs, int32_t n_jobs, const double *
     std::partial_sort(foot.begin(), foot.begin() + k, foot.end(), std::greater<int64_t>());
     int64_t need = 0;
     for (size_t i = 0; i < k; ++i) need += foot[i];
-    prepare_pool(cuda_devices[d], std::min(need, spec.mem_bytes));
+    // ... unless that is most of the device: one chunk that large fragments
+    // under jobs of 7-42 GB (cfg 2) and, with no physical memory left to
+    // grow into, an allocation that does not fit a hole stalls; such runs
+    // let the pool grow and trim per allocation instead
+    if (need <= spec.mem_bytes / 2) prepare_pool(cuda_devices[d], need);
   }
   gs_sched *sched = nullptr;
   rc = gs_sched_create(eng, ledgers.data(), n_devices, policy, cg_ratio, 1, &sched);

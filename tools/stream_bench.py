@@ -83,6 +83,11 @@ def cfg2(args):
         line = {"config": "cfg2 darknet yolov3-tiny + resnet-50 mix", "policy": policy, "jobs": len(jobs),
                 "sum_footprint_gib": round(foot / GIB, 1), **summarize(res)}
         print(json.dumps(line), flush=True)
+        if args.dump:
+            with open(args.dump, "a") as f:
+                f.write(json.dumps({"policy": policy, "summary": line,
+                                    "jobs": [{"kind": j.kind, "n": j.n, "m": j.m, **r}
+                                             for j, r in zip(jobs, res.records)]}) + "\n")
 
 
 def cfg3(args):
