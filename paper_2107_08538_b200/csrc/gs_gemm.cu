@@ -320,6 +320,24 @@ static int make_tmap(CUtensorMap *m, const void *ptr, int64_t rows, int64_t k, i
   return GS_OK;
 }
 
+// Row-major fp32 matrix [rows x cols] (row pitch cols), box [box_rows x
+// box_cols], no swizzle; out-of-bounds elements read as zero.
+int make_tmap_f32(CUtensorMap *m, const void *ptr, int64_t rows, int64_t cols, int box_cols, int box_rows) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return err(GS_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  if ((cols * 4) % 16 || (reinterpret_cast<uintptr_t>(ptr) & 15))
+    return err(GS_ERR_CONFIG, "fp32 tensor map needs 16-byte aligned rows");
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)(cols * 4)};
+  cuuint32_t box[2] = {(cuuint32_t)box_cols, (cuuint32_t)box_rows};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void *>(ptr), dims, strides, box, es,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return err(GS_ERR_CUDA, "cuTensorMapEncodeTiled (f32) failed (" + std::to_string((int)r) + ")");
+  return GS_OK;
+}
+
 template <int BN>
 static int launch_bn(const CUtensorMap &ta, const CUtensorMap &tb, GemmArgs g, int max_ctas, cudaStream_t st) {
   // the attribute is per device (the executor may drive several); set it on

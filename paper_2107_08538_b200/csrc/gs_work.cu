@@ -305,11 +305,20 @@ int run_kernels(const gs_job_desc &j, std::vector<void *> &buf, cudaStream_t st,
       // an odd step count ends with one single-step pass.  (A register-only
       // two-step variant was FP32-issue bound: 2.5 updates per output.)
       CUW(cudaFuncSetAttribute(hotspot_step2, cudaFuncAttributeMaxDynamicSharedMemorySize, kHs2Smem));
+      // TMA descriptors of the two temperature buffers and the power map
+      // (tile boxes of 136 columns x 36 / 34 rows)
+      CUtensorMap mt, mt2, mp;
+      int rc = make_tmap_f32(&mt, t, n, n, kHs2W, kHs2TR);
+      if (!rc) rc = make_tmap_f32(&mt2, t2, n, n, kHs2W, kHs2TR);
+      if (!rc) rc = make_tmap_f32(&mp, p, n, n, kHs2W, kHs2UR);
+      if (rc) return rc;
+      const CUtensorMap *min = &mt, *min2 = &mt2;
       int it = 0;
       for (; it + 1 < j.iters; it += 2) {
-        hotspot_step2<<<g, 256, kHs2Smem, st>>>(t, p, t2, (int)n, cc, rx1, ry1, rz1, tk);
+        hotspot_step2<<<g, 256, kHs2Smem, st>>>(*min, mp, t2, (int)n, cc, rx1, ry1, rz1, tk);
         ++launches;
         std::swap(t, t2);
+        std::swap(min, min2);
       }
       if (it < j.iters) {
         hotspot_step<<<g, dim3(32, 8), 0, st>>>(t, p, t2, (int)n, cc, rx1, ry1, rz1, tk);

@@ -2,6 +2,7 @@
 // (gs_work.cu), the tcgen05 GEMM layers (gs_gemm.cu) and the executor
 // (gs_exec.cu).  Not part of the C-ABI.
 #pragma once
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -50,6 +51,7 @@ int gemm_generate(const gs_job_desc &j, const std::vector<void *> &dst, cudaStre
 int gemm_run(const gs_job_desc &j, std::vector<void *> &buf, cudaStream_t st, int *out_idx, int64_t *launches,
              unsigned *tk);
 int gemm_pick_bn(int m, int n);
+int make_tmap_f32(CUtensorMap *m, const void *ptr, int64_t rows, int64_t cols, int box_cols, int box_rows);
 size_t gemm_smem_for(int bn);
 int gemm_block_threads();
 const void *gemm_kernel_fn(int bn);
