@@ -151,7 +151,11 @@ std::vector<Shape> job_launches(const gs_job_desc &j) {
       return {{(const void *)bp_forward, g, kThreads}, {(const void *)bp_output, 1, 32},
               {(const void *)bp_adjust, g, kThreads}};
     case GS_JOB_NEEDLE:
-      return {{(const void *)needle_bands, needle_grid(j), 32}};
+    {
+      Shape s{(const void *)needle_bands, needle_grid(j), 32};
+      s.dsmem = kNwSmem;
+      return {s};
+    }
     case GS_JOB_LUD:
       return {{(const void *)lud_panel, (int)(j.n / BS), 2 * BS},
               {(const void *)lud_internal, g, 256, kLudSmem2}};
@@ -376,7 +380,8 @@ int run_kernels(const gs_job_desc &j, std::vector<void *> &buf, cudaStream_t st,
       break;
     }
     case GS_JOB_NEEDLE: {
-      needle_bands<<<needle_grid(j), 32, 0, st>>>((int32_t *)buf[1], (const int32_t *)buf[0], (int)n, tk,
+      CUW(cudaFuncSetAttribute(needle_bands, cudaFuncAttributeMaxDynamicSharedMemorySize, kNwSmem));
+      needle_bands<<<needle_grid(j), 32, kNwSmem, st>>>((int32_t *)buf[1], (const int32_t *)buf[0], (int)n, tk,
                                                         (unsigned long long *)buf[2]);
       ++launches;
       *out_idx = 1;
