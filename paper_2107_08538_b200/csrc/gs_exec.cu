@@ -328,6 +328,22 @@ static void prepare_pool(int device, int64_t need) {
   cudaSetDevice(prev);
 }
 
+int gs_exec_ledger_capacity(int32_t cuda_device, int64_t *bytes) {
+  CUE(cudaSetDevice(cuda_device));
+  size_t free_b = 0, total_b = 0;
+  CUE(cudaMemGetInfo(&free_b, &total_b));
+  // memory an earlier run left mapped in the pool is free for this run's
+  // jobs: cudaMemGetInfo counts it as used
+  cudaMemPool_t pool;
+  CUE(cudaDeviceGetDefaultMemPool(&pool, cuda_device));
+  uint64_t reserved = 0, used = 0;
+  CUE(cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &reserved));
+  CUE(cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &used));
+  if (reserved > used) free_b += (size_t)(reserved - used);
+  *bytes = (int64_t)free_b - (int64_t)(6ll << 30);  // 6 GiB reserve (context, other allocators)
+  return GS_OK;
+}
+
 int gs_job_run_solo(const gs_job_desc *job, int cuda_device, int mode, void *host_out, int64_t host_out_bytes,
                     gs_job_record *rec) {
   int rc = validate(*job);
@@ -388,32 +404,34 @@ int gs_exec_run_arrivals(const gs_job_desc *jobs, int32_t n_jobs, const double *
   gs_engine *eng = nullptr;
   int rc = gs_engine_open(cuda_devices[0], &eng);
   if (rc) return err(rc, gs_last_error());
+  phase("engine open");
   std::vector<gs_device *> ledgers(n_devices, nullptr);
   for (int d = 0; d < n_devices; ++d) {
     const cudaDeviceProp &prop = gscache::device_props(cuda_devices[d]);
     CUE(cudaSetDevice(cuda_devices[d]));
-    size_t free_b = 0, total_b = 0;
-    CUE(cudaMemGetInfo(&free_b, &total_b));
     // keep the pool's memory (no trimming between jobs)
     cudaMemPool_t pool;
     CUE(cudaDeviceGetDefaultMemPool(&pool, cuda_devices[d]));
     uint64_t thr = UINT64_MAX;
     CUE(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
-    // memory an earlier run left mapped in the pool is free for this run's
-    // jobs: cudaMemGetInfo counts it as used
-    uint64_t reserved = 0, used = 0;
-    CUE(cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &reserved));
-    CUE(cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &used));
-    if (reserved > used) free_b += (size_t)(reserved - used);
     gs_spec spec;
     spec.sm_count = prop.multiProcessorCount;
-    spec.mem_bytes = ledger_bytes > 0 ? ledger_bytes : (int64_t)free_b - (int64_t)(6ll << 30);
+    if (ledger_bytes > 0) {
+      spec.mem_bytes = ledger_bytes;
+    } else {  // (cudaMemGetInfo takes 5-40 ms now and then: callers that run
+              // many steps pass gs_exec_ledger_capacity's value instead)
+      int64_t cap = 0;
+      rc = gs_exec_ledger_capacity(cuda_devices[d], &cap);
+      if (rc) return rc;
+      spec.mem_bytes = cap;
+    }
     spec.max_warps_per_sm = prop.maxThreadsPerMultiProcessor / 32;
     spec.max_tbs_per_sm = prop.maxBlocksPerMultiProcessor;
     spec.regs_per_sm = prop.regsPerMultiprocessor;
     spec.smem_per_sm_bytes = (int64_t)prop.sharedMemPerMultiprocessor;
     rc = gs_device_create(eng, &spec, d, &ledgers[d]);
     if (rc) return err(rc, gs_last_error());
+    phase("ledger created");
     // at most `workers` jobs hold memory at once: the pool needs the sum of
     // the largest `workers` footprints, capped by the ledger
     std::vector<int64_t> foot;
@@ -433,8 +451,10 @@ int gs_exec_run_arrivals(const gs_job_desc *jobs, int32_t n_jobs, const double *
     if (need <= spec.mem_bytes / 2) prepare_pool(cuda_devices[d], need);
   }
   gs_sched *sched = nullptr;
+  phase("pool ready");
   rc = gs_sched_create(eng, ledgers.data(), n_devices, policy, cg_ratio, 1, &sched);
   if (rc) return err(rc, gs_last_error());
+  phase("sched created");
   rc = gs_engine_reserve_handles(eng, n_jobs + 1);
   if (rc) return err(rc, gs_last_error());
   // Placement calls: one decision launch per call by default.  GS_RING=1

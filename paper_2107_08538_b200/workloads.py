@@ -52,6 +52,7 @@ WORK_SIGNATURES = {
     "gs_exec_run_arrivals": (c_int32, [c_void_p, c_int32, c_void_p, c_int32, c_int32, POINTER(c_int32), c_int32,
                                        c_int32, c_int32, c_int64, c_void_p, POINTER(GsExecStats)]),
     "gs_exec_stage": (c_int32, [c_void_p, c_int32, POINTER(c_int32), c_int32, c_int32]),
+    "gs_exec_ledger_capacity": (c_int32, [c_int32, POINTER(c_int64)]),
     "gs_exec_unstage": (None, []),
     "gs_gemm_bf16": (c_int32, [c_void_p, c_int64, c_void_p, c_int64, c_void_p, c_void_p, c_int64, c_int32,
                                c_int32, c_int32, c_int32, c_int32, c_void_p]),
@@ -173,6 +174,15 @@ class ExecResult:
     kernel_launches: int
     decision_launches: int
     decision_ms: float
+
+
+def ledger_capacity(device: int = 0) -> int:
+    """Bytes a run's ledger gets on `device` by default (free HBM + pool-held
+    unused memory - 6 GiB); query once and pass as run_jobs(ledger_bytes=)
+    when timing many runs."""
+    cap = c_int64(0)
+    nat.check(lib().gs_exec_ledger_capacity(device, ctypes.byref(cap)))
+    return cap.value
 
 
 def run_jobs(jobs: list[Job], policy: str = "mgb-warps", devices: list[int] = (0,), workers: int = 8,
