@@ -148,7 +148,7 @@ std::vector<Shape> job_launches(const gs_job_desc &j) {
     case GS_JOB_KMEANS:
       return {{(const void *)kmeans_assign_fn((int)j.m), g, kThreads}, {(const void *)kmeans_recenter, 1, kThreads}};
     case GS_JOB_BACKPROP:
-      return {{(const void *)bp_forward, g, kThreads}, {(const void *)bp_output, 1, 32},
+      return {{(const void *)bp_forward, g, kThreads}, {(const void *)bp_output, 1, 32 * kMaxHid},
               {(const void *)bp_adjust, g, kThreads}};
     case GS_JOB_NEEDLE:
     {
@@ -373,7 +373,7 @@ int run_kernels(const gs_job_desc &j, std::vector<void *> &buf, cudaStream_t st,
       for (int it = 0; it < j.iters; ++it) {
         const int ntiles = (int)((n + 1 + kBpTile - 1) / kBpTile);
         bp_forward<<<g, kThreads, 0, st>>>(x, w1, n + 1, nh, partial, tk);
-        bp_output<<<1, 32, 0, st>>>(partial, ntiles, nh, state);
+        bp_output<<<1, 32 * kMaxHid, 0, st>>>(partial, ntiles, nh, state);
         bp_adjust<<<g, kThreads, 0, st>>>(x, w1, ow1, n + 1, nh, state, tk);
         launches += 3;
       }
