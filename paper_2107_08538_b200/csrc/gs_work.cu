@@ -158,7 +158,7 @@ std::vector<Shape> job_launches(const gs_job_desc &j) {
     }
     case GS_JOB_LUD:
       return {{(const void *)lud_panel, (int)(j.n / BS), 2 * BS},
-              {(const void *)lud_panel_next, (int)(j.n / BS), 2 * BS},
+              {(const void *)lud_panel_next, (int)(j.n / BS), 32 * kLudNextWarps},
               {(const void *)lud_internal, g, 256, kLudSmem2}};
     case GS_JOB_YOLO:
     case GS_JOB_RESNET:
@@ -411,7 +411,7 @@ int run_kernels(const gs_job_desc &j, std::vector<void *> &buf, cudaStream_t st,
         if (o + BS >= N) break;
         // step o on block row / column o+32, then panel(o+32), in one launch
         const int panels = (N - o - BS) / BS - 1;
-        lud_panel_next<<<panels > 0 ? panels : 1, 2 * BS, 0, st>>>(a, N, o);
+        lud_panel_next<<<panels > 0 ? panels : 1, 32 * kLudNextWarps, 0, st>>>(a, N, o);
         ++launches;
         update(o, o + 2 * BS, N, o + 2 * BS, N, 1);         // the rest: steps o and o+32 in one pass
       }
