@@ -420,7 +420,9 @@ int run_kernels(const gs_job_desc &j, std::vector<void *> &buf, cudaStream_t st,
       // bit-exact but slower, 10.3 vs 8.6 ms at n = 6144: the trailing
       // update's persistent CTAs fill every SM's register file, so the
       // side stream's panels only start when it ends, and the split added
-      // launches.)
+      // launches.  With the trailing update on 1.5 blocks per SM, so panel
+      // blocks fit beside it, it was still 9.4 vs 7.9 ms: the L-shaped band
+      // update it needs first adds two launches per pair to the chain.)
       *out_idx = 0;
       break;
     }
