@@ -32,6 +32,7 @@ CASES = [
     ("needle", dict(n=4096, seed=4), "exact"),    # 128 bands in a wavefront
     ("kmeans", dict(n=100_003, m=8, iters=3, seed=5), "exact"),    # nf < 32, ragged tail
     ("kmeans", dict(n=65_537, m=40, iters=2, seed=6), "exact"),    # generic nf > 32
+    ("kmeans", dict(n=200_004, m=34, iters=3, seed=7), "exact"),   # the catalog's 34 features, partial last tile
     ("lud", dict(n=160, seed=4), 1e-5),           # trailing edge exactly one 128 tile
     ("lud", dict(n=512, seed=3), 1e-5),
     ("lud", dict(n=1056, seed=5), 1e-5),          # partial 128 tiles
