@@ -260,10 +260,41 @@ struct ViewArgs {
 // im2row for a k x k / stride / pad convolution: ws[out pixel][(kh*k + kw)*C
 // + c], zero outside the image and in the pad columns; 16-byte vectors when
 // C % 8 == 0 (all layers but the first).
+// Vector layers work per (output pixel, tap): the pixel's input row segment
+// of C channels is copied as 16-byte chunks (a warp per unit, lane = chunk,
+// when C >= 256; a thread per unit otherwise), and blocks walk output rows
+// so the index arithmetic is 32-bit and per unit (a thread per 16-byte
+// chunk with 64-bit div / mod per chunk was ALU bound: im2row was half of
+// a YOLO / ResNet job).
 __global__ void __launch_bounds__(kThr) im2row(ViewArgs in, __nv_bfloat16 *ws, int k, int stride, int pad, int oh,
                                                int ow, int kdim, int kpad) {
   const int C = in.c;
   const bool vec = (C % 8 == 0) && (in.pitch % 8 == 0);
+  if (vec) {
+    const int taps = k * k, cch = C / 8, tail = (kpad - kdim) / 8;
+    const int rows = in.n * oh, per_row = ow * taps;
+    const uint4 zero = make_uint4(0, 0, 0, 0);
+    const bool warp_units = cch >= 32;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    for (int r = blockIdx.x; r < rows; r += gridDim.x) {
+      const int b = r / oh, oy = r - b * oh;
+      const int u0 = warp_units ? warp : (int)threadIdx.x, us = warp_units ? nw : (int)blockDim.x;
+      for (int u = u0; u < per_row; u += us) {
+        const int ox = u / taps, tap = u - ox * taps;
+        const int ky = tap / k, kx = tap - ky * k;
+        const int iy = oy * stride + ky - pad, ix = ox * stride + kx - pad;
+        uint4 *dst = reinterpret_cast<uint4 *>(ws + ((int64_t)r * ow + ox) * kpad + (int64_t)tap * C);
+        const bool inside = iy >= 0 && iy < in.h && ix >= 0 && ix < in.w;
+        const uint4 *src =
+            reinterpret_cast<const uint4 *>(in.p + (((int64_t)b * in.h + iy) * in.w + ix) * in.pitch);
+        const int q0 = warp_units ? lane : 0, qs = warp_units ? 32 : 1;
+        for (int q = q0; q < cch; q += qs) dst[q] = inside ? src[q] : zero;
+        if (tap == taps - 1)
+          for (int q = q0; q < tail; q += qs) dst[cch + q] = zero;  // pad columns kdim .. kpad
+      }
+    }
+    return;
+  }
   const int64_t pix = (int64_t)in.n * oh * ow;
   const int chunks = kpad / 8;
   const int64_t total = pix * chunks;
@@ -529,8 +560,11 @@ int gemm_run(const gs_job_desc &j, std::vector<void *> &buf, cudaStream_t st, in
         A = in.p;  // 1x1 / stride 1: the activation is already the im2row matrix
         lda = L.in.pitch;
       } else {
-        im2row<<<grid_for(opix * (L.kpad / 8)), kThr, 0, st>>>(in, (__nv_bfloat16 *)buf[B_WS], L.k, L.stride, L.pad,
-                                                               L.out.h, L.out.w, L.kdim, L.kpad);
+        const bool vec_in = L.in.c % 8 == 0 && L.in.pitch % 8 == 0;
+        const int grid = vec_in ? (int)std::min<int64_t>((int64_t)L.in.n * L.out.h, 2 * kSMs)
+                                : grid_for(opix * (L.kpad / 8));
+        im2row<<<grid, kThr, 0, st>>>(in, (__nv_bfloat16 *)buf[B_WS], L.k, L.stride, L.pad, L.out.h, L.out.w,
+                                      L.kdim, L.kpad);
         ++*launches;
         A = buf[B_WS];
         lda = L.kpad;
