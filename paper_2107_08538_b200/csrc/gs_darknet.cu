@@ -402,10 +402,16 @@ __global__ void __launch_bounds__(kThr, 2) conv3x3_direct(ViewArgs in, const __n
   }
   if (threadIdx.x < COUT) sb[threadIdx.x] = bias[threadIdx.x];
   __syncthreads();
-  const int64_t pix = (int64_t)in.n * in.h * in.w;
-  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < pix; p += (int64_t)gridDim.x * blockDim.x) {
-    const int x = (int)(p % in.w), y = (int)((p / in.w) % in.h);
-    const int64_t b = p / ((int64_t)in.w * in.h);
+  // pixel index -> (b, y, x) in 32-bit arithmetic (64-bit div / mod per
+  // pixel cost as much as the 432 FMAs; every Darknet input here has
+  // fewer than 2^31 pixels, gemm_validate's size limits)
+  const unsigned pix = (unsigned)((int64_t)in.n * in.h * in.w);
+  for (unsigned p = blockIdx.x * blockDim.x + threadIdx.x; p < pix; p += gridDim.x * blockDim.x) {
+    const unsigned q = p / (unsigned)in.w;
+    const int x = (int)(p - q * (unsigned)in.w);
+    const unsigned bq = q / (unsigned)in.h;
+    const int y = (int)(q - bq * (unsigned)in.h);
+    const int64_t b = bq;
     float acc[COUT];
 #pragma unroll
     for (int co = 0; co < COUT; ++co) acc[co] = 0.0f;
@@ -444,7 +450,7 @@ __global__ void __launch_bounds__(kThr, 2) conv3x3_direct(ViewArgs in, const __n
         }
       }
     }
-    __nv_bfloat16 *dst = out + p * opitch;
+    __nv_bfloat16 *dst = out + (int64_t)p * opitch;
 #pragma unroll
     for (int q = 0; q < COUT / 8; ++q) {
       __align__(16) __nv_bfloat162 o[4];
@@ -478,6 +484,8 @@ int grid_for(int64_t total) { return (int)std::min<int64_t>((total + kThr - 1) /
 int gemm_validate(const gs_job_desc &j) {
   if (j.n < 32 || j.n % 32) return err(GS_ERR_CONFIG, "network input size must be a positive multiple of 32");
   if (j.m < 1 || j.m > 1024) return err(GS_ERR_CONFIG, "network batch must be 1..1024");
+  if (j.m * j.n * j.n >= (1ll << 31))  // pixel indices (GEMM rows, direct-conv pixels) are 32-bit
+    return err(GS_ERR_CONFIG, "network batch x input pixels must be below 2^31");
   if (j.iters < 1) return err(GS_ERR_CONFIG, "a network job needs at least one forward pass");
   return GS_OK;
 }
