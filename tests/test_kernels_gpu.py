@@ -103,3 +103,30 @@ def test_executor_e2e_mode_moves_bytes():
     for r, j in zip(res.records, MIX[:3]):
         i, _ = W.io_bytes(j)
         assert r["h2d_bytes"] == i and r["d2h_bytes"] > 0
+
+
+def test_executor_colocated_darknet_jobs_match_solo():
+    """YOLO / ResNet jobs co-located with each other and with Rodinia kinds:
+    the GEMM's tiles come from the job's ticket counter, whose order differs
+    run to run, yet every output checksum equals the job's solo run."""
+    jobs = [W.Job("yolo", n=416, m=2, iters=1, seed=11), W.Job("resnet", n=224, m=2, iters=1, seed=12),
+            W.Job("yolo", n=320, m=4, iters=1, seed=13), MIX[1], MIX[3], W.Job("resnet", n=224, m=1, iters=1, seed=14)]
+    solo = [W.run_solo(j)[1].checksum for j in jobs]
+    for policy in ("mgb-warps", "cg:6"):
+        res = W.run_jobs(jobs, policy=policy, workers=6)
+        assert res.completed == len(jobs) and res.oom == 0
+        assert [r["checksum"] for r in res.records] == solo
+
+
+def test_executor_poisson_arrivals():
+    """Jobs arrive over time (cfg 3): none is pulled before it arrives,
+    turnaround is measured from arrival, outputs equal the solo runs."""
+    arrivals = [0.0, 2.0, 4.0, 30.0, 31.0, 60.0, 61.0, 90.0]
+    solo = [W.run_solo(j)[1].checksum for j in MIX]
+    res = W.run_jobs(MIX, policy="mgb-warps", workers=4, arrivals_ms=arrivals)
+    assert res.completed == len(MIX)
+    for r, a, c in zip(res.records, arrivals, solo):
+        assert r["arrival_ms"] == a and r["pull_ms"] >= a - 0.5
+        assert abs(r["turnaround_ms"] - (r["end_ms"] - a)) < 1e-6
+        assert r["checksum"] == c
+    assert res.makespan_ms >= arrivals[-1]
