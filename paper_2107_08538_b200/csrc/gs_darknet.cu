@@ -287,47 +287,51 @@ __global__ void __launch_bounds__(kThr) im2row(ViewArgs in, __nv_bfloat16 *ws, i
         const bool inside = iy >= 0 && iy < in.h && ix >= 0 && ix < in.w;
         const uint4 *src =
             reinterpret_cast<const uint4 *>(in.p + (((int64_t)b * in.h + iy) * in.w + ix) * in.pitch);
-        const int q0 = warp_units ? lane : 0, qs = warp_units ? 32 : 1;
-        for (int q = q0; q < cch; q += qs) dst[q] = inside ? src[q] : zero;
+        if (warp_units) {
+          for (int q = lane; q < cch; q += 32) dst[q] = inside ? src[q] : zero;
+        } else {
+          // all of the segment's loads before its stores (up to 16 chunks in
+          // flight per thread instead of one load-store pair at a time)
+          for (int q0 = 0; q0 < cch; q0 += 16) {
+            uint4 v[16];
+#pragma unroll
+            for (int q = 0; q < 16; ++q) v[q] = (inside && q0 + q < cch) ? src[q0 + q] : zero;
+#pragma unroll
+            for (int q = 0; q < 16; ++q)
+              if (q0 + q < cch) dst[q0 + q] = v[q];
+          }
+        }
         if (tap == taps - 1)
-          for (int q = q0; q < tail; q += qs) dst[cch + q] = zero;  // pad columns kdim .. kpad
+          for (int q = warp_units ? lane : 0; q < tail; q += warp_units ? 32 : 1)
+            dst[cch + q] = zero;  // pad columns kdim .. kpad
       }
     }
     return;
   }
-  const int64_t pix = (int64_t)in.n * oh * ow;
+  // scalar layers (the 3-channel image): blocks walk output rows, threads
+  // take (output column, 8-column chunk) units, 32-bit index arithmetic
   const int chunks = kpad / 8;
-  const int64_t total = pix * chunks;
-  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t p = t / chunks;
-    const int col0 = (int)(t % chunks) * 8;
-    const int ox = (int)(p % ow), oy = (int)((p / ow) % oh), b = (int)(p / ((int64_t)ow * oh));
-    uint4 out;
-    if (vec) {
-      out = make_uint4(0, 0, 0, 0);
-      if (col0 < kdim) {
-        const int tap = col0 / C, c = col0 % C;
-        const int iy = oy * stride + tap / k - pad, ix = ox * stride + tap % k - pad;
-        if (iy >= 0 && iy < in.h && ix >= 0 && ix < in.w)
-          out = *reinterpret_cast<const uint4 *>(in.p + (((int64_t)b * in.h + iy) * in.w + ix) * in.pitch + c);
-      }
-    } else {
+  const int rows = in.n * oh, per_row = ow * chunks;
+  for (int r = blockIdx.x; r < rows; r += gridDim.x) {
+    const int b = r / oh, oy = r - b * oh;
+    for (int u = threadIdx.x; u < per_row; u += blockDim.x) {
+      const int ox = u / chunks, col0 = (u - ox * chunks) * 8;
       __align__(16) __nv_bfloat16 v[8];
 #pragma unroll
       for (int q = 0; q < 8; ++q) {
         const int col = col0 + q;
         float x = 0.0f;
         if (col < kdim) {
-          const int tap = col / C, c = col % C;
-          const int iy = oy * stride + tap / k - pad, ix = ox * stride + tap % k - pad;
+          const int tap = col / C, c = col - tap * C;
+          const int ky = tap / k, kx = tap - ky * k;
+          const int iy = oy * stride + ky - pad, ix = ox * stride + kx - pad;
           if (iy >= 0 && iy < in.h && ix >= 0 && ix < in.w)
             x = __bfloat162float(in.p[(((int64_t)b * in.h + iy) * in.w + ix) * in.pitch + c]);
         }
         v[q] = __float2bfloat16_rn(x);
       }
-      out = *reinterpret_cast<uint4 *>(v);
+      *reinterpret_cast<uint4 *>(ws + ((int64_t)r * ow + ox) * kpad + col0) = *reinterpret_cast<uint4 *>(v);
     }
-    *reinterpret_cast<uint4 *>(ws + p * kpad + col0) = out;
   }
 }
 
@@ -568,9 +572,7 @@ int gemm_run(const gs_job_desc &j, std::vector<void *> &buf, cudaStream_t st, in
         A = in.p;  // 1x1 / stride 1: the activation is already the im2row matrix
         lda = L.in.pitch;
       } else {
-        const bool vec_in = L.in.c % 8 == 0 && L.in.pitch % 8 == 0;
-        const int grid = vec_in ? (int)std::min<int64_t>((int64_t)L.in.n * L.out.h, 2 * kSMs)
-                                : grid_for(opix * (L.kpad / 8));
+        const int grid = (int)std::min<int64_t>((int64_t)L.in.n * L.out.h, 2 * kSMs);  // blocks walk output rows
         im2row<<<grid, kThr, 0, st>>>(in, (__nv_bfloat16 *)buf[B_WS], L.k, L.stride, L.pad, L.out.h, L.out.w,
                                       L.kdim, L.kpad);
         ++*launches;
