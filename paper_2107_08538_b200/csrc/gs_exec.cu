@@ -180,7 +180,17 @@ int run_job(const gs_job_desc &j, const Staged *stg, int mode, cudaStream_t st, 
     *oom = true;
     return GS_OK;
   }
-  cudaEvent_t es, e0, e1, ed;
+  // from here on every return path (errors included) destroys the events
+  // and gives the job's memory back
+  cudaEvent_t es = nullptr, e0 = nullptr, e1 = nullptr, ed = nullptr;
+  struct Cleanup {
+    std::function<void()> f;
+    ~Cleanup() { f(); }
+  } cleanup{[&]() {
+    for (cudaEvent_t ev : {es, e0, e1, ed})
+      if (ev) cudaEventDestroy(ev);
+    release();
+  }};
   CUE(cudaEventCreate(&es));
   CUE(cudaEventCreate(&e0));
   CUE(cudaEventCreate(&e1));
@@ -250,11 +260,6 @@ int run_job(const gs_job_desc &j, const Staged *stg, int mode, cudaStream_t st, 
   CUE(cudaEventElapsedTime(&ms, e1, ed));
   rec.tail_ms = ms;
   rec.checksum = *host_sum;
-  cudaEventDestroy(es);
-  cudaEventDestroy(e0);
-  cudaEventDestroy(e1);
-  cudaEventDestroy(ed);
-  release();
   return GS_OK;
 }
 
