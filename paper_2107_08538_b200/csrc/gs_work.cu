@@ -398,7 +398,7 @@ int run_kernels(const gs_job_desc &j, std::vector<void *> &buf, cudaStream_t st,
       CUW(cudaFuncSetAttribute(lud_internal, cudaFuncAttributeMaxDynamicSharedMemorySize, kLudSmem2));
       auto panel = [&](int o) {
         const int panels = (N - o) / BS - 1;
-        lud_panel<<<panels > 0 ? panels : 1, 2 * BS, 0, st>>>(a, N, o);
+        lud_panel<<<panels > 0 ? panels : 1, 2 * BS, 0, st>>>(a, N, o, tk + 2);
         ++launches;
       };
       auto update = [&](int o, int rb, int re, int cb, int ce, int two) {
@@ -411,7 +411,7 @@ int run_kernels(const gs_job_desc &j, std::vector<void *> &buf, cudaStream_t st,
         if (o + BS >= N) break;
         // step o on block row / column o+32, then panel(o+32), in one launch
         const int panels = (N - o - BS) / BS - 1;
-        lud_panel_next<<<panels > 0 ? panels : 1, 32 * kLudNextWarps, 0, st>>>(a, N, o);
+        lud_panel_next<<<panels > 0 ? panels : 1, 32 * kLudNextWarps, 0, st>>>(a, N, o, tk + 2);
         ++launches;
         update(o, o + 2 * BS, N, o + 2 * BS, N, 1);         // the rest: steps o and o+32 in one pass
       }

@@ -130,3 +130,16 @@ def test_executor_poisson_arrivals():
         assert abs(r["turnaround_ms"] - (r["end_ms"] - a)) < 1e-6
         assert r["checksum"] == c
     assert res.makespan_ms >= arrivals[-1]
+
+
+def test_lud_panels_colocated_are_deterministic():
+    """lud's panel launches read the diagonal block in every CTA and write
+    it back factored; under co-location some CTAs start late, so the write
+    must wait for the last reader (it once came from block 0 and raced)."""
+    jobs = [W.Job("lud", n=1024, seed=21), W.Job("hotspot", n=2048, iters=20, seed=22),
+            W.Job("lud", n=2048, seed=23), W.Job("srad", n=2048, iters=4, seed=24),
+            W.Job("lud", n=1056, seed=25), W.Job("hotspot", n=2048, iters=20, seed=26)]
+    solo = [W.run_solo(j)[1].checksum for j in jobs]
+    for _ in range(4):
+        res = W.run_jobs(jobs, policy="cg:6", workers=6)
+        assert [r["checksum"] for r in res.records] == solo
