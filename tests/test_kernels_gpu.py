@@ -143,3 +143,17 @@ def test_lud_panels_colocated_are_deterministic():
     for _ in range(4):
         res = W.run_jobs(jobs, policy="cg:6", workers=6)
         assert [r["checksum"] for r in res.records] == solo
+
+
+@pytest.mark.parametrize("policy", ["mgb-warps", "sa"])
+def test_executor_places_across_two_ledgers(policy):
+    """Two ledgers (both on this GPU, memory split between them): one
+    decision authority places the mix across devices; every job lands on one
+    of them and reproduces its solo output."""
+    solo = [W.run_solo(j)[1].checksum for j in MIX]
+    cap = W.ledger_capacity(0) // 2
+    res = W.run_jobs(MIX, policy=policy, devices=[0, 0], workers=8, ledger_bytes=cap)
+    assert res.completed == len(MIX) and res.oom == 0
+    assert [r["checksum"] for r in res.records] == solo
+    used = {r["device"] for r in res.records}
+    assert used <= {0, 1} and len(used) == 2
