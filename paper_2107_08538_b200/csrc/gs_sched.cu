@@ -147,7 +147,7 @@ struct KParams {
 
 struct SLed {
   long long free_mem, in_use_warps, version, held_mem, held_warps, grow_epoch;
-  int rr_cursor, dirty;
+  int rr_cursor, dirty;  // dirty: bit 0 header changed, bit 1 per-SM arrays changed
 };
 
 struct Smem {
@@ -316,8 +316,11 @@ __device__ void stage(const KParams &p, int *dyn, const Smem &S, bool in, int la
       if (q < p.stage_q) {
         const int d = dev_of_q(p, q);
         int4 *g = reinterpret_cast<int4 *>(p.dev[d].led) + (q - (p.dev[d].smem_off >> 2));
+        // write-back: the 64 B header when it changed, the per-SM arrays
+        // only when they did (mgb-warps never touches them: a 2.4 KB
+        // write-back over PCIe per command became 64 B)
         if (in) r[k] = *g;
-        else if (S.led[d].dirty) *g = sm4[q];
+        else if ((S.led[d].dirty & 2) || ((S.led[d].dirty & 1) && q - (p.dev[d].smem_off >> 2) < 4)) *g = sm4[q];
       }
     }
     if (in) {
@@ -457,7 +460,7 @@ __device__ void warp_commit_blocks(const KDev &D, int *dyn, SLed &L, int h, cons
   if (lane == 0) {
     L.rr_cursor = cursor;
     L.version += 1;
-    L.dirty = 1;
+    L.dirty |= 3;
     if (neg) L.grow_epoch += 1;
     reinterpret_cast<gs_residency *>(res_row(D, h))->thread_blocks = tot;
   }
@@ -520,7 +523,7 @@ __device__ void apply_release(const KDev &D, int *dyn, Smem &S, int d, const Rel
     L.held_warps -= rr.warps;
     L.version += 1;
     L.grow_epoch += 1;
-    L.dirty = 1;
+    L.dirty |= rr.has_blocks ? 3 : 1;
     if (rr.has_blocks && S.agg_ok[d]) {
       if (rr.wpb >= 0 && rr.rpb >= 0 && rr.spb >= 0) {
         S.agg[d][0] += rr.T;
@@ -776,7 +779,7 @@ __device__ Dec decide(const KParams &p, Smem &S, int *dyn, const gs_probe &pr, u
       L.in_use_warps += sh.tw;
       L.held_warps += sh.tw;
       L.version += 3;
-      L.dirty = 1;
+      L.dirty |= 1;
     }
     __syncwarp();
     if (p.sweep) fifo_push_slot(p, S, dyn, chosen, h, sh, new_mem, new_warps, sm_policy, P, lane);
@@ -981,7 +984,7 @@ __device__ void exec_cmd(const KParams &p, Smem &S, int *dyn, const Cmd &c, gs_d
         } else {
           L.free_mem -= c.a;
           L.version += 1;
-          L.dirty = 1;
+          L.dirty |= 1;
           if (c.a < 0) L.grow_epoch += 1;
           if (c.op == OP_ALLOC_RAW) {
             gs_residency *row = entry(p.dev[c.dev], c.handle);
@@ -1000,7 +1003,7 @@ __device__ void exec_cmd(const KParams &p, Smem &S, int *dyn, const Cmd &c, gs_d
         row->mem_bytes += c.a;
         L.held_mem += c.a;
         L.version += 1;
-        L.dirty = 1;
+        L.dirty |= 1;
         out->outcome = GS_OK;
       }
       break;
@@ -1012,7 +1015,7 @@ __device__ void exec_cmd(const KParams &p, Smem &S, int *dyn, const Cmd &c, gs_d
         L.in_use_warps += c.a;
         L.held_warps += c.a;
         L.version += 1;
-        L.dirty = 1;
+        L.dirty |= 1;
         out->outcome = GS_OK;
       }
       break;
