@@ -78,10 +78,33 @@ typedef struct gs_exec_stats {
     double decision_ms;        /* host wall time spent in placement calls */
 } gs_exec_stats;
 
-/* Probe producer: footprint (buffers rounded to the 2 MiB allocation
- * granule, plus the 8 MiB device heap the reference counts per task,
- * task_builder.py:264-268) and the widest launch shape of the job, with
- * registers and static shared memory taken from cudaFuncGetAttributes. */
+/* ---- probe capture (replaces the reference's trace-level
+ * compute_resource_request, gs/task_builder.py:258-290, for real CUDA host
+ * code: a launch wrapper or interceptor records each kernel launch of a task
+ * and its buffers, and the probe follows the reference's aggregation) ---- */
+typedef struct gs_launch_desc {
+    int32_t thread_blocks;
+    int32_t threads_per_block;
+    int32_t regs_per_thread;
+    int32_t smem_per_block;   /* static + dynamic bytes */
+    double est_duration_ms;
+} gs_launch_desc;
+/* Descriptor of launching `fn` (a __global__ function's host stub, as
+ * cudaLaunchKernel takes it) with grid x block and `dyn_smem` dynamic shared
+ * memory: registers and static shared memory from cudaFuncGetAttributes
+ * (queried once per kernel). */
+int gs_launch_desc_of(const void *fn, int32_t grid, int32_t block, int32_t dyn_smem, gs_launch_desc *out);
+/* compute_resource_request: mem = sum of the task's distinct buffers + the
+ * heap limit, counted once; the widest launch is the FIRST maximum of
+ * tbs * ceil(threads / 32) and gives the shape; regs / smem are maxima over
+ * all launches; the duration estimate is the sum.  Pure host arithmetic (no
+ * GPU needed).  GS_ERR_CONFIG for no launches or a byte overflow. */
+int gs_request_from_launches(const gs_launch_desc *launches, int32_t n, const int64_t *buffer_bytes, int32_t nbuf,
+                             int64_t heap_limit_bytes, gs_probe *out);
+/* Probe of a catalog job: its kernels' real launch shapes through
+ * gs_launch_desc_of, its buffers rounded to the executor's 2 MiB allocation
+ * granule, plus the 8 MiB device heap the reference counts per task
+ * (task_builder.py:264-268). */
 int gs_job_probe(const gs_job_desc *job, gs_probe *out);
 /* Bytes of the job's host inputs / outputs (for the e2e accounting). */
 int gs_job_io_bytes(const gs_job_desc *job, int64_t *in_bytes, int64_t *out_bytes);

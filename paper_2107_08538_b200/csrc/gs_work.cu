@@ -13,6 +13,7 @@
 #include <string.h>
 
 #include <algorithm>
+#include <climits>
 #include <map>
 #include <mutex>
 #include <string>
@@ -171,47 +172,84 @@ std::vector<Shape> job_launches(const gs_job_desc &j) {
 
 using namespace gsw;
 
-extern "C" int gs_job_probe(const gs_job_desc *job, gs_probe *out) {
-  int rc = validate(*job);
-  if (rc) return rc;
+// ---- probe capture: launch descriptors -> 64 B probe ----
+
+extern "C" int gs_launch_desc_of(const void *fn, int32_t grid, int32_t block, int32_t dyn_smem,
+                                 gs_launch_desc *out) {
+  if (!fn || !out) return err(GS_ERR_CONFIG, "gs_launch_desc_of: null argument");
+  // a kernel's attributes never change: query the driver once per kernel
+  static std::mutex mu;
+  static std::map<const void *, cudaFuncAttributes> cache;
+  cudaFuncAttributes a;
+  {
+    std::lock_guard<std::mutex> g(mu);
+    auto it = cache.find(fn);
+    if (it == cache.end()) {
+      if (cudaFuncGetAttributes(&a, fn) != cudaSuccess) return err(GS_ERR_CUDA, "cudaFuncGetAttributes failed");
+      cache.emplace(fn, a);
+    } else {
+      a = it->second;
+    }
+  }
+  out->thread_blocks = grid;
+  out->threads_per_block = block;
+  out->regs_per_thread = a.numRegs;
+  out->smem_per_block = (int32_t)a.sharedSizeBytes + dyn_smem;
+  out->est_duration_ms = 0.0;
+  return GS_OK;
+}
+
+extern "C" int gs_request_from_launches(const gs_launch_desc *launches, int32_t n, const int64_t *buffer_bytes,
+                                        int32_t nbuf, int64_t heap_limit_bytes, gs_probe *out) {
+  if (!out || n < 1 || !launches) return err(GS_ERR_CONFIG, "a task needs at least one launch");
+  if (nbuf < 0 || (nbuf > 0 && !buffer_bytes)) return err(GS_ERR_CONFIG, "bad buffer list");
   memset(out, 0, sizeof(*out));
-  int64_t mem = kHeap;
-  for (const Buf &b : job_buffers(*job)) mem += round_granule(b.bytes);
+  // mem = distinct buffers + the device heap, counted once per task
+  int64_t mem = heap_limit_bytes;
+  for (int i = 0; i < nbuf; ++i) {
+    if (buffer_bytes[i] < 0 || mem > INT64_MAX - buffer_bytes[i])
+      return err(GS_ERR_CONFIG, "task memory request overflows the byte limit");
+    mem += buffer_bytes[i];
+  }
   out->mem_bytes = mem;
-  out->heap_limit_bytes = kHeap;
-  // widest launch = first max of tbs * ceil(threads / 32); regs and smem are
-  // maxima over the job's kernels (task_builder.py:272-289)
+  out->heap_limit_bytes = heap_limit_bytes;
+  // widest launch = FIRST max of tbs * ceil(threads / 32); regs and smem are
+  // maxima over the launches; the duration estimate is their sum
   int64_t best = -1;
-  for (const Shape &s : job_launches(*job)) {
-    // a kernel's attributes never change: query the driver once per kernel
-    static std::mutex mu;
-    static std::map<const void *, cudaFuncAttributes> cache;
-    cudaFuncAttributes a;
-    {
-      std::lock_guard<std::mutex> g(mu);
-      auto it = cache.find(s.fn);
-      if (it == cache.end()) {
-        if (cudaFuncGetAttributes(&a, s.fn) != cudaSuccess) return err(GS_ERR_CUDA, "cudaFuncGetAttributes failed");
-        cache.emplace(s.fn, a);
-      } else {
-        a = it->second;
-      }
-    }
-    const int wpb = (s.block + 31) / 32;
-    if ((int64_t)s.grid * wpb > best) {
-      best = (int64_t)s.grid * wpb;
-      out->thread_blocks = s.grid;
+  for (int i = 0; i < n; ++i) {
+    const gs_launch_desc &l = launches[i];
+    const int wpb = (l.threads_per_block + 31) / 32;
+    if ((int64_t)l.thread_blocks * wpb > best) {
+      best = (int64_t)l.thread_blocks * wpb;
+      out->thread_blocks = l.thread_blocks;
       out->warps_per_block = wpb;
-      out->threads_per_block = s.block;
+      out->threads_per_block = l.threads_per_block;
     }
-    out->regs_per_thread = std::max(out->regs_per_thread, a.numRegs);
-    out->smem_per_block = std::max<int32_t>(out->smem_per_block, (int32_t)a.sharedSizeBytes + s.dsmem);
+    out->regs_per_thread = std::max(out->regs_per_thread, l.regs_per_thread);
+    out->smem_per_block = std::max(out->smem_per_block, l.smem_per_block);
+    out->est_duration_ms += l.est_duration_ms;
   }
   out->total_warps = (int64_t)out->thread_blocks * out->warps_per_block;
-  out->est_duration_ms = 0.0;
   out->handle = -1;
   out->job = -1;
   return GS_OK;
+}
+
+// A catalog job's probe: its kernels' real launch shapes through the same
+// capture path, buffers on the executor's 2 MiB allocation granule.
+extern "C" int gs_job_probe(const gs_job_desc *job, gs_probe *out) {
+  int rc = validate(*job);
+  if (rc) return rc;
+  std::vector<gs_launch_desc> ls;
+  for (const Shape &sh : job_launches(*job)) {
+    gs_launch_desc d;
+    rc = gs_launch_desc_of(sh.fn, sh.grid, sh.block, sh.dsmem, &d);
+    if (rc) return rc;
+    ls.push_back(d);
+  }
+  std::vector<int64_t> bytes;
+  for (const Buf &b : job_buffers(*job)) bytes.push_back(round_granule(b.bytes));
+  return gs_request_from_launches(ls.data(), (int32_t)ls.size(), bytes.data(), (int32_t)bytes.size(), kHeap, out);
 }
 
 extern "C" int gs_job_io_bytes(const gs_job_desc *job, int64_t *in_bytes, int64_t *out_bytes) {

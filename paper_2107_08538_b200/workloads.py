@@ -42,8 +42,16 @@ class GsExecStats(ctypes.Structure):
                 ("decision_ms", c_double)]
 
 
+class GsLaunchDesc(ctypes.Structure):
+    _fields_ = [("thread_blocks", c_int32), ("threads_per_block", c_int32), ("regs_per_thread", c_int32),
+                ("smem_per_block", c_int32), ("est_duration_ms", c_double)]
+
+
 WORK_SIGNATURES = {
     "gs_job_probe": (c_int32, [POINTER(GsJobDesc), POINTER(nat.GsProbe)]),
+    "gs_request_from_launches": (c_int32, [POINTER(GsLaunchDesc), c_int32, POINTER(c_int64), c_int32, c_int64,
+                                           POINTER(nat.GsProbe)]),
+    "gs_launch_desc_of": (c_int32, [c_void_p, c_int32, c_int32, c_int32, POINTER(GsLaunchDesc)]),
     "gs_job_io_bytes": (c_int32, [POINTER(GsJobDesc), POINTER(c_int64), POINTER(c_int64)]),
     "gs_job_run_solo": (c_int32, [POINTER(GsJobDesc), c_int32, c_int32, c_void_p, c_int64,
                                   POINTER(GsJobRecord)]),
@@ -174,6 +182,21 @@ class ExecResult:
     kernel_launches: int
     decision_launches: int
     decision_ms: float
+
+
+def request_from_launches(launches, buffers, heap_limit_bytes: int = 8 << 20):
+    """Probe capture for any task: `launches` are
+    (thread_blocks, threads_per_block, regs_per_thread, smem_per_block
+    [, est_duration_ms]) as a launch wrapper records them, `buffers` the
+    task's distinct allocation sizes; returns the 64 B gs_probe the
+    placement engine takes (compute_resource_request's aggregation).  Host
+    arithmetic in libgs; no GPU needed."""
+    ls = (GsLaunchDesc * len(launches))(*[GsLaunchDesc(*l) for l in launches])
+    bs = (c_int64 * max(len(buffers), 1))(*[int(b) for b in buffers])
+    out = nat.GsProbe()
+    nat.check(lib().gs_request_from_launches(ls, len(launches), bs, len(buffers), int(heap_limit_bytes),
+                                             ctypes.byref(out)))
+    return out
 
 
 def ledger_capacity(device: int = 0) -> int:

@@ -40,3 +40,7 @@ def test_exec_stats_layout():
 
 def test_job_desc_layout():
     assert py_fields(W.GsJobDesc) == c_fields("gs_job_desc")
+
+
+def test_launch_desc_layout():
+    assert py_fields(W.GsLaunchDesc) == c_fields("gs_launch_desc")
