@@ -100,13 +100,18 @@ class Clocks:
                 "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(sm)}
 
 
-def run_steps(W, jobs, policy, device, workers, mode, steps, warmup, torch):
-    """W warm-up + K timed steps; device-timed with CUDA events.  The
-    ledger capacity is queried once (a slow driver query) before the steps."""
+def run_steps(W, jobs, policy, device, workers, mode, steps, warmup, torch, dist=None):
+    """W warm-up + K timed steps; device-timed with CUDA events; the K steps
+    are bracketed by a barrier across ranks (and a device synchronize) on
+    both sides.  The ledger capacity is queried once (a slow driver query)
+    before the steps."""
     cap = W.ledger_capacity(device)
     for w in range(warmup):
         r = W.run_jobs(jobs, policy=policy, devices=[device], workers=workers, mode=mode, ledger_bytes=cap)
         log(f"warmup {w} {policy} mode={mode}: {r.makespan_ms:.1f} ms, {r.completed} done, {r.oom} oom")
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
     times, results = [], []
     # the interpreter's cyclic GC is host noise, not executor work: collect
     # before the timed steps and keep it off while they run
@@ -125,6 +130,9 @@ def run_steps(W, jobs, policy, device, workers, mode, steps, warmup, torch):
         log(f"step {policy} mode={mode}: {times[-1]:.1f} ms (executor makespan {res.makespan_ms:.1f}), "
             f"{res.completed} done, {res.oom} oom")
     gc.enable()
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
     return times, results
 
 
@@ -316,11 +324,11 @@ def main() -> int:
         dist.barrier()
     with Clocks(device) as clk:
         times, results = run_steps(W, jobs, args.policy, device, args.workers, W.MODE_DEVICE, args.steps,
-                                   args.warmup, torch)
+                                   args.warmup, torch, dist)
     ours = summarize(results, times)
     sa = None
     if not args.skip_sa:
-        st, sr = run_steps(W, jobs, "sa", device, args.workers, W.MODE_DEVICE, args.steps, 1, torch)
+        st, sr = run_steps(W, jobs, "sa", device, args.workers, W.MODE_DEVICE, args.steps, 1, torch, dist)
         sa = summarize(sr, st)
     W.unstage()
     kern, solo_ms = kernel_rooflines(W, C, mix, device, pk)
@@ -330,20 +338,26 @@ def main() -> int:
     if not args.skip_e2e:
         log("staging (e2e mode: pinned host inputs)")
         W.stage(jobs, [device], W.MODE_E2E)
-        et, er = run_steps(W, jobs, args.policy, device, args.workers, W.MODE_E2E, args.steps, 1, torch)
+        et, er = run_steps(W, jobs, args.policy, device, args.workers, W.MODE_E2E, args.steps, 1, torch, dist)
         e2e = summarize(er, et)
         e2e["h2d"] = sum(r["h2d_bytes"] for r in er[-1].records)
         e2e["d2h"] = sum(r["d2h_bytes"] for r in er[-1].records)
         if not args.skip_sa:
-            st2, sr2 = run_steps(W, jobs, "sa", device, args.workers, W.MODE_E2E, args.steps, 1, torch)
+            st2, sr2 = run_steps(W, jobs, "sa", device, args.workers, W.MODE_E2E, args.steps, 1, torch, dist)
             sa_e2e = summarize(sr2, st2)
         W.unstage()
 
     # ---- max over ranks ----
     ms_step = ours["ms_per_step"]
     e2e_ms = e2e["ms_per_step"] if e2e else None
-    ms_step, e2e_max = max_over_ranks([ms_step, e2e_ms or 0.0], dist, device="cuda")
+    ms_step, e2e_max, sa_max, sa_e2e_max = max_over_ranks(
+        [ms_step, e2e_ms or 0.0, sa["ms_per_step"] if sa else 0.0, sa_e2e["ms_per_step"] if sa_e2e else 0.0],
+        dist, device="cuda")
     e2e_ms = e2e_max or None
+    if sa:
+        sa["ms_per_step"] = sa_max
+    if sa_e2e:
+        sa_e2e["ms_per_step"] = sa_e2e_max
     n_total = len(jobs) * world
     value = whole_job_rate(len(jobs), world, ms_step)
 
