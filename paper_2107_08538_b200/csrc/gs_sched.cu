@@ -123,7 +123,7 @@ struct KParams {
   int32_t n_cmds, max_sm_pad, max_resident, sweep;
   int32_t stage_q;   // int4 count of all staged ledger blocks
   int32_t scratch_off;
-  int32_t fifo_off, fifo_cap, fifo_stride, pad0;
+  int32_t fifo_off, fifo_cap, fifo_stride, sweep_fast;
   KDev dev[GS_MAX_DEVICES];
   SchedState *st;
   const Cmd *cmds;
@@ -1123,6 +1123,205 @@ __device__ __forceinline__ unsigned long long globaltimer() {
   return t;
 }
 
+// Specialised mgb-warps sweep (BASELINE cfg 4).  The same decisions as
+// submit / fifo_pop_release / on_release above, for the case the sweep
+// stream is built of: fresh probes and an empty pending FIFO.  Lane d holds
+// device d's ledger header in registers; _try_mgb_warps
+// (schedulers.py:155-171: feasible = free_mem >= mem, choose
+// min((in_use_warps, idx))) is one redux.sync min over the packed 32-bit
+// key (in_use_warps << 5 | d), exact while every in_use_warps is in
+// [0, 2^26); release_task (device_model.py:192-209) is a lane-local update.
+// Only that chain is serial: the events and residency rows of a batch of 32
+// probes are written afterwards, one lane per probe, while the next batch
+// streams in from HBM.  The chain hands over to the general path, with
+// identical state, at the first probe it does not cover (not fresh,
+// deferred, a full resident FIFO, or a key out of range) and returns that
+// probe's index.
+constexpr long long kKeyLim = 1LL << 26;
+
+__device__ int sweep_warps_fast(const KParams &p, Smem &S, int *dyn, int lane) {
+  __shared__ long long q_mem[33], q_tw[33];
+  __shared__ int q_h[33], q_lv[33];
+  __shared__ int q_dev[32], q_rd[32], q_rh[32];  // decision, released (dev, handle)
+  __shared__ int32_t *q_res[GS_MAX_DEVICES];
+  __shared__ int q_stride[GS_MAX_DEVICES];
+  const int n = p.n_cmds, nd = p.n_dev;
+  const bool mine = lane < nd;
+  if (mine) {
+    q_res[lane] = p.dev[lane].res;
+    q_stride[lane] = p.dev[lane].stride;
+  }
+  const long long cap = mine ? p.dev[lane].spec.mem_bytes : 0;
+  long long fr = mine ? S.led[lane].free_mem : 0, iu = mine ? S.led[lane].in_use_warps : 0;
+  const long long fr0 = fr, iu0 = iu;
+  int nas = 0, nrel = 0;
+  bool released = false;
+  int head = S.st.fifo_head, tail = S.st.fifo_tail;
+  int hs = head % p.fifo_cap, ts = tail % p.fifo_cap;
+  long long ne = S.st.n_events;
+  int stop_at = n;
+  int *const fifo = dyn + p.fifo_off;
+  const int fst = p.fifo_stride;
+  const int32_t *src = reinterpret_cast<const int32_t *>(p.sweep_probes);
+  // probe words: mem_bytes 0-1, total_warps 4-5, handle 13, level 15
+  long long r_mem = 0, r_tw = 0;
+  int r_h = 0, r_lv = 0;
+  if (lane < n) {
+    const int32_t *w = src + 16 * lane;
+    r_mem = *reinterpret_cast<const long long *>(w);
+    r_tw = *reinterpret_cast<const long long *>(w + 4);
+    r_h = w[13];
+    r_lv = w[15];
+  }
+  if (lane == 0) {  // sentinel after the last probe of a batch
+    q_mem[32] = 0;
+    q_tw[32] = 0;
+    q_h[32] = 0;
+    q_lv[32] = GS_PROBE_FRESH;
+  }
+  for (int base = 0; base < n && stop_at == n; base += 32) {
+    __syncwarp();
+    q_mem[lane] = r_mem;
+    q_tw[lane] = r_tw;
+    q_h[lane] = r_h;
+    q_lv[lane] = r_lv;
+    q_dev[lane] = -1;
+    q_rd[lane] = -1;
+    __syncwarp();
+    const int nx = base + 32 + lane;  // next batch: loads in flight while this one is decided
+    if (nx < n) {
+      const int32_t *w = src + 16 * (size_t)nx;
+      r_mem = *reinterpret_cast<const long long *>(w);
+      r_tw = *reinterpret_cast<const long long *>(w + 4);
+      r_h = w[13];
+      r_lv = w[15];
+    }
+    const int cnt = min(32, n - base);
+    int j = 0;
+    long long mem = q_mem[0], tw = q_tw[0];
+    int h = q_h[0], lv = q_lv[0];
+    // the oldest resident's slot, read ahead of the push that may precede its pop
+    int o_d = fifo[hs * fst], o_h = fifo[hs * fst + 1];
+    long long o_m = *reinterpret_cast<const long long *>(fifo + hs * fst + 6);
+    long long o_w = *reinterpret_cast<const long long *>(fifo + hs * fst + 8);
+    for (; j < cnt; ++j) {
+      const long long n_mem = q_mem[j + 1], n_tw = q_tw[j + 1];  // next probe, ahead of use
+      const int n_h = q_h[j + 1], n_lv = q_lv[j + 1];
+      const bool key_ok = !mine || (iu >= 0 && iu < kKeyLim);
+      if (!(lv & GS_PROBE_FRESH) || !__all_sync(kFull, key_ok)) break;
+      const bool ok = mine && fr >= mem;
+      const unsigned m = __reduce_min_sync(kFull, ok ? ((unsigned)iu << 5) | (unsigned)lane : 0xffffffffu);
+      if (m == 0xffffffffu) {
+        if (__any_sync(kFull, mine && !(mem > cap))) break;  // deferred: the general path queues it
+        // _impossible_everywhere: rejected (q_dev stays -1)
+      } else {
+        if (tail - head >= p.fifo_cap) break;  // the general path flags the overflow
+        const int best = (int)(m & 31u);
+        // assign (reserve_memory, assign_memory, add_warps)
+        if (lane == best) {
+          fr -= mem;
+          iu += tw;
+          ++nas;
+        }
+        if (lane == 0) {
+          int *slot = fifo + ts * fst;
+          slot[0] = best;
+          slot[1] = h;
+          slot[2] = 0;
+          reinterpret_cast<long long *>(slot + 6)[0] = mem;
+          reinterpret_cast<long long *>(slot + 6)[1] = tw;
+          q_dev[j] = best;
+        }
+        if (ts == hs) {  // the FIFO was empty: the oldest resident is this task
+          o_d = best;
+          o_h = h;
+          o_m = mem;
+          o_w = tw;
+        }
+        ++tail;
+        if (++ts == p.fifo_cap) ts = 0;
+        if (tail - head > p.max_resident) {
+          // release the oldest resident task, then on_release over an empty
+          // pending FIFO (it only records the grow epochs)
+          if (lane == o_d) {
+            fr += o_m;
+            iu -= o_w;
+            ++nrel;
+          }
+          if (lane == 0) {
+            q_rd[j] = o_d;
+            q_rh[j] = o_h;
+          }
+          ++head;
+          if (++hs == p.fifo_cap) hs = 0;
+          released = true;
+          __syncwarp();
+          o_d = fifo[hs * fst];
+          o_h = fifo[hs * fst + 1];
+          o_m = *reinterpret_cast<const long long *>(fifo + hs * fst + 6);
+          o_w = *reinterpret_cast<const long long *>(fifo + hs * fst + 8);
+        }
+      }
+      mem = n_mem;
+      tw = n_tw;
+      h = n_h;
+      lv = n_lv;
+    }
+    if (j < cnt) stop_at = base + j;
+    __syncwarp();
+    // this batch's outputs, one lane per probe: events, assigned rows, then
+    // the released rows (ordered after the assignments by the warp barrier)
+    if (lane < j) {
+      const int d = q_dev[lane];
+      const long long e = ne + lane;
+      if (e < p.events_cap) {
+        p.events[3 * e] = d >= 0 ? 0 : 2;
+        p.events[3 * e + 1] = q_h[lane];
+        p.events[3 * e + 2] = d;
+      }
+      if (d >= 0) {
+        long long *row = reinterpret_cast<long long *>(q_res[d] + (size_t)q_h[lane] * q_stride[d]);
+        row[0] = q_mem[lane];  // mem_bytes
+        row[1] = q_tw[lane];   // warps
+        row[2] = 0;            // regs_per_block
+        row[3] = 0;            // smem_per_block
+        row[4] = 1;            // present = 1, has_blocks = 0
+        row[5] = 0;            // warps_per_block, thread_blocks
+      }
+    }
+    __syncwarp();
+    if (lane < j && q_rd[lane] >= 0) {
+      const int d = q_rd[lane];
+      reinterpret_cast<gs_residency *>(q_res[d] + (size_t)q_rh[lane] * q_stride[d])->present = 0;
+    }
+    ne += j;
+  }
+  __syncwarp();
+  // hand the chain's state back to the shared ledgers
+  if (mine) {
+    SLed &L = S.led[lane];
+    L.free_mem = fr;
+    L.in_use_warps = iu;
+    L.held_mem += fr0 - fr;
+    L.held_warps += iu - iu0;
+    L.version += 3LL * nas + nrel;
+    L.grow_epoch += nrel;
+    if (nas | nrel) L.dirty |= 1;
+    if (released) S.st.seen_epoch[lane] = L.grow_epoch;
+  }
+  if (lane == 0) {
+    if (released) {
+      S.st.n_tried = 0;
+      S.st.n_admitted = 0;
+    }
+    S.st.fifo_head = head;
+    S.st.fifo_tail = tail;
+    S.st.n_events = ne;
+  }
+  __syncwarp();
+  return stop_at;
+}
+
 __global__ void __launch_bounds__(kThreads, 1) gs_interp_kernel(KParams p) {
   extern __shared__ __align__(16) int dyn[];
   __shared__ Smem S;
@@ -1144,8 +1343,10 @@ __global__ void __launch_bounds__(kThreads, 1) gs_interp_kernel(KParams p) {
     // max_resident tasks are resident or requests are queued, release the
     // oldest resident task and re-drive the FIFO.
     const int32_t *src = reinterpret_cast<const int32_t *>(p.sweep_probes);
-    int nextw = (lane < 16 && p.n_cmds > 0) ? src[lane] : 0;
-    for (int ci = 0; ci < p.n_cmds; ++ci) {
+    int ci0 = 0;
+    if (p.sweep_fast && p.policy == GS_POLICY_MGB_WARPS) ci0 = sweep_warps_fast(p, S, dyn, lane);
+    int nextw = (lane < 16 && ci0 < p.n_cmds) ? src[16 * ci0 + lane] : 0;
+    for (int ci = ci0; ci < p.n_cmds; ++ci) {
       if (lane < 16) reinterpret_cast<int32_t *>(&S.cur)[lane] = nextw;
       __syncwarp();
       if (lane < 16 && ci + 1 < p.n_cmds) nextw = src[16 * (ci + 1) + lane];  // prefetch next probe
@@ -1673,7 +1874,12 @@ int gs_engine_open(int cuda_device, gs_engine **out) {
   if (prop.major < 10) return set_err(GS_ERR_CUDA, "libgs is built for sm_100a (B200)");
   auto *eng = new gs_engine();
   eng->cuda_dev = cuda_device;
-  eng->max_smem = (int)prop.sharedMemPerBlockOptin - (int)sizeof(Smem) - 1024;
+  {
+    // dynamic shared memory left next to the kernel's static arrays
+    cudaFuncAttributes fa;
+    CU(cudaFuncGetAttributes(&fa, gs_interp_kernel));
+    eng->max_smem = ((int)prop.sharedMemPerBlockOptin - (int)fa.sharedSizeBytes) & ~15;
+  }
   CU(cudaFuncSetAttribute(gs_interp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, eng->max_smem));
   {
     // decisions preempt workload blocks at the block scheduler
@@ -2117,6 +2323,12 @@ int gs_sweep(gs_sched *s, const gs_probe *probes, int32_t n, int32_t max_residen
   }
   L.p.sweep = 1;
   L.p.sweep_probes = dprobes;
+  {
+    // GS_SWEEP_GENERAL=1: every probe through the general interpreter path
+    // (the specialised mgb-warps chain is checked against it in the tests)
+    const char *g = getenv("GS_SWEEP_GENERAL");
+    L.p.sweep_fast = !(g && g[0] == '1');
+  }
   {
     // resident FIFO slots with cached residency data (kSlotHdr + blocks)
     int stride = kSlotHdr + (s->policy == GS_POLICY_MGB_SM ? L.p.max_sm_pad : 0);

@@ -90,3 +90,68 @@ def test_ring_mode_replays_reference_streams(chunk):
         finally:
             be.close()
     assert n > 0
+
+
+def _sweep_state(spec, n_dev, probes, max_res, policy, general, monkeypatch):
+    """Events plus every byte of state a sweep leaves: ledger headers and
+    the residency row of every handle on every device."""
+    from paper_2107_08538_b200 import _native as nat
+    from paper_2107_08538_b200.gpushare import DeviceState, Scheduler, parse_policy
+
+    monkeypatch.setenv("GS_SWEEP_GENERAL", "1" if general else "0")
+    devs = [DeviceState(spec, i) for i in range(n_dev)]
+    sched = Scheduler(devs, parse_policy(policy))
+    cap = 2 * len(probes) + 16
+    ev = np.zeros((cap, 3), dtype=np.int32)
+    ne, ms = ctypes.c_int64(), ctypes.c_float()
+    lib = nat.lib()
+    nat.check(lib.gs_sweep(sched._ptr, probes.ctypes.data, len(probes), max_res, ev.ctypes.data, cap,
+                           ctypes.byref(ne), ctypes.byref(ms)))
+    hdr = [ctypes.string_at(ctypes.addressof(d._led), 56) for d in devs]  # all but rr_cursor/sm_count
+    rows = []
+    row = nat.GsResidency()
+    for d in devs:
+        for h in range(len(probes)):
+            nat.check(lib.gs_residency_read(d._ptr, h, ctypes.byref(row), None))
+            rows.append(ctypes.string_at(ctypes.addressof(row), ctypes.sizeof(row)) if row.present else b"")
+    return ev[: ne.value], hdr, rows, lib.gs_pending_count(sched._ptr)
+
+
+@pytest.mark.parametrize("label", ["b200x2-warps-3k", "p100x2-warps-2k", "b200x8-warps-1k"])
+def test_gpu_sweep_fast_chain_matches_general_path(label, monkeypatch):
+    """The specialised mgb-warps sweep chain leaves exactly the state the
+    general interpreter path does: events, ledger headers (free/in-use,
+    version, held sums, grow epoch) and residency rows — including the
+    streams that defer and hand over to the general path mid-sweep."""
+    spec, n_dev, probes, max_res, policy = sweep_inputs(label)
+    fast = _sweep_state(spec, n_dev, probes, max_res, policy, False, monkeypatch)
+    slow = _sweep_state(spec, n_dev, probes, max_res, policy, True, monkeypatch)
+    np.testing.assert_array_equal(fast[0], slow[0])
+    np.testing.assert_array_equal(fast[0], SWEEPS[label])
+    assert fast[1] == slow[1]
+    assert fast[2] == slow[2]
+    assert fast[3] == slow[3]
+
+
+@pytest.mark.parametrize("case", ["non_fresh", "wide_key"])
+def test_gpu_sweep_fast_chain_rejects_and_hands_over(case):
+    """Oversized probes are rejected inside the fast chain; a non-fresh probe,
+    or in-use warps beyond the packed 32-bit key, hands the rest of the
+    stream to the general path — all vs the oracle."""
+    from oracle import oracle as O
+    from paper_2107_08538_b200.gpushare import device_spec
+    from paper_2107_08538_b200.sweep import gen_probes
+
+    spec = device_spec("b200")
+    probes = gen_probes(5000, seed=5)
+    probes["mem_bytes"][::97] = spec.mem_bytes + 1  # impossible everywhere
+    if case == "non_fresh":
+        probes["level"][4000] = 0                    # not fresh (still a new handle)
+    else:
+        probes["total_warps"][3000:3400] = 1 << 24   # in_use_warps passes 2^26
+    ev, final, _ = run_gpu_sweep(spec, 8, probes, 32, "mgb-warps")
+    devs = [O.OracleDevice(spec, i) for i in range(8)]
+    oev = O.OracleScheduler(devs, 3, 6, True).sweep(probes, 32)
+    np.testing.assert_array_equal(ev, oev)
+    assert (ev[:, 0] == 2).sum() == len(range(0, 5000, 97))
+    np.testing.assert_array_equal(final, np.array([d.snapshot() for d in devs], dtype=np.int64))
