@@ -265,10 +265,30 @@ __device__ __forceinline__ int sm_cap(const KDev &D, int *dyn, int s, const Shap
   return (int)c;
 }
 
-__device__ __forceinline__ long long warp_total_cap(const KDev &D, int *dyn, const Shape &sh, int lane) {
+// Warp sum of per-SM block counts, each clamped to T: one redux.sync when
+// n_sm * T fits in 31 bits (every partial and total sum does), else 64-bit
+// shuffles.
+__device__ __forceinline__ long long warp_sum_blocks(long long v, bool small) {
+  return small ? (long long)__reduce_add_sync(kFull, (unsigned)v) : warp_sum64(v);
+}
+__device__ __forceinline__ bool blocks_small(const KDev &D, const Shape &sh) {
+  return sh.T >= 0 && sh.T <= INT_MAX / max(D.n_sm, 1);
+}
+
+// Σ sm_cap over the device's SMs; also leaves every SM's cap in cap[] and
+// the warp max in *mx for the warp_plan that follows an admission.
+__device__ __forceinline__ long long warp_total_cap(const KDev &D, int *dyn, const Shape &sh, int *cap, int *mx,
+                                                    int lane) {
   long long tot = 0;
-  for (int s = lane; s < D.n_sm; s += 32) tot += sm_cap(D, dyn, s, sh);
-  return warp_sum64(tot);
+  int m = 0;
+  for (int s = lane; s < D.n_sm; s += 32) {
+    const int c = sm_cap(D, dyn, s, sh);
+    cap[s] = c;
+    tot += c;
+    m = max(m, c);
+  }
+  *mx = __reduce_max_sync(kFull, m);
+  return warp_sum_blocks(tot, blocks_small(D, sh));
 }
 
 // occupancy_limit_per_sm (device_model.py:48-58) x sm_count.
@@ -369,18 +389,26 @@ __device__ void led_to_stage(const KParams &p, int *dyn, Smem &S, int lane) {
 // Closed-form round-robin placement == try_place_blocks
 // (device_model.py:120-139).  Writes P[0..n) and returns the final cursor,
 // or -1 when the blocks cannot fit (the reference's None).
-__device__ int warp_plan(const KDev &D, int *dyn, const SLed &L, const Shape &sh, int *cap, int *P, int lane) {
+// With caps_mx >= 0 the caller already left this shape's caps in cap[]
+// (warp_total_cap, tot >= T) and caps_mx is their maximum.
+__device__ int warp_plan(const KDev &D, int *dyn, const SLed &L, const Shape &sh, int *cap, int *P, int lane,
+                         int caps_mx = -1) {
   const int n = D.n_sm;
-  long long tot = 0;
-  int mx = 0;
-  for (int s = lane; s < n; s += 32) {
-    int c = sm_cap(D, dyn, s, sh);
-    cap[s] = c;
-    tot += c;
-    mx = max(mx, c);
+  const bool small = blocks_small(D, sh);
+  long long tot = sh.T;
+  int mx = caps_mx;
+  if (caps_mx < 0) {
+    tot = 0;
+    mx = 0;
+    for (int s = lane; s < n; s += 32) {
+      int c = sm_cap(D, dyn, s, sh);
+      cap[s] = c;
+      tot += c;
+      mx = max(mx, c);
+    }
+    tot = warp_sum_blocks(tot, small);
+    mx = __reduce_max_sync(kFull, mx);
   }
-  tot = warp_sum64(tot);
-  mx = __reduce_max_sync(kFull, mx);
   __syncwarp();
   if (tot < sh.T) return -1;
   int c0 = L.rr_cursor % n;
@@ -396,7 +424,7 @@ __device__ int warp_plan(const KDev &D, int *dyn, const SLed &L, const Shape &sh
     const int mid = (lo + hi + 1) >> 1;
     long long sk = 0;
     for (int s = lane; s < n; s += 32) sk += min(cap[s], mid);
-    sk = warp_sum64(sk);
+    sk = warp_sum_blocks(sk, small);
     if (sk <= sh.T) lo = mid; else hi = mid - 1;
   }
   const int k = lo;
@@ -406,7 +434,7 @@ __device__ int warp_plan(const KDev &D, int *dyn, const SLed &L, const Shape &sh
     P[s] = v;
     sk += v;
   }
-  sk = warp_sum64(sk);
+  sk = warp_sum_blocks(sk, small);
   __syncwarp();
   const long long rem = sh.T - sk;
   int last = -1;
@@ -696,7 +724,7 @@ __device__ Dec decide(const KParams &p, Smem &S, int *dyn, const gs_probe &pr, u
       r_mem = row->mem_bytes;
       r_warps = row->warps;
     }
-    int chosen = -1;
+    int chosen = -1, caps_mx = -1;
     if (p.policy == GS_POLICY_MGB_WARPS) {
       // _try_mgb_warps (schedulers.py:155-171): feasible = free_mem >= mem,
       // choose min((in_use_warps, idx))
@@ -713,9 +741,10 @@ __device__ Dec decide(const KParams &p, Smem &S, int *dyn, const gs_probe &pr, u
       // exact per-SM count only for devices that pass both.
       const bool cand = lane < n_dev && ((mask >> lane) & 1) && S.led[lane].free_mem >= sh.mem &&
                         agg_admits(S, lane, sh);
+      int *cap = dyn + p.scratch_off;
       for (unsigned m = __ballot_sync(kFull, cand); m; m &= m - 1) {
         const int d = __ffs(m) - 1;
-        if (warp_total_cap(p.dev[d], dyn, sh, lane) >= sh.T) {
+        if (warp_total_cap(p.dev[d], dyn, sh, cap, &caps_mx, lane) >= sh.T) {
           chosen = d;
           break;
         }
@@ -743,7 +772,7 @@ __device__ Dec decide(const KParams &p, Smem &S, int *dyn, const gs_probe &pr, u
     const bool sm_policy = p.policy == GS_POLICY_MGB_SM;
     if (sm_policy) {
       int *cap = dyn + p.scratch_off;
-      const int cur = warp_plan(D, dyn, L, sh, cap, P, lane);
+      const int cur = warp_plan(D, dyn, L, sh, cap, P, lane, caps_mx);
       warp_commit_blocks(D, dyn, L, h, sh, P, cur, lane);  // commit_placement
     }
     const long long new_mem = (present ? pm : 0) + sh.mem, new_warps = (present ? pw : 0) + sh.tw;
