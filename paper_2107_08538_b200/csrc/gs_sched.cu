@@ -887,6 +887,17 @@ __device__ void on_release(const KParams &p, Smem &S, int *dyn, bool write_out, 
     dirty = __ballot_sync(kFull, g);
   }
   const unsigned dmask = mgb ? dirty : all;
+  if (mgb && !dirty && !write_out) {
+    // no device's grow epoch moved since the last full pass: nothing pending
+    // can fit (resources only shrank) — the pass below would try nothing
+    // and keep the FIFO as is; skip reading it back from HBM
+    if (lane == 0) {
+      S.st.n_tried = P > 0 ? (p.skip_ahead ? P : 1) : 0;
+      S.st.n_admitted = 0;
+    }
+    __syncwarp();
+    return;
+  }
   int w = 0, tried = 0, admitted = 0;
   bool stop = false;
   const unsigned lt = (1u << lane) - 1u;
