@@ -202,6 +202,14 @@ int gs_submit_batch(gs_sched *s, const gs_probe *reqs, int32_t n, gs_decision *o
  * *n_admitted are set.  Admitted entries leave the device-side queue. */
 int gs_on_release(gs_sched *s, gs_decision *out, int32_t out_cap,
                   int32_t *n_tried, int32_t *n_admitted);
+/* A task's completion in one decision launch: DeviceState.release_task
+ * (device_model.py:192-209) on the scheduler's device `dev_index`, then
+ * on_release (schedulers.py:97-113) — the pair SimEngine runs at every
+ * task end (sim_engine.py:541-547).  Outputs as gs_release + gs_on_release;
+ * the re-drive runs even when the release names an unknown task (then
+ * GS_ERR_CONTRACT is returned after it). */
+int gs_release_redrive(gs_sched *s, int32_t dev_index, int32_t handle, int64_t *freed,
+                       gs_decision *out, int32_t out_cap, int32_t *n_tried, int32_t *n_admitted);
 /* job_ended (schedulers.py:115-123). */
 int gs_job_ended(gs_sched *s, int32_t job);
 int32_t gs_pending_count(gs_sched *s);

@@ -111,6 +111,8 @@ SIGNATURES = {
     "gs_submit": (c_int32, [c_void_p, POINTER(GsProbe), POINTER(GsDecision)]),
     "gs_submit_batch": (c_int32, [c_void_p, c_void_p, c_int32, c_void_p]),
     "gs_on_release": (c_int32, [c_void_p, c_void_p, c_int32, POINTER(c_int32), POINTER(c_int32)]),
+    "gs_release_redrive": (c_int32, [c_void_p, c_int32, c_int32, POINTER(c_int64), c_void_p, c_int32,
+                                     POINTER(c_int32), POINTER(c_int32)]),
     "gs_job_ended": (c_int32, [c_void_p, c_int32]),
     "gs_pending_count": (c_int32, [c_void_p]),
     "gs_sched_job_state": (c_int32, [c_void_p, c_void_p, c_void_p, POINTER(c_int32)]),

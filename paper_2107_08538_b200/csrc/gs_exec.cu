@@ -493,15 +493,18 @@ int gs_exec_run_arrivals(const gs_job_desc *jobs, int32_t n_jobs, const double *
   }
   const auto t0 = Clock::now();
 
+  auto admit_drained = [&](int32_t tried, int32_t adm) {  // caller holds mu
+    for (int k = 0; k < tried; ++k)
+      if (drain[k].outcome == GS_ASSIGN) admitted[drain[k].handle] = drain[k].device;
+    if (adm) cv.notify_all();
+  };
   auto redrive = [&]() {  // caller holds mu
     int32_t tried = 0, adm = 0;
     const auto a = Clock::now();
     int r = gs_on_release(sched, drain.data(), (int32_t)drain.size(), &tried, &adm);
     decision_ms += ms_since(a);
     if (r < 0) return r;
-    for (int k = 0; k < tried; ++k)
-      if (drain[k].outcome == GS_ASSIGN) admitted[drain[k].handle] = drain[k].device;
-    if (adm) cv.notify_all();
+    admit_drained(tried, adm);
     return GS_OK;
   };
 
@@ -602,15 +605,20 @@ int gs_exec_run_arrivals(const gs_job_desc *jobs, int32_t n_jobs, const double *
         first_err = r;
         first_msg = t_err;
       }
-      const auto a = Clock::now();
       if (task_level) {
+        // release_task + the FIFO re-drive in one decision launch
+        int32_t tried = 0, adm = 0;
         int64_t freed = 0;
-        gs_release(ledgers[dev], j, &freed);
+        const auto a = Clock::now();
+        const int rr = gs_release_redrive(sched, dev, j, &freed, drain.data(), (int32_t)drain.size(), &tried, &adm);
+        decision_ms += ms_since(a);
+        if (rr >= 0) admit_drained(tried, adm);
       } else {
+        const auto a = Clock::now();
         gs_job_ended(sched, j);
+        decision_ms += ms_since(a);
+        redrive();
       }
-      decision_ms += ms_since(a);
-      redrive();
     }
     const auto tw = Clock::now();
     for (int d = 0; d < n_devices; ++d) {

@@ -2239,6 +2239,45 @@ int gs_on_release(gs_sched *s, gs_decision *out, int32_t out_cap, int32_t *n_tri
   return GS_OK;
 }
 
+int gs_release_redrive(gs_sched *s, int32_t dev_index, int32_t handle, int64_t *freed, gs_decision *out,
+                       int32_t out_cap, int32_t *n_tried, int32_t *n_admitted) {
+  gs_engine *eng = s->eng;
+  EngineLock g(eng);
+  if (dev_index < 0 || dev_index >= (int32_t)s->devs.size()) return set_err(GS_ERR_CONFIG, "bad device index");
+  int rc = check_handle(eng, handle);
+  if (!rc) rc = ensure_pending(s, 0);
+  if (!rc) rc = ensure_cmds(eng, 2);
+  if (rc) return rc;
+  Launch L;
+  rc = sched_params(s, L);
+  if (rc) return rc;
+  Cmd *c = eng->cmds.h;
+  memset(c, 0, 2 * sizeof(Cmd));
+  c[0].op = OP_RELEASE;
+  c[0].dev = dev_index;
+  c[0].handle = handle;
+  c[1].op = OP_ON_RELEASE;
+  gs_decision res[2];
+  if (s->ring_active) {
+    rc = ring_call(s, c, 2, res);
+  } else {
+    eng->decisions++;
+    L.p.cmds = eng->cmds.d;
+    L.p.n_cmds = 2;
+    L.p.results = eng->results.d;
+    rc = launch(eng, L);
+    if (!rc) memcpy(res, eng->results.h, sizeof res);
+  }
+  if (rc) return rc;
+  const int tried = s->st.h->n_tried, adm = s->st.h->n_admitted;
+  if (n_tried) *n_tried = tried;
+  if (n_admitted) *n_admitted = adm;
+  if (out) memcpy(out, s->drain.h, sizeof(gs_decision) * std::min(tried, out_cap));
+  if (res[0].outcome == GS_ERR_CONTRACT) return set_err(GS_ERR_CONTRACT, "release of unknown task");
+  if (freed) *freed = res[0].free_mem_after;
+  return GS_OK;
+}
+
 int gs_job_ended(gs_sched *s, int32_t job) {
   gs_engine *eng = s->eng;
   EngineLock g(eng);
