@@ -155,3 +155,39 @@ def test_gpu_sweep_fast_chain_rejects_and_hands_over(case):
     np.testing.assert_array_equal(ev, oev)
     assert (ev[:, 0] == 2).sum() == len(range(0, 5000, 97))
     np.testing.assert_array_equal(final, np.array([d.snapshot() for d in devs], dtype=np.int64))
+
+
+@pytest.mark.parametrize("max_res,ev_cap", [(0, None), (1, None), (5, 700), (31, 100)])
+def test_gpu_sweep_fast_chain_fifo_edges(max_res, ev_cap, monkeypatch):
+    """FIFO depths where the oldest resident is the task just pushed
+    (max_resident 0) or a few slots back, and event logs shorter than the
+    stream: the specialised chain and the general path agree on the events,
+    the event count and the final ledgers, and both match the oracle."""
+    from oracle import oracle as O
+    from paper_2107_08538_b200 import _native as nat
+    from paper_2107_08538_b200.gpushare import DeviceState, Scheduler, device_spec, parse_policy
+    from paper_2107_08538_b200.sweep import gen_probes
+
+    spec = device_spec("b200")
+    probes = gen_probes(3000, seed=21, mem_gib=(10, 60))
+
+    def run(general):
+        monkeypatch.setenv("GS_SWEEP_GENERAL", "1" if general else "0")
+        devs = [DeviceState(spec, i) for i in range(3)]
+        sched = Scheduler(devs, parse_policy("mgb-warps"))
+        cap = ev_cap or 2 * len(probes) + 16
+        ev = np.zeros((cap, 3), dtype=np.int32)
+        ne, ms = ctypes.c_int64(), ctypes.c_float()
+        nat.check(nat.lib().gs_sweep(sched._ptr, probes.ctypes.data, len(probes), max_res, ev.ctypes.data, cap,
+                                     ctypes.byref(ne), ctypes.byref(ms)))
+        hdr = [ctypes.string_at(ctypes.addressof(d._led), 56) for d in devs]
+        return ev[: min(ne.value, cap)], ne.value, hdr
+
+    fast, slow = run(False), run(True)
+    np.testing.assert_array_equal(fast[0], slow[0])
+    assert fast[1] == slow[1]
+    assert fast[2] == slow[2]
+    devs = [O.OracleDevice(spec, i) for i in range(3)]
+    oev = O.OracleScheduler(devs, 3, 6, True).sweep(probes, max_res)
+    assert fast[1] == len(oev)
+    np.testing.assert_array_equal(fast[0], oev[: len(fast[0])])
