@@ -1236,19 +1236,28 @@ __device__ int sweep_warps_fast(const KParams &p, Smem &S, int *dyn, int lane) {
       r_h = w[13];
       r_lv = w[15];
     }
-    const int cnt = min(32, n - base);
+    // batch-level guards instead of per-probe ones: the chain covers the
+    // probes before the first non-fresh one, and only while every key stays
+    // packable — in_use_warps < 2^25 now and each total_warps < 2^20, so
+    // 32 assignments keep it below 2^26 (releases only lower it)
+    int cnt = min(32, n - base);
+    {
+      const unsigned nf = __ballot_sync(kFull, lane < cnt && (!(q_lv[lane] & GS_PROBE_FRESH) || q_tw[lane] < 0 ||
+                                                              q_tw[lane] >= (1LL << 20)));
+      if (nf) cnt = __ffs(nf) - 1;
+      if (!__all_sync(kFull, !mine || (iu >= 0 && iu < (kKeyLim >> 1)))) cnt = 0;
+    }
+    const int full = min(32, n - base);
     int j = 0;
     long long mem = q_mem[0], tw = q_tw[0];
-    int h = q_h[0], lv = q_lv[0];
+    int h = q_h[0];
     // the oldest resident's slot, read ahead of the push that may precede its pop
     int o_d = fifo[hs * fst], o_h = fifo[hs * fst + 1];
     long long o_m = *reinterpret_cast<const long long *>(fifo + hs * fst + 6);
     long long o_w = *reinterpret_cast<const long long *>(fifo + hs * fst + 8);
     for (; j < cnt; ++j) {
       const long long n_mem = q_mem[j + 1], n_tw = q_tw[j + 1];  // next probe, ahead of use
-      const int n_h = q_h[j + 1], n_lv = q_lv[j + 1];
-      const bool key_ok = !mine || (iu >= 0 && iu < kKeyLim);
-      if (!(lv & GS_PROBE_FRESH) || !__all_sync(kFull, key_ok)) break;
+      const int n_h = q_h[j + 1];
       const bool ok = mine && fr >= mem;
       const unsigned m = __reduce_min_sync(kFull, ok ? ((unsigned)iu << 5) | (unsigned)lane : 0xffffffffu);
       if (m == 0xffffffffu) {
@@ -1305,9 +1314,8 @@ __device__ int sweep_warps_fast(const KParams &p, Smem &S, int *dyn, int lane) {
       mem = n_mem;
       tw = n_tw;
       h = n_h;
-      lv = n_lv;
     }
-    if (j < cnt) stop_at = base + j;
+    if (j < full) stop_at = base + j;
     __syncwarp();
     // this batch's outputs, one lane per probe: events, assigned rows, then
     // the released rows (ordered after the assignments by the warp barrier)
