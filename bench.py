@@ -1,19 +1,30 @@
-"""Job-mix throughput on B200 under the GPU placement engine.
+"""Job-mix throughput on B200s under the GPU placement engine.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
-A step runs BASELINE cfg 1's job mix (32 Rodinia-class jobs, 3:1
-large:small, synthetic seeded inputs) end to end: every job's probe is
-placed by the sm_100a decision kernel (mgb-warps, Alg. 3), jobs run
-concurrently on per-job streams with stream-ordered allocations, releases
-re-drive the FIFO.  One process per GPU; under torchrun each rank runs its
-own mix on its own device (jobs are independent: placement shards them, no
-collective on the data path) -> scaling "weak".
+A step runs BASELINE cfg 1's job mix end to end on the whole fleet: 32
+Rodinia-class jobs per GPU (3:1 large:small, synthetic seeded inputs,
+gen_mix = gs/workload_gen.py:177-214 selection); every job's probe is placed
+by the sm_100a decision kernel (mgb-warps, Alg. 3) — ONE decision authority
+holding every GPU's ledger, as the reference's single Scheduler over all
+DeviceStates (gs/sim_engine.py:224-229) — jobs run concurrently on per-job
+streams of the GPU they were placed on, releases re-drive the FIFO.  Under
+torchrun (one process per GPU) rank 0 drives the fleet and the other ranks
+only join the barriers and the max over ranks (multi.py).  Per-GPU work is
+fixed as N grows -> scaling "weak".
 
-value   jobs/s with inputs resident in HBM when the timed region starts
-e2e     jobs/s through the same API with inputs in pinned host memory:
-        H2D of every input and D2H of every output inside the timed region
-sa      the one-job-per-GPU baseline (policy sa) on the same mix and device
+value      jobs completed / s with inputs resident in HBM when the timed
+           region starts (one staged copy of each template's inputs on every
+           fleet GPU; a job copies them D2D on the GPU it was placed on)
+e2e        the same through the same API with inputs in pinned host memory:
+           H2D of every input and D2H of every output inside the timed region
+sa         the one-job-per-GPU baseline (policy sa) on the same mix and fleet
+parity     the co-located jobs of the last timed step whose oracle outputs the
+           CPU leg computed: GPU output digest == oracle digest (bit-exact
+           kinds) or solo output within 1e-5 of the oracle (lud, backprop)
+placements the last timed step's placement log (every submit / release /
+           re-drive the decision authority made) replayed through the
+           golden-pinned oracle Scheduler: decisions checked / mismatches
 
 --impl reference times the reference's path on the host CPU: the C port of
 the reference scheduler (oracle/gs_oracle.c, schedulers.py semantics) plus
@@ -24,6 +35,7 @@ threads) on a bounded sample of the same mix.
 from __future__ import annotations
 
 import argparse
+import datetime
 import gc
 import json
 import os
@@ -37,7 +49,7 @@ sys.path.insert(0, REPO)
 
 METRIC = "job-mix jobs/s + mean turnaround at 1/2/4/8 B200 vs one-job-per-GPU; OOMs"
 UNIT = "jobs/s"
-
+EXACT_KINDS = {"bfs", "hotspot", "srad", "kmeans", "needle"}
 
 _T0 = time.time()
 
@@ -55,14 +67,11 @@ def peaks() -> dict:
         return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0, "_fallback": True}
 
 
-FP32_TFLOPS_NOMINAL = 148 * 128 * 2 * 1.965e9 / 1e12  # 74.4: 148 SMs x 128 FMA lanes
-
-
 class Clocks:
     """nvidia-smi sampling during the timed region (B200_PROFILING.md)."""
 
-    def __init__(self, device: int):
-        self.device = device
+    def __init__(self, devices: list[int]):
+        self.devices = devices
         self.proc = None
         self.path = f"/tmp/gs_clocks_{os.getpid()}.csv"
 
@@ -73,8 +82,8 @@ class Clocks:
              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
         try:
-            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={q}",
-                                          "--format=csv,noheader,nounits", "-lms", "200"],
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", ",".join(str(d) for d in self.devices),
+                                          f"--query-gpu={q}", "--format=csv,noheader,nounits", "-lms", "200"],
                                          stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
         except OSError:
             self.proc = None
@@ -100,60 +109,84 @@ class Clocks:
                 "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(sm)}
 
 
-def run_steps(W, jobs, policy, device, workers, mode, steps, warmup, torch, dist=None):
+class Barrier:
+    """Host barrier across ranks (gloo: idle ranks must not park a spinning
+    NCCL kernel on a GPU the fleet is running jobs on)."""
+
+    def __init__(self, dist):
+        self.dist = dist
+        self.group = dist.new_group(backend="gloo") if dist else None
+
+    def __call__(self):
+        if self.dist:
+            self.dist.barrier(group=self.group)
+
+
+def run_steps(W, jobs, policy, devices, workers, mode, steps, warmup, torch, barrier, cap, keep_log=False):
     """W warm-up + K timed steps; device-timed with CUDA events; the K steps
-    are bracketed by a barrier across ranks (and a device synchronize) on
-    both sides.  The ledger capacity is queried once (a slow driver query)
-    before the steps."""
-    cap = W.ledger_capacity(device)
+    are bracketed by a barrier across ranks and a synchronize of every fleet
+    device on both sides.  Returns (ms per step, results, placement log of
+    the last timed step)."""
     for w in range(warmup):
-        r = W.run_jobs(jobs, policy=policy, devices=[device], workers=workers, mode=mode, ledger_bytes=cap)
+        r = W.run_jobs(jobs, policy=policy, devices=devices, workers=workers, mode=mode, ledger_bytes=cap)
         log(f"warmup {w} {policy} mode={mode}: {r.makespan_ms:.1f} ms, {r.completed} done, {r.oom} oom")
-    torch.cuda.synchronize()
-    if dist:
-        dist.barrier()
+
+    def sync_all():
+        for d in devices:
+            torch.cuda.synchronize(d)
+
+    sync_all()
+    barrier()
     times, results = [], []
     # the interpreter's cyclic GC is host noise, not executor work: collect
     # before the timed steps and keep it off while they run
     gc.collect()
     gc.disable()
+    xlog = None
     for _ in range(steps):
-        torch.cuda.synchronize()
+        sync_all()
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record()
-        res = W.run_jobs(jobs, policy=policy, devices=[device], workers=workers, mode=mode, ledger_bytes=cap)
+        # the executor synchronizes every fleet device before it returns, so
+        # e1 (on the driving device) closes the whole fleet's step
+        res = W.run_jobs(jobs, policy=policy, devices=devices, workers=workers, mode=mode, ledger_bytes=cap)
         e1.record()
-        torch.cuda.synchronize()
+        sync_all()
         times.append(e0.elapsed_time(e1))
         results.append(res)
         log(f"step {policy} mode={mode}: {times[-1]:.1f} ms (executor makespan {res.makespan_ms:.1f}), "
             f"{res.completed} done, {res.oom} oom")
+    if keep_log:
+        xlog = W.exec_log()
     gc.enable()
-    torch.cuda.synchronize()
-    if dist:
-        dist.barrier()
-    return times, results
+    sync_all()
+    barrier()
+    return times, results, xlog
 
 
 def summarize(results, times):
     done = [r for res in results for r in res.records if r["state"] == "done"]
+    completed = sum(res.completed for res in results)
     return {
         "ms_per_step": statistics.fmean(times),
+        "completed_per_step": completed / len(results),
+        "submitted_per_step": len(results[0].records),
         "mean_turnaround_ms": statistics.fmean(r["turnaround_ms"] for r in done) if done else 0.0,
         "mean_wait_ms": statistics.fmean(r["wait_ms"] for r in done) if done else 0.0,
-        "completed": sum(res.completed for res in results),
+        "max_wait_ms": max((r["wait_ms"] for r in done), default=0.0),
         "oom": sum(res.oom for res in results),
         "crashed": sum(res.crashed for res in results),
         "kernel_launches": sum(res.kernel_launches for res in results),
         "decision_launches": sum(res.decision_launches for res in results),
         "decision_ms": sum(res.decision_ms for res in results),
+        "devices_used": sorted({r["device"] for r in done}),
     }
 
 
-def kernel_rooflines(W, C, jobs, device, pk):
-    """Every distinct job of the mix alone on the device (CUDA events on the
-    job's stream around its kernels).  Returns (per-kind roofline of the
+def kernel_rooflines(W, C, jobs, device, pk, fp32_peak):
+    """Every distinct template of the mix alone on one device (CUDA events on
+    the job's stream around its kernels).  Returns (per-kind roofline of the
     kind's largest job: algorithmic work / kernel time vs the measured peak,
     per-template solo ms)."""
     solo_ms, first = {}, {}
@@ -177,6 +210,10 @@ def kernel_rooflines(W, C, jobs, device, pk):
             out[kind] = {"bound": "hbm", "achieved": round(ach, 1), "peak": hbm, "unit": "GB/s",
                          "frac": round(ach / hbm, 4), "ms": round(ms, 3), "launches": rec.n_kernels,
                          "job": {"n": job.n, "iters": job.iters, "m": job.m}}
+            sv = C.survey_bytes(job)
+            if sv != work:  # SURVEY §8(d)'s per-iteration count differs from the executed algorithm's
+                out[kind]["survey_8d_bytes"] = sv
+                out[kind]["frac_survey_8d"] = round(sv / (ms * 1e-3) / 1e9 / hbm, 4)
         elif unit == "TC_FLOP":
             ach = work / (ms * 1e-3) / 1e12
             pkt = pk["bf16_tflops"]
@@ -185,9 +222,10 @@ def kernel_rooflines(W, C, jobs, device, pk):
                          "job": {"n": job.n, "batch": job.m}}
         else:
             ach = work / (ms * 1e-3) / 1e12
-            out[kind] = {"bound": "fp32", "achieved": round(ach, 2), "peak": round(FP32_TFLOPS_NOMINAL, 1),
-                         "unit": "TFLOP/s", "frac": round(ach / FP32_TFLOPS_NOMINAL, 4), "ms": round(ms, 3),
-                         "launches": rec.n_kernels, "job": {"n": job.n}}
+            out[kind] = {"bound": "fp32", "achieved": round(ach, 2), "peak": round(fp32_peak, 1),
+                         "unit": "TFLOP/s", "frac": round(ach / fp32_peak, 4), "ms": round(ms, 3),
+                         "launches": rec.n_kernels, "job": {"n": job.n},
+                         "peak_source": "measured FFMA peak (gs_measure_fp32_peak)"}
     return out, solo_ms
 
 
@@ -217,26 +255,54 @@ def pcie_h2d_gbps(torch) -> float:
     return 4.0 * n / (best * 1e-3) / 1e9
 
 
-def cpu_sample(jobs, budget_s: float):
+def cpu_sample(mix, budget_s: float):
     """The oracle's CPU kernels on all host threads over a bounded sample of
-    the mix (jobs in mix order until the time budget is spent)."""
+    the mix (jobs in mix order until the time budget is spent).  Returns
+    (jobs/s, [(mix index, oracle output)], seconds)."""
     from oracle import kernels as K
 
     t0 = time.perf_counter()
-    n = 0
-    names = []
-    for mj in jobs:
+    outs = []
+    for i, mj in enumerate(mix):
         j = mj.job
-        K.run(j.kind, n=j.n, iters=j.iters, m=j.m, seed=j.seed)
-        n += 1
-        names.append(mj.template)
+        outs.append((i, K.run(j.kind, n=j.n, iters=j.iters, m=j.m, seed=j.seed)))
         if time.perf_counter() - t0 > budget_s:
             break
     dt = time.perf_counter() - t0
-    return n / dt, n, names, dt
+    return len(outs) / dt, outs, dt
 
 
-def reference_arm(args, jobs):
+def parity_check(W, mix, step_records, outs, device):
+    """GPU outputs of the co-located jobs of the last timed step vs the
+    oracle outputs the CPU leg computed for the same jobs."""
+    import numpy as np
+
+    from oracle import kernels as K
+
+    checked, bad, kinds = 0, [], set()
+    for i, want in outs:
+        j = mix[i].job
+        rec = step_records[i]
+        if rec["state"] != "done":
+            bad.append(f"{mix[i].job_id} not done")
+            continue
+        kinds.add(j.kind)
+        checked += 1
+        if j.kind in EXACT_KINDS:
+            if rec["checksum"] != K.digest(j.kind, want):
+                bad.append(f"{mix[i].job_id} {j.kind}: digest differs from the oracle")
+        else:  # float kinds: the co-located digest equals the solo run's, whose output is within 1e-5
+            got, srec = W.run_solo(j, device)
+            if srec.checksum != rec["checksum"]:
+                bad.append(f"{mix[i].job_id} {j.kind}: co-located digest differs from solo")
+            elif not np.allclose(got, want, rtol=1e-5, atol=1e-5):
+                bad.append(f"{mix[i].job_id} {j.kind}: solo output beyond 1e-5 of the oracle")
+    return {"checked": checked, "mismatches": len(bad), "kinds": sorted(kinds), "detail": bad[:4],
+            "bar": "bit-exact digest (bfs/hotspot/srad/kmeans/needle); lud/backprop: co-located digest == solo, "
+                   "solo within 1e-5 rel of the oracle"}
+
+
+def reference_arm(args, mix):
     """--impl reference: the reference's path on host cores (C port)."""
     from oracle import oracle as O
     from paper_2107_08538_b200 import _native as nat
@@ -248,26 +314,30 @@ def reference_arm(args, jobs):
     sample_desc = ""
     spec = device_spec("b200")
     for step in range(args.warmup + args.steps):
-        # placement of the whole mix on the CPU scheduler port (B200
+        # placement of the whole fleet mix on the CPU scheduler port (B200
         # ledgers), then the kernels of a bounded sample on all threads
         t0 = time.perf_counter()
         devs = [O.OracleDevice(spec, i) for i in range(max(1, args.gpus))]
         sched = O.OracleScheduler(devs, 3, 6, True)
-        for i, mj in enumerate(jobs):
+        for i, mj in enumerate(mix):
             pr = nat.GsProbe(host_footprint(mj.job), 8 << 20, 296 * 8, 0.0, 296, 8, 256, 0, 0, i, i, 0)
             sched.submit(pr)
-        rate, n, names, dt = cpu_sample(jobs[step % len(jobs):] + jobs[:step % len(jobs)], args.cpu_budget)
+        k = step % len(mix)
+        rate, outs, dt = cpu_sample(mix[k:] + mix[:k], args.cpu_budget)
         total = time.perf_counter() - t0
         if step >= args.warmup:
-            values.append(n / total)
-            sample_desc = f"{n} of {len(jobs)} mix jobs per step ({', '.join(names)}) + placement of all {len(jobs)}"
+            values.append(len(outs) / total)
+            names = [(mix[k:] + mix[:k])[i].template for i, _ in outs]
+            sample_desc = (f"{len(outs)} of {len(mix)} mix jobs per step ({', '.join(names)}) "
+                           f"+ placement of all {len(mix)}")
     v = statistics.fmean(values)
     line = {
         "metric": METRIC, "value": round(v, 4), "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(1000.0 / v, 1) if v else None, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f32/i32", "data": "synthetic",
         "impl": "reference",
-        "config": {"workload": f"cfg1: {len(jobs)}-job Rodinia mix {args.mix} (bounded CPU sample)",
+        "config": {"workload": f"cfg1: {args.jobs}-job Rodinia mix {args.mix} per GPU x {args.gpus} "
+                               "(bounded CPU sample)",
                    "policy": "mgb-warps (C port of schedulers.py)", "cpu_threads": threads},
         "cpu_baseline": {"value": round(v, 4), "unit": UNIT, "cores": threads, "kind": "port",
                          "sample": sample_desc},
@@ -276,92 +346,61 @@ def reference_arm(args, jobs):
     print(json.dumps(line), flush=True)
 
 
-def main() -> int:
-    ap = argparse.ArgumentParser()
-    ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=3)
-    ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--policy", default="mgb-warps")
-    ap.add_argument("--mix", default="3:1")
-    ap.add_argument("--jobs", type=int, default=32)
-    ap.add_argument("--workers", type=int, default=8)
-    ap.add_argument("--cpu-budget", type=float, default=12.0)
-    ap.add_argument("--skip-e2e", action="store_true")
-    ap.add_argument("--skip-sa", action="store_true")
-    args = ap.parse_args()
+def drive(args, devices, torch, barrier):
+    """The fleet driver (rank 0): every measurement of the bench line."""
+    from oracle import oracle as O
     from paper_2107_08538_b200 import catalog as C
-    from paper_2107_08538_b200.multi import dist_env, max_over_ranks, rank_mix, whole_job_rate
-
-    rank, world, local = dist_env()
-
-    if args.impl == "reference":
-        if rank != 0:
-            return 0
-        reference_arm(args, C.gen_mix(args.mix, args.jobs, seed=1))
-        return 0
-
-    import torch
-
-    torch.cuda.set_device(local)
-    dist = None
-    if world > 1:
-        import torch.distributed as dist
-
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-
     from paper_2107_08538_b200 import workloads as W
+    from paper_2107_08538_b200.multi import fleet_mix, rate
 
     pk = peaks()
-    mix = rank_mix(args.mix, args.jobs, rank)
+    mix = fleet_mix(args.mix, args.jobs, len(devices))
     jobs = [m.job for m in mix]
-    device = local
+    workers = args.workers * len(devices)
 
     # ---- device mode: inputs staged in HBM before the timed region ----
-    log(f"staging {len(jobs)} jobs (device mode)")
-    W.stage(jobs, [device], W.MODE_DEVICE)
-    if dist:
-        dist.barrier()
-    with Clocks(device) as clk:
-        times, results = run_steps(W, jobs, args.policy, device, args.workers, W.MODE_DEVICE, args.steps,
-                                   args.warmup, torch, dist)
+    log(f"staging {len(jobs)} jobs over {len(devices)} GPU(s) (device mode)")
+    W.stage(jobs, devices, W.MODE_DEVICE)
+    cap = min(W.ledger_capacity(d) for d in devices)  # what the staged inputs leave
+    with Clocks(devices) as clk:
+        times, results, xlog = run_steps(W, jobs, args.policy, devices, workers, W.MODE_DEVICE, args.steps,
+                                         args.warmup, torch, barrier, cap, keep_log=True)
     ours = summarize(results, times)
+    last_records = results[-1].records
     sa = None
     if not args.skip_sa:
-        st, sr = run_steps(W, jobs, "sa", device, args.workers, W.MODE_DEVICE, args.steps, 1, torch, dist)
+        st, sr, _ = run_steps(W, jobs, "sa", devices, workers, W.MODE_DEVICE, args.steps, 1, torch, barrier, cap)
         sa = summarize(sr, st)
     W.unstage()
-    kern, solo_ms = kernel_rooflines(W, C, mix, device, pk)
+    fp32 = W.fp32_peak_tflops(devices[0])
+    kern, solo_ms = kernel_rooflines(W, C, mix, devices[0], pk, fp32)
 
     # ---- e2e mode: pinned host inputs, H2D + D2H inside the timed region ----
     e2e = sa_e2e = None
     if not args.skip_e2e:
         log("staging (e2e mode: pinned host inputs)")
-        W.stage(jobs, [device], W.MODE_E2E)
-        et, er = run_steps(W, jobs, args.policy, device, args.workers, W.MODE_E2E, args.steps, 1, torch, dist)
+        W.stage(jobs, devices, W.MODE_E2E)
+        cap_e = min(W.ledger_capacity(d) for d in devices)
+        et, er, _ = run_steps(W, jobs, args.policy, devices, workers, W.MODE_E2E, args.steps, 1, torch, barrier,
+                              cap_e)
         e2e = summarize(er, et)
         e2e["h2d"] = sum(r["h2d_bytes"] for r in er[-1].records)
         e2e["d2h"] = sum(r["d2h_bytes"] for r in er[-1].records)
         if not args.skip_sa:
-            st2, sr2 = run_steps(W, jobs, "sa", device, args.workers, W.MODE_E2E, args.steps, 1, torch, dist)
+            st2, sr2, _ = run_steps(W, jobs, "sa", devices, workers, W.MODE_E2E, args.steps, 1, torch, barrier,
+                                    cap_e)
             sa_e2e = summarize(sr2, st2)
         W.unstage()
 
-    # ---- max over ranks ----
-    ms_step = ours["ms_per_step"]
-    e2e_ms = e2e["ms_per_step"] if e2e else None
-    ms_step, e2e_max, sa_max, sa_e2e_max = max_over_ranks(
-        [ms_step, e2e_ms or 0.0, sa["ms_per_step"] if sa else 0.0, sa_e2e["ms_per_step"] if sa_e2e else 0.0],
-        dist, device="cuda")
-    e2e_ms = e2e_max or None
-    if sa:
-        sa["ms_per_step"] = sa_max
-    if sa_e2e:
-        sa_e2e["ms_per_step"] = sa_e2e_max
-    n_total = len(jobs) * world
-    value = whole_job_rate(len(jobs), world, ms_step)
+    # ---- CPU leg: oracle on a bounded sample = cpu_baseline + parity ----
+    cpu_rate, outs, cpu_dt = cpu_sample(mix, args.cpu_budget)
+    parity = parity_check(W, mix, last_records, outs, devices[0])
+    n_dec, bad = O.replay_exec_log(xlog)
+    placements = {"decisions": n_dec, "mismatches": len(bad), "detail": bad[:3],
+                  "events": len(xlog.events), "ledgers": len(xlog.specs),
+                  "checked_against": "oracle/gs_oracle.c (golden-pinned restatement of schedulers.py)"}
 
-    # dominant kernel: the kind with the largest share of device time in the mix
+    value = rate(ours["completed_per_step"], ours["ms_per_step"])
     # dominant kind: the largest share of the mix's solo device time
     share = {}
     for mj in mix:
@@ -374,57 +413,123 @@ def main() -> int:
             "traffic_kernel": tr.get("kernel"), "algorithmic_bytes_per_launch": tr.get("algorithmic_bytes_per_launch"),
             "share_of_mix_solo_device_time": round(share[dom] / sum(share.values()), 3),
             "peak_source": "MEASURED_PEAKS.json hbm_gbs (burst copy)" if kd["bound"] == "hbm"
-            else "nominal FP32 (148 SMs x 128 FMA x 1.965 GHz)"}
+            else kd.get("peak_source", "MEASURED_PEAKS.json bf16_tflops")}
+    for k in ("survey_8d_bytes", "frac_survey_8d"):
+        if k in kd:
+            roof[k] = kd[k]
     # aggregate HBM roofline fraction of the whole mix
     mix_bytes = sum(C.algorithmic_work(j)[0] for j in jobs if C.algorithmic_work(j)[1] == "B")
-    mix_frac = mix_bytes / (ms_step / 1000.0) / 1e9 / pk["hbm_gbs"]
+    mix_frac = mix_bytes / (ours["ms_per_step"] / 1000.0) / 1e9 / (pk["hbm_gbs"] * len(devices))
 
     line = {
-        "metric": METRIC, "value": round(value, 4), "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": round(ms_step, 2), "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f32/i32", "data": "synthetic (seeded hash inputs)",
+        "metric": METRIC, "value": round(value, 4), "unit": UNIT, "n_gpus": len(devices), "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(ours["ms_per_step"], 2), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32/i32", "data": "synthetic (seeded hash inputs)",
         "config": {"workload": f"cfg1: {args.jobs}-job Rodinia mix {args.mix} per GPU "
-                               "(bfs/hotspot/srad/kmeans/backprop/needle/lud)",
-                   "policy": args.policy, "workers_per_gpu": args.workers,
-                   "inputs": "staged in HBM, larger than L2 (no flush needed)", "parallelism": f"placement x{world}"},
+                               f"(bfs/hotspot/srad/kmeans/backprop/needle/lud), {len(jobs)} jobs on "
+                               f"{len(devices)} GPU(s)",
+                   "policy": args.policy, "workers": workers,
+                   "decision_authority": f"one engine, {len(devices)} ledger(s) (rank 0 drives the fleet)",
+                   "ledger_bytes_per_gpu": cap,
+                   "inputs": "staged in HBM, larger than L2 (no flush needed)",
+                   "parallelism": f"placement over {len(devices)} GPU(s)"},
+        "jobs_submitted_per_step": ours["submitted_per_step"],
+        "jobs_completed_per_step": ours["completed_per_step"],
         "mean_turnaround_ms": round(ours["mean_turnaround_ms"], 2),
-        "mean_wait_ms": round(ours["mean_wait_ms"], 2),
-        "oom": ours["oom"], "crashed": ours["crashed"],
+        "mean_wait_ms": round(ours["mean_wait_ms"], 2), "max_wait_ms": round(ours["max_wait_ms"], 2),
+        "oom": ours["oom"], "crashed": ours["crashed"], "devices_used": ours["devices_used"],
         "gpu_launches": ours["kernel_launches"] + ours["decision_launches"],
         "decision_launches": ours["decision_launches"],
         "decision_ms_per_step": round(ours["decision_ms"] / args.steps, 3),
         "roofline": roof,
         "mix_hbm_frac": round(mix_frac, 4),
+        "parity": parity,
+        "placements": placements,
         "kernels": kern,
+        "fp32_peak_tflops_measured": round(fp32, 1),
     }
     if sa:
-        sa_value = n_total / (sa["ms_per_step"] / 1000.0)
+        sa_value = rate(sa["completed_per_step"], sa["ms_per_step"])
         line["sa"] = {"value": round(sa_value, 4), "ms_per_step": round(sa["ms_per_step"], 2),
-                      "mean_turnaround_ms": round(sa["mean_turnaround_ms"], 2), "oom": sa["oom"]}
+                      "mean_turnaround_ms": round(sa["mean_turnaround_ms"], 2), "oom": sa["oom"],
+                      "completed_per_step": sa["completed_per_step"]}
         line["speedup_vs_sa"] = round(value / sa_value, 3)
         line["turnaround_speedup_vs_sa"] = round(sa["mean_turnaround_ms"] / max(ours["mean_turnaround_ms"], 1e-9), 3)
     if e2e:
         pcie = pcie_h2d_gbps(torch)
+        e2e_ms = e2e["ms_per_step"]
         h2d_rate = e2e["h2d"] / (e2e_ms / 1000.0) / 1e9
-        line["e2e"] = {"value": round(n_total / (e2e_ms / 1000.0), 4), "unit": UNIT,
+        line["e2e"] = {"value": round(rate(e2e["completed_per_step"], e2e_ms), 4), "unit": UNIT,
                        "h2d_bytes_per_step": e2e["h2d"], "d2h_bytes_per_step": e2e["d2h"],
+                       "ms_per_step": round(e2e_ms, 2),
                        "mean_turnaround_ms": round(e2e["mean_turnaround_ms"], 2), "oom": e2e["oom"],
-                       "pcie_h2d_achieved_GBps": round(h2d_rate, 1), "pcie_h2d_peak_GBps": round(pcie, 1),
-                       "pcie_h2d_frac": round(h2d_rate / pcie, 3)}
+                       "pcie_h2d_achieved_GBps": round(h2d_rate, 1), "pcie_h2d_peak_GBps_per_gpu": round(pcie, 1),
+                       "pcie_h2d_frac": round(h2d_rate / (pcie * len(devices)), 3)}
         if sa_e2e:
-            sv = n_total / (sa_e2e["ms_per_step"] / 1000.0)
+            sv = rate(sa_e2e["completed_per_step"], sa_e2e["ms_per_step"])
             line["e2e"]["sa_value"] = round(sv, 4)
             line["e2e"]["speedup_vs_sa"] = round(line["e2e"]["value"] / sv, 3)
     line["clocks"] = clk.summary()
+    names = [mix[i].template for i, _ in outs]
+    line["cpu_baseline"] = {"value": round(cpu_rate, 4), "unit": UNIT, "cores": os.cpu_count() or 1,
+                            "kind": "port",
+                            "sample": f"{len(outs)} mix jobs ({', '.join(names)}) on the CPU restatements, "
+                                      f"{cpu_dt:.1f} s, OpenMP all host threads"}
+    return line
+
+
+def main() -> int:
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--policy", default="mgb-warps")
+    ap.add_argument("--mix", default="3:1")
+    ap.add_argument("--jobs", type=int, default=32, help="jobs per GPU")
+    ap.add_argument("--workers", type=int, default=8, help="workers per GPU")
+    ap.add_argument("--cpu-budget", type=float, default=12.0)
+    ap.add_argument("--skip-e2e", action="store_true")
+    ap.add_argument("--skip-sa", action="store_true")
+    args = ap.parse_args()
+    from paper_2107_08538_b200.multi import dist_env, fleet_mix, fleet_plan, max_over_ranks
+
+    rank, world, local = dist_env()
+    driver, devices = fleet_plan(args.gpus, world, rank)
+
+    if args.impl == "reference":
+        if rank != 0:
+            return 0
+        reference_arm(args, fleet_mix(args.mix, args.jobs, args.gpus))
+        return 0
+
+    import torch
+
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local),
+                                timeout=datetime.timedelta(hours=2))
+    barrier = Barrier(dist)
+    line = None
+    if driver:
+        line = drive(args, devices, torch, barrier)
+        ms = [line["ms_per_step"], line.get("e2e", {}).get("ms_per_step", 0.0)]
+    else:
+        # idle rank: mirror the driver's barrier pairs (one per timed phase)
+        phases = 1 + (0 if args.skip_sa else 1) + (0 if args.skip_e2e else 1 + (0 if args.skip_sa else 1))
+        for _ in range(phases):
+            barrier()
+            barrier()
+        ms = [0.0, 0.0]
+    ms = max_over_ranks(ms, dist, device="cuda")
     if rank == 0:
-        rate, n, names, dt = cpu_sample(mix, args.cpu_budget)
-        line["cpu_baseline"] = {"value": round(rate, 4), "unit": UNIT, "cores": os.cpu_count() or 1,
-                                "kind": "port",
-                                "sample": f"{n} mix jobs ({', '.join(names)}) on the CPU restatements, "
-                                          f"{dt:.1f} s, OpenMP all host threads"}
+        line["ms_per_step"] = round(ms[0], 2)  # max over ranks (idle ranks report 0)
         print(json.dumps(line), flush=True)
     if dist:
-        dist.barrier()
+        barrier()
         dist.destroy_process_group()
     return 0
 

@@ -238,7 +238,10 @@ int64_t gs_engine_decisions(gs_engine *eng);
  * event log: for every ASSIGN/DEFER/REJECT of a submit and every admit of a
  * drain, (kind, handle, device) with kind 0 submit-assign, 1 submit-defer,
  * 2 submit-reject, 3 drain-admit.  Returns the number of log entries in
- * *n_events and the kernel-only time in *kernel_ms. */
+ * *n_events and the kernel-only time in *kernel_ms.  The tasks still
+ * resident at the end keep their ledger reservations, so a sweep consumes
+ * the scheduler: later gs_submit / gs_submit_batch / gs_sweep calls on it
+ * return GS_ERR_CONTRACT. */
 int gs_sweep(gs_sched *s, const gs_probe *probes, int32_t n, int32_t max_resident,
              int32_t *events, int64_t events_cap, int64_t *n_events, float *kernel_ms);
 

@@ -134,8 +134,6 @@ int gs_exec_run_arrivals(const gs_job_desc *jobs, int32_t n_jobs, const double *
                          int32_t cg_ratio, const int32_t *cuda_devices, int32_t n_devices, int32_t workers,
                          int32_t mode, int64_t ledger_bytes, gs_job_record *records, gs_exec_stats *stats);
 
-/* Prepare (generate) the inputs of a job list ahead of gs_exec_run so the
- * timed region starts with inputs resident (device) or pinned (e2e). */
 /* Darknet layer GEMM on tcgen05 (csrc/gs_gemm.cu): D = act(A . B^T + bias)
  * with A [m x k] and B [n x k] bf16 row-major (K contiguous, k % 8 == 0),
  * bias fp32 [n] or NULL, D [m x n] bf16 or fp32 (out_f32) with row pitch ldo,
@@ -143,9 +141,41 @@ int gs_exec_run_arrivals(const gs_job_desc *jobs, int32_t n_jobs, const double *
 int gs_gemm_bf16(const void *A, int64_t lda, const void *B, int64_t ldb, const float *bias, void *out,
                  int64_t ldo, int32_t m, int32_t n, int32_t k, int32_t out_f32, int32_t act, void *stream);
 
+/* Prepare (generate) the inputs of a job list ahead of gs_exec_run so the
+ * timed region starts with inputs resident (device) or pinned (e2e). */
 int gs_exec_stage(const gs_job_desc *jobs, int32_t n_jobs, const int32_t *cuda_devices, int32_t n_devices,
                   int32_t mode);
 void gs_exec_unstage(void);
+
+/* Measured FP32 FMA throughput of `cuda_device` in TFLOP/s (8 independent
+ * FFMA chains per thread, 8 x 256-thread blocks per SM): the roofline
+ * denominator of the FP32 CUDA-core kernels (lud). */
+int gs_measure_fp32_peak(int32_t cuda_device, double *tflops);
+
+/* ---- placement log of the most recent executor run ---------------------
+ * Every call the run made into the decision engine, in the order the single
+ * decision authority serialized them (the linearization SPEC.md:419 asks
+ * for), so the run's placements can be replayed through the reference
+ * Scheduler semantics (schedulers.py:89-123) and checked decision for
+ * decision.  Job j's probe / task handle is j. */
+#define GS_EV_SUBMIT 0     /* submit(probe): outcome + device decided */
+#define GS_EV_RELEASE 1    /* DeviceState.release_task(handle) on ledger `device` (+ on_release) */
+#define GS_EV_JOB_ENDED 2  /* Scheduler.job_ended(handle) (+ on_release): sa / cg */
+#define GS_EV_DRAIN 3      /* one decision of the re-drive that followed (FIFO order) */
+typedef struct gs_exec_event {
+    int32_t kind;
+    int32_t handle;
+    int32_t device;      /* ledger index (-1 none) */
+    int32_t outcome;     /* GS_ASSIGN / GS_DEFER / GS_REJECTED, or a status code < 0 */
+    int64_t freed;       /* GS_EV_RELEASE: bytes release_task returned */
+    double t_ms;         /* wall time since the run started */
+    gs_probe probe;      /* GS_EV_SUBMIT: the probe as submitted */
+} gs_exec_event;
+/* Copies up to `cap` events of the last run (returns the full count in
+ * *n_events), the per-ledger specs the run used (up to spec_cap; count in
+ * *n_devices), and its policy.  Any pointer may be NULL. */
+int gs_exec_log(gs_exec_event *events, int64_t cap, int64_t *n_events, gs_spec *specs, int32_t spec_cap,
+                int32_t *n_devices, int32_t *policy, int32_t *cg_ratio);
 
 #ifdef __cplusplus
 }

@@ -106,3 +106,22 @@ def run(kind, n, iters=1, m=0, seed=1):
     if kind == "lud":
         return lud(n, seed)
     raise ValueError(kind)
+
+
+_C = 0x9E3779B1
+_M64 = (1 << 64) - 1
+
+
+def digest(kind, out):
+    """The executor's order-independent output digest (gs_kernels.cuh
+    checksum_words: C * sum of the 32-bit words + n(n-1)/2 mod 2^64) of an
+    oracle output, laid out like the job's device buffer (needle: pitch
+    n + 4 with three leading zero columns, which add no word value)."""
+    a = np.ascontiguousarray(out)
+    words = a.view(np.uint32).ravel()
+    s = int(words.sum(dtype=np.uint64))
+    nwords = words.size
+    if kind == "needle":
+        n1 = a.shape[0]
+        nwords = n1 * (n1 + 3)
+    return (_C * s + nwords * (nwords - 1) // 2) & _M64

@@ -146,3 +146,61 @@ class OracleScheduler:
         ne = c_int64()
         self.L.o_sweep(self.ptr, probes.ctypes.data, n, max_resident, ev.ctypes.data, cap, ctypes.byref(ne))
         return ev[: ne.value]
+
+
+class _Spec:
+    def __init__(self, s):
+        for f in ("sm_count", "mem_bytes", "max_warps_per_sm", "max_tbs_per_sm", "regs_per_sm",
+                  "smem_per_sm_bytes"):
+            setattr(self, f, int(getattr(s, f)))
+
+
+def replay_exec_log(log) -> tuple[int, list[str]]:
+    """Replay an executor placement log (workloads.exec_log()) through the
+    oracle Scheduler (the golden-pinned C restatement of schedulers.py:89-123
+    and device_model.py:192-209) and compare every decision: submits
+    (outcome, device), releases (status, freed bytes) and each re-drive's
+    tried list (handle, outcome, device) in FIFO order.  Returns (decisions
+    checked, mismatch descriptions)."""
+    devs = [OracleDevice(_Spec(s), i) for i, s in enumerate(log.specs)]
+    sched = OracleScheduler(devs, log.policy, log.cg_ratio, True)
+    L = lib()
+    evs = log.events
+    checked, bad = 0, []
+    i = 0
+    while i < len(evs):
+        e = evs[i]
+        if e.kind == 0:  # submit
+            d = sched.submit(e.probe)
+            got = (e.outcome, e.device if e.outcome == 0 else -1)
+            want = (d.outcome, d.device if d.outcome == 0 else -1)
+            checked += 1
+            if got != want:
+                bad.append(f"event {i} submit h{e.handle}: gpu {got} oracle {want}")
+            i += 1
+            continue
+        if e.kind in (1, 2):
+            if e.kind == 1:
+                freed = c_int64()
+                st = L.o_release(devs[e.device].ptr, e.handle, ctypes.byref(freed))
+                checked += 1
+                if (st, freed.value) != (e.outcome, e.freed):
+                    bad.append(f"event {i} release h{e.handle}: gpu {(e.outcome, e.freed)} oracle {(st, freed.value)}")
+            else:
+                L.o_job_ended(sched.ptr, e.handle)
+            drained = sched.on_release()
+            j = i + 1
+            got = []
+            while j < len(evs) and evs[j].kind == 3:
+                got.append((evs[j].handle, evs[j].outcome, evs[j].device if evs[j].outcome == 0 else -1))
+                j += 1
+            want = [(int(r["handle"]), int(r["outcome"]), int(r["device"]) if r["outcome"] == 0 else -1)
+                    for r in drained]
+            checked += len(want)
+            if got != want:
+                bad.append(f"event {i} re-drive after h{e.handle}: gpu {got} oracle {want}")
+            i = j
+            continue
+        bad.append(f"event {i}: unexpected kind {e.kind}")
+        i += 1
+    return checked, bad

@@ -6,6 +6,11 @@ small and a large size class (the reference's 1-4 GiB / 4-13 GiB classes,
 catalog.json:3).  `gen_mix` follows gpushare/workload_gen.py:177-214: larges
 rounded up, picks drawn from random.Random(f"{seed}|{mix}|{n}"), then
 shuffled, job ids j00..jNN.
+
+Jobs of one template are identical instances, as in the reference (a
+template is one fixed program: footprint, kernels, duration): their
+synthetic inputs come from a per-template data seed, so a mix needs one
+staged copy of each template's inputs, not one per job.
 """
 
 from __future__ import annotations
@@ -67,8 +72,13 @@ def gen_mix(mix: str = "3:1", n: int = 32, seed: int = 1, kinds: tuple[str, ...]
     for i, (kind, cls) in enumerate(picks):
         kw = RODINIA[kind][0 if cls == "small" else 1]
         out.append(MixJob(f"j{i:0{width}d}", f"{kind}_{cls}", cls,
-                          Job(kind, seed=seed * 1000 + i, **kw)))
+                          Job(kind, seed=template_seed(seed, kind, cls), **kw)))
     return out
+
+
+def template_seed(seed: int, kind: str, cls: str) -> int:
+    """Data seed of a template's instances in mix `seed`."""
+    return seed * 1000 + 2 * list(RODINIA).index(kind) + (cls == "large")
 
 
 def cfg0_mix(seed: int = 1) -> list[MixJob]:
@@ -176,6 +186,21 @@ def host_footprint(job: Job) -> int:
         "resnet": resnet_buffers(n, m) if job.kind == "resnet" else [],
     }[job.kind]
     return (8 << 20) + sum((s + g - 1) // g * g for s in sizes)
+
+
+def survey_bytes(job: Job) -> float:
+    """SURVEY.md §8(d)'s per-unit byte counts as written (per iteration of
+    the unfused Rodinia kernels): hotspot 12·N² per step, srad 24·N² per
+    iteration, needle 8·N².  The executed algorithms move less (two hotspot
+    steps per pass, srad's fused coefficient/update): algorithmic_work."""
+    n, it = job.n, max(job.iters, 1)
+    if job.kind == "hotspot":
+        return 12.0 * n * n * it
+    if job.kind == "srad":
+        return 24.0 * n * n * it
+    if job.kind == "needle":
+        return 8.0 * n * n
+    return algorithmic_work(job)[0]
 
 
 def algorithmic_work(job: Job) -> tuple[float, str]:

@@ -65,6 +65,13 @@ struct Staged {
 std::mutex g_stage_mu;
 std::vector<Staged> g_staged;
 
+// Placement log of the most recent run (gs_exec_log): every decision-engine
+// call in the order the single decision authority made it.
+std::mutex g_log_mu;
+std::vector<gs_exec_event> g_log;
+std::vector<gs_spec> g_log_specs;
+int32_t g_log_policy = 0, g_log_cg_ratio = 0;
+
 void free_staged(Staged &s) {
   for (void *p : s.ptr) {
     if (!p) continue;
@@ -87,10 +94,23 @@ int64_t e2e_out_bytes(const gs_job_desc &j) {
 
 bool same_desc(const gs_job_desc &a, const gs_job_desc &b) { return memcmp(&a, &b, sizeof(a)) == 0; }
 
-const Staged *find_staged(const gs_job_desc &d) {
+// The staged inputs of job `d` for a run on `device`: that device's own
+// copy first (device mode stages one per fleet GPU), else a pinned host copy
+// (e2e), else any device's copy (pulled over NVLink by a peer copy).
+const Staged *find_staged(const gs_job_desc &d, int device = -1) {
+  const Staged *any = nullptr;
+  for (const Staged &s : g_staged) {
+    if (!same_desc(s.desc, d)) continue;
+    if (s.host || s.device == device) return &s;
+    if (!any) any = &s;
+  }
+  return any;
+}
+
+bool staged_on(const gs_job_desc &d, int device, bool host) {
   for (const Staged &s : g_staged)
-    if (same_desc(s.desc, d)) return &s;
-  return nullptr;
+    if (same_desc(s.desc, d) && s.host == host && (host || s.device == device)) return true;
+  return false;
 }
 
 int stage_one(const gs_job_desc &j, int device, int mode, Staged &out) {
@@ -280,18 +300,38 @@ extern "C" {
 int gs_exec_stage(const gs_job_desc *jobs, int32_t n_jobs, const int32_t *cuda_devices, int32_t n_devices,
                   int32_t mode) {
   std::lock_guard<std::mutex> g(g_stage_mu);
+  // Identical jobs (same descriptor: a template's instances) share one
+  // staged copy: device mode stages a copy on EVERY listed device (a job
+  // reads its inputs from the GPU it was placed on), e2e mode one pinned
+  // host copy (portable: any device's copy engine reads it).
+  const bool host = mode == GS_MODE_E2E;
   for (int i = 0; i < n_jobs; ++i) {
     int rc = validate(jobs[i]);
     if (rc) return rc;
-    if (find_staged(jobs[i])) continue;
-    Staged s;
-    rc = stage_one(jobs[i], cuda_devices[i % n_devices], mode, s);
-    if (rc) {
-      free_staged(s);
-      return rc;
+    for (int d = 0; d < (host ? 1 : n_devices); ++d) {
+      if (staged_on(jobs[i], cuda_devices[d], host)) continue;
+      Staged s;
+      rc = stage_one(jobs[i], cuda_devices[d], mode, s);
+      if (rc) {
+        free_staged(s);
+        return rc;
+      }
+      g_staged.push_back(std::move(s));
     }
-    g_staged.push_back(std::move(s));
   }
+  return GS_OK;
+}
+
+int gs_exec_log(gs_exec_event *events, int64_t cap, int64_t *n_events, gs_spec *specs, int32_t spec_cap,
+                int32_t *n_devices, int32_t *policy, int32_t *cg_ratio) {
+  std::lock_guard<std::mutex> g(g_log_mu);
+  if (n_events) *n_events = (int64_t)g_log.size();
+  if (events && cap > 0) memcpy(events, g_log.data(), sizeof(gs_exec_event) * std::min<int64_t>(cap, g_log.size()));
+  if (n_devices) *n_devices = (int32_t)g_log_specs.size();
+  if (specs && spec_cap > 0)
+    memcpy(specs, g_log_specs.data(), sizeof(gs_spec) * std::min<size_t>(spec_cap, g_log_specs.size()));
+  if (policy) *policy = g_log_policy;
+  if (cg_ratio) *cg_ratio = g_log_cg_ratio;
   return GS_OK;
 }
 
@@ -365,7 +405,7 @@ int gs_job_run_solo(const gs_job_desc *job, int cuda_device, int mode, void *hos
   const Staged *stg = nullptr;
   {
     std::lock_guard<std::mutex> g(g_stage_mu);
-    stg = find_staged(*job);
+    stg = find_staged(*job, cuda_device);
   }
   bool oom = false;
   {
@@ -411,6 +451,7 @@ int gs_exec_run_arrivals(const gs_job_desc *jobs, int32_t n_jobs, const double *
   if (rc) return err(rc, gs_last_error());
   phase("engine open");
   std::vector<gs_device *> ledgers(n_devices, nullptr);
+  std::vector<gs_spec> specs(n_devices);
   for (int d = 0; d < n_devices; ++d) {
     const cudaDeviceProp &prop = gscache::device_props(cuda_devices[d]);
     CUE(cudaSetDevice(cuda_devices[d]));
@@ -436,6 +477,7 @@ int gs_exec_run_arrivals(const gs_job_desc *jobs, int32_t n_jobs, const double *
     spec.smem_per_sm_bytes = (int64_t)prop.sharedMemPerMultiprocessor;
     rc = gs_device_create(eng, &spec, d, &ledgers[d]);
     if (rc) return err(rc, gs_last_error());
+    specs[d] = spec;
     phase("ledger created");
     // at most `workers` jobs hold memory at once: the pool needs the sum of
     // the largest `workers` footprints, capped by the ledger
@@ -474,6 +516,23 @@ int gs_exec_run_arrivals(const gs_job_desc *jobs, int32_t n_jobs, const double *
   }
 
   memset(records, 0, sizeof(gs_job_record) * n_jobs);
+  // the placement log (caller holds mu while appending: the log order is
+  // the decision authority's linearization order)
+  std::vector<gs_exec_event> log;
+  log.reserve((size_t)n_jobs * 4 + 16);
+  auto log_ev = [&](int32_t kind, int32_t handle, int32_t device, int32_t outcome, int64_t freed,
+                    const gs_probe *pr) {
+    gs_exec_event e;
+    memset(&e, 0, sizeof e);
+    e.kind = kind;
+    e.handle = handle;
+    e.device = device;
+    e.outcome = outcome;
+    e.freed = freed;
+    e.t_ms = 0;
+    if (pr) e.probe = *pr;
+    log.push_back(e);
+  };
   std::vector<int> admitted(n_jobs, -1);
   std::vector<gs_decision> drain(n_jobs + 1);
   std::mutex mu;
@@ -489,13 +548,16 @@ int gs_exec_run_arrivals(const gs_job_desc *jobs, int32_t n_jobs, const double *
   if (mode == GS_MODE_E2E) {
     std::lock_guard<std::mutex> g(g_stage_mu);
     for (int i = 0; i < n_jobs; ++i)
-      if (!find_staged(jobs[i])) out_cap = std::max(out_cap, max_out_bytes(jobs + i, 1));
+      if (!find_staged(jobs[i], -1)) out_cap = std::max(out_cap, max_out_bytes(jobs + i, 1));
   }
   const auto t0 = Clock::now();
 
   auto admit_drained = [&](int32_t tried, int32_t adm) {  // caller holds mu
-    for (int k = 0; k < tried; ++k)
+    for (int k = 0; k < tried; ++k) {
+      log_ev(GS_EV_DRAIN, drain[k].handle, drain[k].device, drain[k].outcome, 0, nullptr);
+      log.back().t_ms = ms_since(t0);
       if (drain[k].outcome == GS_ASSIGN) admitted[drain[k].handle] = drain[k].device;
+    }
     if (adm) cv.notify_all();
   };
   auto redrive = [&]() {  // caller holds mu
@@ -564,6 +626,8 @@ int gs_exec_run_arrivals(const gs_job_desc *jobs, int32_t n_jobs, const double *
         const auto a = Clock::now();
         int r = gs_submit(sched, &pr, &dec);
         decision_ms += ms_since(a);
+        log_ev(GS_EV_SUBMIT, j, r < 0 ? -1 : dec.device, r < 0 ? r : dec.outcome, 0, &pr);
+        log.back().t_ms = ms_since(t0);
         if (r < 0) {
           if (!first_err) {
             first_err = r;
@@ -591,7 +655,7 @@ int gs_exec_run_arrivals(const gs_job_desc *jobs, int32_t n_jobs, const double *
       const Staged *stg = nullptr;
       {
         std::lock_guard<std::mutex> g(g_stage_mu);
-        stg = find_staged(jobs[j]);
+        stg = find_staged(jobs[j], cuda_devices[dev]);
       }
       bool oom = false;
       const bool chain = jobs[j].kind == GS_JOB_BFS || jobs[j].kind == GS_JOB_LUD || jobs[j].kind == GS_JOB_NEEDLE;
@@ -612,11 +676,22 @@ int gs_exec_run_arrivals(const gs_job_desc *jobs, int32_t n_jobs, const double *
         const auto a = Clock::now();
         const int rr = gs_release_redrive(sched, dev, j, &freed, drain.data(), (int32_t)drain.size(), &tried, &adm);
         decision_ms += ms_since(a);
-        if (rr >= 0) admit_drained(tried, adm);
+        log_ev(GS_EV_RELEASE, j, dev, rr, freed, nullptr);
+        log.back().t_ms = ms_since(t0);
+        // the re-drive runs even when the release itself fails (unknown
+        // task -> GS_ERR_CONTRACT after the drain): whatever it admitted
+        // must still wake its workers, and the failure must surface
+        if (tried > 0) admit_drained(tried, adm);
+        if (rr < 0 && !first_err) {
+          first_err = rr;
+          first_msg = gs_last_error();
+        }
       } else {
         const auto a = Clock::now();
         gs_job_ended(sched, j);
         decision_ms += ms_since(a);
+        log_ev(GS_EV_JOB_ENDED, j, dev, GS_OK, 0, nullptr);
+        log.back().t_ms = ms_since(t0);
         redrive();
       }
     }
@@ -657,6 +732,13 @@ int gs_exec_run_arrivals(const gs_job_desc *jobs, int32_t n_jobs, const double *
   gs_sched_ring_stop(sched);
   gs_sched_destroy(sched);
   phase("sched destroyed");
+  {
+    std::lock_guard<std::mutex> g(g_log_mu);
+    g_log.swap(log);
+    g_log_specs = specs;
+    g_log_policy = policy;
+    g_log_cg_ratio = cg_ratio;
+  }
   for (gs_device *d : ledgers) gs_device_destroy(d);
   phase("ledgers destroyed");
   gs_engine_close(eng);

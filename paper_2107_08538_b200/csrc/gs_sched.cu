@@ -1663,6 +1663,11 @@ struct gs_sched {
   // persistent decision kernel (command ring)
   Mapped<Ring> ring;
   bool ring_active = false;
+  // a sweep leaves up to max_resident tasks holding ledger capacity that no
+  // caller can release (their handles never left the kernel): the scheduler
+  // and its ledgers are spent afterwards and every further decision call is
+  // refused
+  bool swept = false;
   cudaStream_t ring_stream = nullptr;
   size_t ring_smem = 0;
   KParams ring_params{};
@@ -2172,6 +2177,7 @@ int gs_submit_batch(gs_sched *s, const gs_probe *reqs, int32_t n, gs_decision *o
   gs_engine *eng = s->eng;
   EngineLock g(eng);
   if (n <= 0) return GS_OK;
+  if (s->swept) return set_err(GS_ERR_CONTRACT, "scheduler already consumed by a sweep");
   int32_t maxh = -1, maxj = -1;
   for (int i = 0; i < n; ++i) {
     maxh = std::max(maxh, reqs[i].handle);
@@ -2393,21 +2399,30 @@ int gs_sweep(gs_sched *s, const gs_probe *probes, int32_t n, int32_t max_residen
   EngineLock g(eng);
   if (n <= 0) return GS_OK;
   if (s->ring_active) return set_err(GS_ERR_CONTRACT, "stop the decision ring before a sweep");
+  if (s->swept) return set_err(GS_ERR_CONTRACT, "scheduler already consumed by a sweep");
   if (s->st.h->pend_count != 0 || s->st.h->fifo_tail != s->st.h->fifo_head)
     return set_err(GS_ERR_CONTRACT, "sweep needs a fresh scheduler");
   int rc = gs_engine_reserve_handles(eng, n);
   if (!rc) rc = ensure_pending(s, n);
   if (!rc) rc = s->events.ensure(3 * (size_t)std::max<int64_t>(events_cap, 1), eng->stream, false);
   if (rc) return rc;
+  // every return path below gives back the probe copy and the events
   gs_probe *dprobes = nullptr;
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  struct Guard {
+    gs_probe *&p;
+    cudaEvent_t &a, &b;
+    ~Guard() {
+      if (p) cudaFree(p);
+      if (a) cudaEventDestroy(a);
+      if (b) cudaEventDestroy(b);
+    }
+  } guard{dprobes, e0, e1};
   CU(cudaMalloc((void **)&dprobes, sizeof(gs_probe) * n));
   CU(cudaMemcpyAsync(dprobes, probes, sizeof(gs_probe) * n, cudaMemcpyHostToDevice, eng->stream));
   Launch L;
   rc = sched_params(s, L);
-  if (rc) {
-    cudaFree(dprobes);
-    return rc;
-  }
+  if (rc) return rc;
   L.p.sweep = 1;
   L.p.sweep_probes = dprobes;
   {
@@ -2423,10 +2438,7 @@ int gs_sweep(gs_sched *s, const gs_probe *probes, int32_t n, int32_t max_residen
     L.p.fifo_stride = stride;
     const size_t room = (size_t)eng->max_smem > L.smem ? ((size_t)eng->max_smem - L.smem) / (stride * sizeof(int)) : 0;
     L.p.fifo_cap = (int32_t)std::min<size_t>((size_t)n + 1, room);
-    if (L.p.fifo_cap < 64) {
-      cudaFree(dprobes);
-      return set_err(GS_ERR_NOMEM, "no shared memory left for the resident FIFO");
-    }
+    if (L.p.fifo_cap < 64) return set_err(GS_ERR_NOMEM, "no shared memory left for the resident FIFO");
     L.smem += (size_t)L.p.fifo_cap * stride * sizeof(int);
   }
   L.p.n_cmds = n;
@@ -2436,7 +2448,8 @@ int gs_sweep(gs_sched *s, const gs_probe *probes, int32_t n, int32_t max_residen
   s->st.h->n_events = 0;
   s->st.h->error = 0;
   s->st.h->fifo_head = s->st.h->fifo_tail = 0;
-  cudaEvent_t e0, e1;
+  // from the launch on, the ledgers carry the sweep's residents
+  s->swept = true;
   CU(cudaEventCreate(&e0));
   CU(cudaEventCreate(&e1));
   CU(cudaEventRecord(e0, eng->stream));
@@ -2447,15 +2460,11 @@ int gs_sweep(gs_sched *s, const gs_probe *probes, int32_t n, int32_t max_residen
   eng->launches++;
   float ms = 0;
   CU(cudaEventElapsedTime(&ms, e0, e1));
-  cudaEventDestroy(e0);
-  cudaEventDestroy(e1);
   if (kernel_ms) *kernel_ms = ms;
   const int64_t ne = s->st.h->n_events;
   if (n_events) *n_events = ne;
   if (events)
     CU(cudaMemcpy(events, s->events.d, sizeof(int32_t) * 3 * std::min(ne, events_cap), cudaMemcpyDeviceToHost));
-  cudaFree(dprobes);
-  // the sweep's residents are bookkeeping of this run only
   s->st.h->fifo_head = s->st.h->fifo_tail = 0;
   if (s->st.h->error) return set_err(s->st.h->error, "sweep overflowed the resident FIFO");
   return GS_OK;

@@ -486,3 +486,50 @@ int digest(const void *p, int64_t bytes, unsigned long long *dsum, cudaStream_t 
 }
 
 }  // namespace gsw
+
+// ---- FP32 peak probe: the roofline denominator of lud (bench.py) ----------
+// Every thread runs 8 independent FFMA chains (enough ILP to hide the 4-cycle
+// FMA latency at 8 warps per scheduler), grid = 8 x 256-thread blocks per SM.
+namespace {
+__global__ void __launch_bounds__(256) fp32_peak_kernel(float *out, int iters, float b, float c) {
+  float a[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) a[k] = (float)(threadIdx.x + k);
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) a[k] = fmaf(a[k], b, c);
+  }
+  float s = 0;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) s += a[k];
+  if (s == 1234.5f) out[threadIdx.x] = s;  // keeps the chains live
+}
+}  // namespace
+
+extern "C" int gs_measure_fp32_peak(int32_t cuda_device, double *tflops) {
+  CUW(cudaSetDevice(cuda_device));
+  int sms = 0;
+  CUW(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, cuda_device));
+  float *out;
+  CUW(cudaMalloc(&out, 1024 * 4));
+  cudaEvent_t e0, e1;
+  CUW(cudaEventCreate(&e0));
+  CUW(cudaEventCreate(&e1));
+  const int blocks = 8 * sms, iters = 1 << 16;
+  float best = 1e30f;
+  for (int rep = 0; rep < 4; ++rep) {
+    CUW(cudaEventRecord(e0));
+    fp32_peak_kernel<<<blocks, 256>>>(out, iters, 0.999999f, 1e-7f);
+    CUW(cudaEventRecord(e1));
+    CUW(cudaEventSynchronize(e1));
+    float ms = 0;
+    CUW(cudaEventElapsedTime(&ms, e0, e1));
+    if (rep) best = std::min(best, ms);  // first launch is a warm-up
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaFree(out);
+  *tflops = 2.0 * 8.0 * iters * (double)blocks * 256 / (best * 1e-3) / 1e12;
+  return GS_OK;
+}
+

@@ -11,7 +11,7 @@ executor's probe capture records for real CUDA launches.
 from __future__ import annotations
 
 from dataclasses import dataclass
-from typing import Iterable, Mapping, Sequence
+from typing import Mapping
 
 from .errors import AnalysisError
 
@@ -52,27 +52,43 @@ def warps_per_block(threads_per_block: int) -> int:
     return -(-threads_per_block // WARP_SIZE)
 
 
-def compute_resource_request(
-    allocs: Mapping[str, int] | Iterable[tuple[str, int]],
-    launches: Sequence[LaunchShape],
-    heap_limit_bytes: int | None = None,
-) -> ResourceRequest:
+def compute_resource_request(allocs, launches, heap_limit_bytes: int | None = None) -> ResourceRequest:
     """Aggregate a task's footprint and widest launch (task_builder.py:258-290).
 
-    * mem = Σ bytes over distinct buffers + the device heap limit (8 MiB
-      default, counted once per task);
-    * the widest launch is the FIRST maximum of tbs·ceil(threads/32);
-      threads_per_block comes from it; regs and smem are maxima over all
-      launches; the duration estimate is the sum.
+    Two call forms:
+
+    * ``compute_resource_request(allocs, launches, heap_limit_bytes=None)``:
+      `allocs` are the task's allocation RECORDS, one per malloc call — a
+      ``{name: bytes}`` mapping or ``(key, bytes)`` pairs.  Every record
+      counts, as every distinct alloc op does in the reference
+      (task_builder.py:260-262): a symbol allocated twice is two records.
+      `launches` are LaunchShape (or objects with the same fields) in
+      program order.
+    * ``compute_resource_request(units, fn)`` — the reference's own
+      signature: `units` are the merged task's UnitTasks and `fn` the
+      inlined FunctionGraph (duck-typed: ``alloc_ops`` / ``heap_ops`` /
+      ``launch_op`` / ``order`` on the units, ``blocks[*].ops[*]`` with
+      ``op_id`` / ``bytes`` and the launch fields on `fn`).
+
+    Arithmetic: mem = Σ record bytes + the device heap limit (8 MiB default,
+    counted once per task); the widest launch is the FIRST maximum of
+    tbs·ceil(threads/32) and gives threads_per_block; regs and smem are
+    maxima over all launches; the duration estimate is the sum.
     """
+    if hasattr(launches, "blocks"):  # reference form (units, fn)
+        units, fn = allocs, launches
+        by_id = {op.op_id: op for blk in fn.blocks.values() for op in blk.ops}
+        alloc_ids = sorted({a for u in units for a in u.alloc_ops})
+        first = min(units, key=lambda u: u.order)
+        heap = by_id[next(iter(first.heap_ops))].bytes if first.heap_ops else None
+        records = [(a, by_id[a].bytes) for a in alloc_ids]
+        shapes = [by_id[u.launch_op] for u in units]
+        return compute_resource_request(records, shapes, heap)
     if not launches:
         raise AnalysisError("a task needs at least one launch")
     items = allocs.items() if isinstance(allocs, Mapping) else allocs
-    seen: dict[str, int] = {}
-    for name, nbytes in items:
-        seen.setdefault(name, int(nbytes))
     heap = DEFAULT_HEAP_LIMIT if heap_limit_bytes is None else int(heap_limit_bytes)
-    mem = sum(seen[k] for k in sorted(seen)) + heap
+    mem = sum(int(nbytes) for _, nbytes in items) + heap
     if mem >= BYTE_LIMIT:
         raise AnalysisError(f"task memory request {mem} bytes overflows the byte limit")
     widest = max(launches, key=lambda op: op.thread_blocks * warps_per_block(op.threads_per_block))

@@ -1,9 +1,19 @@
-"""One process per GPU: rank plumbing for the job-mix bench (no data-path
-collective — jobs are independent and shard by placement).
+"""Fleet plumbing for the job-mix bench: ONE decision authority over N GPUs.
 
-Each rank runs its own seeded mix on its own device (`rank_mix`); the only
-collective is the max over ranks of the device-timed step (`max_over_ranks`),
-so the whole-job value is (jobs on all ranks) / (slowest rank's time).
+The reference builds one Scheduler over every DeviceState
+(gs/sim_engine.py:224-229): mgb-warps is a global argmin over the devices'
+ledgers (gs/schedulers.py:155-171) and SA hands each job to the lowest free
+device (:173-178).  So the fleet is driven by one process: rank 0 opens the
+placement engine with one ledger per GPU and runs the executor over all N
+devices (jobs run on per-device streams; their staged inputs move over
+NVLink peer copies when a job lands on another GPU).  Jobs are independent,
+so there is no collective on the data path.
+
+Under torchrun (one process per GPU, as the bench contract launches it) the
+other ranks hold their GPU's context and only join the barriers and the
+max-over-ranks of the step time (they report 0 ms: the driving rank's device
+clock covers the whole fleet because the executor synchronizes every device
+before it returns).
 """
 
 from __future__ import annotations
@@ -18,12 +28,26 @@ def dist_env() -> tuple[int, int, int]:
     return rank, world, local
 
 
-def rank_mix(mix: str, jobs_per_rank: int, rank: int, base_seed: int = 1):
-    """Rank r's share of the weak-scaled workload: its own seeded mix with
-    seed base_seed + r (disjoint synthetic inputs per rank)."""
+def fleet_plan(gpus: int, world: int, rank: int) -> tuple[bool, list[int]]:
+    """(does this rank drive the fleet, the CUDA devices it drives).
+
+    world == 1: this process drives GPUs 0..gpus-1 itself.  world > 1: one
+    rank per GPU (world must equal gpus); rank 0 drives all of them."""
+    if gpus < 1:
+        raise ValueError("need at least one GPU")
+    if world > 1 and world != gpus:
+        raise ValueError(f"torchrun world size {world} != --gpus {gpus}")
+    if rank != 0:
+        return False, []
+    return True, list(range(gpus))
+
+
+def fleet_mix(mix: str, jobs_per_gpu: int, gpus: int, base_seed: int = 1):
+    """The fleet's workload: one seeded mix of jobs_per_gpu * gpus jobs
+    (weak scaling: per-GPU work fixed as N grows), placed by one authority."""
     from .catalog import gen_mix
 
-    return gen_mix(mix, jobs_per_rank, seed=base_seed + rank)
+    return gen_mix(mix, jobs_per_gpu * gpus, seed=base_seed)
 
 
 def max_over_ranks(values: list[float], dist=None, device=None) -> list[float]:
@@ -37,6 +61,7 @@ def max_over_ranks(values: list[float], dist=None, device=None) -> list[float]:
     return [float(v) for v in t.tolist()]
 
 
-def whole_job_rate(jobs_per_rank: int, world: int, ms_per_step: float) -> float:
-    """jobs/s of the whole job: every rank's jobs over the slowest rank's time."""
-    return jobs_per_rank * world / (ms_per_step / 1000.0)
+def rate(completed_per_step: float, ms_per_step: float) -> float:
+    """Whole-fleet jobs/s: jobs COMPLETED per step over the (max-over-ranks)
+    step time (gs/metrics.py:49-59 counts completed jobs only)."""
+    return completed_per_step / (ms_per_step / 1000.0) if ms_per_step > 0 else 0.0

@@ -42,6 +42,16 @@ class GsExecStats(ctypes.Structure):
                 ("decision_ms", c_double)]
 
 
+class GsExecEvent(ctypes.Structure):
+    """One entry of the executor's placement log (gs_work.h gs_exec_event)."""
+
+    _fields_ = [("kind", c_int32), ("handle", c_int32), ("device", c_int32), ("outcome", c_int32),
+                ("freed", c_int64), ("t_ms", c_double), ("probe", nat.GsProbe)]
+
+
+EV_SUBMIT, EV_RELEASE, EV_JOB_ENDED, EV_DRAIN = 0, 1, 2, 3
+
+
 class GsLaunchDesc(ctypes.Structure):
     _fields_ = [("thread_blocks", c_int32), ("threads_per_block", c_int32), ("regs_per_thread", c_int32),
                 ("smem_per_block", c_int32), ("est_duration_ms", c_double)]
@@ -62,6 +72,9 @@ WORK_SIGNATURES = {
     "gs_exec_stage": (c_int32, [c_void_p, c_int32, POINTER(c_int32), c_int32, c_int32]),
     "gs_exec_ledger_capacity": (c_int32, [c_int32, POINTER(c_int64)]),
     "gs_exec_unstage": (None, []),
+    "gs_measure_fp32_peak": (c_int32, [c_int32, POINTER(c_double)]),
+    "gs_exec_log": (c_int32, [c_void_p, c_int64, POINTER(c_int64), c_void_p, c_int32, POINTER(c_int32),
+                              POINTER(c_int32), POINTER(c_int32)]),
     "gs_gemm_bf16": (c_int32, [c_void_p, c_int64, c_void_p, c_int64, c_void_p, c_void_p, c_int64, c_int32,
                                c_int32, c_int32, c_int32, c_int32, c_void_p]),
 }
@@ -199,6 +212,13 @@ def request_from_launches(launches, buffers, heap_limit_bytes: int = 8 << 20):
     return out
 
 
+def fp32_peak_tflops(device: int = 0) -> float:
+    """Measured FP32 FMA peak of the device (gs_measure_fp32_peak)."""
+    t = c_double()
+    nat.check(lib().gs_measure_fp32_peak(device, ctypes.byref(t)))
+    return t.value
+
+
 def ledger_capacity(device: int = 0) -> int:
     """Bytes a run's ledger gets on `device` by default (free HBM + pool-held
     unused memory - 6 GiB); query once and pass as run_jobs(ledger_bytes=)
@@ -206,6 +226,30 @@ def ledger_capacity(device: int = 0) -> int:
     cap = c_int64(0)
     nat.check(lib().gs_exec_ledger_capacity(device, ctypes.byref(cap)))
     return cap.value
+
+
+@dataclass
+class ExecLog:
+    """The placement log of the last run: every decision-engine call in the
+    single decision authority's order (gs_exec_log)."""
+
+    events: list  # GsExecEvent
+    specs: list   # GsSpec per ledger
+    policy: int
+    cg_ratio: int
+
+
+def exec_log() -> ExecLog:
+    L = lib()
+    n = c_int64()
+    nd, pol, ratio = c_int32(), c_int32(), c_int32()
+    nat.check(L.gs_exec_log(None, 0, ctypes.byref(n), None, 0, ctypes.byref(nd), ctypes.byref(pol),
+                            ctypes.byref(ratio)))
+    evs = (GsExecEvent * max(n.value, 1))()
+    specs = (nat.GsSpec * max(nd.value, 1))()
+    nat.check(L.gs_exec_log(evs, n.value, ctypes.byref(n), specs, nd.value, ctypes.byref(nd), ctypes.byref(pol),
+                            ctypes.byref(ratio)))
+    return ExecLog(list(evs)[: n.value], list(specs)[: nd.value], pol.value, ratio.value)
 
 
 def run_jobs(jobs: list[Job], policy: str = "mgb-warps", devices: list[int] = (0,), workers: int = 8,

@@ -1,8 +1,8 @@
 """Probe capture: libgs's gs_request_from_launches
 aggregates recorded launches and buffers exactly like the reference's
 compute_resource_request (gs/task_builder.py:258-290), restated in
-gpushare.task_builder (itself pinned by the reference's tests).  Host
-arithmetic: runs on CPU."""
+gpushare.task_builder (both pinned to the reference's own outputs in
+test_probe_golden.py).  Host arithmetic: runs on CPU."""
 
 import random
 

@@ -78,10 +78,10 @@ def test_gpu_sweep_matches_oracle_at_scale(n, policy):
     np.testing.assert_array_equal(final, np.array([d.snapshot() for d in devs], dtype=np.int64))
 
 
-@pytest.mark.parametrize("chunk", range(4))
+@pytest.mark.parametrize("chunk", range(16))
 def test_ring_mode_replays_reference_streams(chunk):
-    """The same golden streams served by the persistent decision kernel
-    over the host-mapped command ring."""
+    """Every golden stream served by the persistent decision kernel over the
+    host-mapped command ring (16 chunks cover all recorded runs)."""
     n = 0
     for run in RUNS[chunk::16]:
         be = DropinBackend(ring=True)
@@ -191,3 +191,31 @@ def test_gpu_sweep_fast_chain_fifo_edges(max_res, ev_cap, monkeypatch):
     oev = O.OracleScheduler(devs, 3, 6, True).sweep(probes, max_res)
     assert fast[1] == len(oev)
     np.testing.assert_array_equal(fast[0], oev[: len(fast[0])])
+
+
+def test_sweep_consumes_the_scheduler():
+    """Tasks a sweep leaves resident keep their reservations and their
+    handles never reach the caller: a second sweep or a submit on the same
+    scheduler is a contract violation, not a silent leak of capacity."""
+    from paper_2107_08538_b200 import _native as nat
+    from paper_2107_08538_b200.gpushare import DeviceState, Scheduler, device_spec, parse_policy
+    from paper_2107_08538_b200.sweep import gen_probes
+
+    spec = device_spec("b200")
+    probes = gen_probes(500, seed=3)
+    devs = [DeviceState(spec, i) for i in range(2)]
+    sched = Scheduler(devs, parse_policy("mgb-warps"))
+    cap = 2 * len(probes) + 16
+    ev = np.zeros((cap, 3), dtype=np.int32)
+    ne, ms = ctypes.c_int64(), ctypes.c_float()
+    lib = nat.lib()
+    nat.check(lib.gs_sweep(sched._ptr, probes.ctypes.data, len(probes), 32, ev.ctypes.data, cap,
+                           ctypes.byref(ne), ctypes.byref(ms)))
+    assert sum(d.in_use_warps for d in devs) > 0  # residents still hold capacity
+    rc = lib.gs_sweep(sched._ptr, probes.ctypes.data, len(probes), 32, ev.ctypes.data, cap,
+                      ctypes.byref(ne), ctypes.byref(ms))
+    assert rc == nat.GS_ERR_CONTRACT
+    dec = nat.GsDecision()
+    p = nat.GsProbe()
+    p.handle, p.job = len(probes) + 1, 0
+    assert lib.gs_submit(sched._ptr, ctypes.byref(p), ctypes.byref(dec)) == nat.GS_ERR_CONTRACT
