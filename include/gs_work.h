@@ -168,6 +168,8 @@ typedef struct gs_exec_event {
     int32_t device;      /* ledger index (-1 none) */
     int32_t outcome;     /* GS_ASSIGN / GS_DEFER / GS_REJECTED, or a status code < 0 */
     int64_t freed;       /* GS_EV_RELEASE: bytes release_task returned */
+    int64_t free_mem_after;      /* submit / drain: the decision-log values */
+    int64_t in_use_warps_after;  /* (schedulers.py:203-218) */
     double t_ms;         /* wall time since the run started */
     gs_probe probe;      /* GS_EV_SUBMIT: the probe as submitted */
 } gs_exec_event;

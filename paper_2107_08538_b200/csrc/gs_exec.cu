@@ -556,6 +556,8 @@ int gs_exec_run_arrivals(const gs_job_desc *jobs, int32_t n_jobs, const double *
     for (int k = 0; k < tried; ++k) {
       log_ev(GS_EV_DRAIN, drain[k].handle, drain[k].device, drain[k].outcome, 0, nullptr);
       log.back().t_ms = ms_since(t0);
+      log.back().free_mem_after = drain[k].free_mem_after;
+      log.back().in_use_warps_after = drain[k].in_use_warps_after;
       if (drain[k].outcome == GS_ASSIGN) admitted[drain[k].handle] = drain[k].device;
     }
     if (adm) cv.notify_all();
@@ -623,11 +625,14 @@ int gs_exec_run_arrivals(const gs_job_desc *jobs, int32_t n_jobs, const double *
       {
         std::unique_lock<std::mutex> lk(mu);
         gs_decision dec;
+        memset(&dec, 0, sizeof dec);
         const auto a = Clock::now();
         int r = gs_submit(sched, &pr, &dec);
         decision_ms += ms_since(a);
         log_ev(GS_EV_SUBMIT, j, r < 0 ? -1 : dec.device, r < 0 ? r : dec.outcome, 0, &pr);
         log.back().t_ms = ms_since(t0);
+        log.back().free_mem_after = dec.free_mem_after;
+        log.back().in_use_warps_after = dec.in_use_warps_after;
         if (r < 0) {
           if (!first_err) {
             first_err = r;

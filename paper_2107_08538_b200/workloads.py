@@ -46,7 +46,8 @@ class GsExecEvent(ctypes.Structure):
     """One entry of the executor's placement log (gs_work.h gs_exec_event)."""
 
     _fields_ = [("kind", c_int32), ("handle", c_int32), ("device", c_int32), ("outcome", c_int32),
-                ("freed", c_int64), ("t_ms", c_double), ("probe", nat.GsProbe)]
+                ("freed", c_int64), ("free_mem_after", c_int64), ("in_use_warps_after", c_int64),
+                ("t_ms", c_double), ("probe", nat.GsProbe)]
 
 
 EV_SUBMIT, EV_RELEASE, EV_JOB_ENDED, EV_DRAIN = 0, 1, 2, 3
