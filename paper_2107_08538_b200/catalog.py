@@ -175,7 +175,7 @@ def host_footprint(job: Job) -> int:
     g = 2 << 20
     n, m = job.n, job.m
     sizes = {
-        "bfs": [(n + 1) * 4, n * 24, n * 4] + [(n // 32 + 1) * 4] * 3 + [32],
+        "bfs": [(n + 1) * 4, n * 24, n * 4] + [(n // 32 + 4) // 4 * 16] * 3 + [8 * 17, (n + 1) * 4, n * 24],
         "hotspot": [n * n * 4] * 3,
         "srad": [n * n * 4] * 2 + [16],
         "kmeans": [n * m * 4, n * 4, 5 * m * 4, 5 * m * 8, 40],

@@ -8,6 +8,7 @@
 // brings its inputs in (D2D from staged HBM, or H2D from pinned host memory
 // in e2e mode), runs its kernels on its own stream with grids sized to its
 // SM share, returns its outputs and frees everything.
+#include <cub/device/device_scan.cuh>
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <string.h>
@@ -42,9 +43,21 @@ int err(int code, const std::string &m) {
   } while (0)
 
 constexpr int kBfsBatch = 8;                // bfs levels launched per host round trip
+// bfs direction switch: a level runs bottom-up when alpha x frontier >
+// unvisited (GS_BFS_ALPHA overrides, for tuning runs only)
+static unsigned bfs_alpha() {
+  static const unsigned a = [] {
+    const char *e = getenv("GS_BFS_ALPHA");
+    return e ? (unsigned)atoi(e) : 2u;
+  }();
+  return a;
+}
 constexpr int64_t kGranule = 2 << 20;       // device-pool allocation granule
 constexpr int64_t kHeap = 8 << 20;          // per-task heap (task_builder.py:29)
 constexpr int kThreads = 256;
+
+// bitmap length of a bfs job in uint4s (n + 1 bits, whole uint4s)
+static int64_t bfs_words4(int64_t n) { return (n / 32 + 1 + 3) / 4; }
 
 int64_t round_granule(int64_t b) { return (b + kGranule - 1) / kGranule * kGranule; }
 
@@ -55,9 +68,12 @@ std::vector<Buf> job_buffers(const gs_job_desc &j) {
   const int64_t n = j.n;
   switch (j.kind) {
     case GS_JOB_BFS:
-      // row_ptr, col, level, then the frontier / visited / snapshot bitmaps and the counter
-      b = {{(n + 1) * 4, IN}, {n * GS_BFS_DEGREE * 4, IN}, {n * 4, OUT}, {(n / 32 + 1) * 4, SCR},
-           {(n / 32 + 1) * 4, SCR}, {(n / 32 + 1) * 4, SCR}, {8 * kBfsBatch, SCR}};
+      // row_ptr, col, level, the frontier / visited / snapshot bitmaps, the
+      // level counters (two batches + the running visited total), then the
+      // transposed CSR (in_row, in_col) the bottom-up levels scan
+      b = {{(n + 1) * 4, IN}, {n * GS_BFS_DEGREE * 4, IN}, {n * 4, OUT}, {bfs_words4(n) * 16, SCR},
+           {bfs_words4(n) * 16, SCR}, {bfs_words4(n) * 16, SCR}, {8 * (2 * kBfsBatch + 1), SCR},
+           {(n + 1) * 4, IN}, {n * GS_BFS_DEGREE * 4, IN}};
       break;
     case GS_JOB_HOTSPOT:
       b = {{n * n * 4, INOUT}, {n * n * 4, IN}, {n * n * 4, SCR}};
@@ -137,7 +153,7 @@ std::vector<Shape> job_launches(const gs_job_desc &j) {
   const int g = job_grid(j);
   switch (j.kind) {
     case GS_JOB_BFS:
-      return {{(const void *)bfs_expand, g, kThreads}, {(const void *)bfs_commit, g, kThreads}};
+      return {{(const void *)bfs_expand, g, kBfsThreads}, {(const void *)bfs_commit, g, kBfsThreads}};
     case GS_JOB_HOTSPOT:
     {
       Shape s2{(const void *)hotspot_step2, g, kThreads};
@@ -274,8 +290,25 @@ int generate_inputs(const gs_job_desc &j, const std::vector<void *> &dst, cudaSt
   const int64_t n = j.n;
   switch (j.kind) {
     case GS_JOB_BFS:
-      gen_bfs<<<g, kThreads, 0, st>>>((int32_t *)dst[0], (int32_t *)dst[1], n, j.seed);
+    {
+      int32_t *row = (int32_t *)dst[0], *col = (int32_t *)dst[1], *in_row = (int32_t *)dst[7];
+      gen_bfs<<<g, kThreads, 0, st>>>(row, col, n, j.seed);
+      // transposed CSR: in-degree histogram, inclusive scan, scatter
+      CUW(cudaMemsetAsync(in_row, 0, (n + 1) * 4, st));
+      bfs_indeg<<<g, kThreads, 0, st>>>(col, n * GS_BFS_DEGREE, in_row + 1);
+      size_t tmp_bytes = 0;
+      CUW(cub::DeviceScan::InclusiveSum(nullptr, tmp_bytes, in_row + 1, in_row + 1, (int)n, st));
+      void *tmp = nullptr;
+      int32_t *cursor = nullptr;
+      CUW(cudaMallocAsync(&tmp, tmp_bytes, st));
+      CUW(cudaMallocAsync((void **)&cursor, n * 4, st));
+      CUW(cub::DeviceScan::InclusiveSum(tmp, tmp_bytes, in_row + 1, in_row + 1, (int)n, st));
+      CUW(cudaMemcpyAsync(cursor, in_row, n * 4, cudaMemcpyDeviceToDevice, st));
+      bfs_scatter<<<g, kThreads, 0, st>>>(row, col, n, cursor, (int32_t *)dst[8]);
+      CUW(cudaFreeAsync(tmp, st));
+      CUW(cudaFreeAsync(cursor, st));
       break;
+    }
     case GS_JOB_HOTSPOT:
       gen_hotspot<<<g, kThreads, 0, st>>>((float *)dst[0], (float *)dst[1], n * n, j.seed);
       break;
@@ -317,23 +350,30 @@ int run_kernels(const gs_job_desc &j, std::vector<void *> &buf, cudaStream_t st,
       const int32_t *row = (const int32_t *)buf[0], *col = (const int32_t *)buf[1];
       int32_t *level = (int32_t *)buf[2];
       uint32_t *F = (uint32_t *)buf[3], *V = (uint32_t *)buf[4], *S = (uint32_t *)buf[5];
-      auto *cnt = (unsigned long long *)buf[6];
-      const int64_t nwords = n / 32 + 1;
+      auto *cnt = (unsigned long long *)buf[6];  // [2 batches of kBfsBatch levels][visited total]
+      const int32_t *in_row = (const int32_t *)buf[7], *in_col = (const int32_t *)buf[8];
+      unsigned long long *visited = cnt + 2 * kBfsBatch;
+      const int64_t nwords4 = bfs_words4(n);
       CUW(cudaMemsetAsync(level, 0xff, n * 4, st));
       CUW(cudaMemsetAsync(level, 0, 4, st));
       for (uint32_t *bm : {F, V, S}) CUW(cudaMemsetAsync(bm, 1, 1, st));  // source vertex 0 (bitmaps zeroed)
       // kBfsBatch levels per host round trip (Rodinia checks after every
       // level): a level whose predecessor found nothing returns at once, so
       // a batch overruns the depth for the price of empty launches
-      for (int32_t depth = 0;; depth += kBfsBatch) {
-        CUW(cudaMemsetAsync(cnt, 0, 8 * kBfsBatch, st));
+      // (batches alternate between the two counter halves, so a batch's
+      // first level reads the previous batch's last count)
+      for (int32_t depth = 0, half = 0;; depth += kBfsBatch, half ^= 1) {
+        unsigned long long *c = cnt + half * kBfsBatch;
+        CUW(cudaMemsetAsync(c, 0, 8 * kBfsBatch, st));
         for (int q = 0; q < kBfsBatch; ++q) {
-          const unsigned long long *prev = q ? cnt + q - 1 : nullptr;
-          bfs_expand<<<g, kThreads, 0, st>>>(row, col, F, V, nwords, prev, tk);
-          bfs_commit<<<g, kThreads, 0, st>>>(V, S, F, level, n, nwords, depth + q + 1, prev, cnt + q, tk);
+          const unsigned long long *prev = q ? c + q - 1 : (depth ? cnt + (half ^ 1) * kBfsBatch + kBfsBatch - 1 : nullptr);
+          bfs_expand<<<g, kBfsThreads, 0, st>>>(row, col, in_row, in_col, F, V, 4 * nwords4, n, prev, visited,
+                                                bfs_alpha(), tk);
+          bfs_commit<<<g, kBfsThreads, 0, st>>>((const uint4 *)V, (uint4 *)S, (uint4 *)F, level, n, nwords4,
+                                                depth + q + 1, prev, c + q, visited, tk);
         }
         launches += 2 * kBfsBatch;
-        CUW(cudaMemcpyAsync(host_scalar, cnt + kBfsBatch - 1, 8, cudaMemcpyDeviceToHost, st));
+        CUW(cudaMemcpyAsync(host_scalar, c + kBfsBatch - 1, 8, cudaMemcpyDeviceToHost, st));
         CUW(cudaStreamSynchronize(st));
         if (*reinterpret_cast<unsigned long long *>(host_scalar) == 0) break;  // the batch's last level was empty
       }

@@ -46,3 +46,11 @@ def test_bench_size_kernel_matches_oracle(tpl, kind, kw):
         print(f"{tpl}: max |err| {float(np.max(np.abs(got - want))):.3g}, bit-exact {exact}")
         if exact:
             assert rec.checksum == K.digest(kind, want)
+
+
+@pytest.mark.parametrize("tpl,kind,kw", CASES, ids=[c[0] for c in CASES])
+def test_bench_template_probe_matches_host_footprint(tpl, kind, kw):
+    """The CPU reference arm places the mix with catalog.host_footprint; it
+    must be the probe's mem_bytes (gs_job_probe, the executor's capture)."""
+    job = W.Job(kind, seed=1001, **kw)
+    assert W.probe(job).mem_bytes == C.host_footprint(job)
