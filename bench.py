@@ -302,6 +302,39 @@ def parity_check(W, mix, step_records, outs, device):
                    "solo within 1e-5 rel of the oracle"}
 
 
+def cfg2_block(W, C, devices, workers, jobs_n, seed):
+    """BASELINE cfg 2 beside the headline: a Darknet YOLOv3-tiny + ResNet-50
+    inference mix whose co-running footprint exceeds the fleet's HBM, under
+    the memory-safe policy, one-job-per-GPU and cg:8 (no memory check).
+    Each job synthesizes its inputs on the device (inside its timing).  One
+    warm-up run then one run timed with CUDA events per policy."""
+    import torch
+
+    jobs = C.darknet_mix(jobs_n * len(devices), seed, C.CFG2_SIZES, C.CFG2_BATCHES, C.CFG2_RESNET)
+    foot = sum(C.host_footprint(j) for j in jobs)
+    out = {"workload": f"cfg2: {len(jobs)} Darknet jobs (YOLOv3-tiny / ResNet-50, batch 32-64) on "
+                       f"{len(devices)} GPU(s)", "sum_footprint_gib": round(foot / 2**30, 1)}
+    for policy in ("mgb-warps", "sa", "cg:8"):
+        W.run_jobs(jobs, policy=policy, devices=devices, workers=workers)
+        for d in devices:
+            torch.cuda.synchronize(d)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        res = W.run_jobs(jobs, policy=policy, devices=devices, workers=workers)
+        e1.record()
+        for d in devices:
+            torch.cuda.synchronize(d)
+        ms = e0.elapsed_time(e1)
+        done = [r for r in res.records if r["state"] == "done"]
+        out[policy] = {"jobs_per_s": round(res.completed / (ms / 1000.0), 3), "ms": round(ms, 1),
+                       "completed": res.completed, "oom": res.oom,
+                       "mean_turnaround_ms": round(statistics.fmean(r["turnaround_ms"] for r in done), 1)
+                       if done else None}
+        log(f"cfg2 {policy}: {out[policy]}")
+    out["speedup_vs_sa"] = round(out["mgb-warps"]["jobs_per_s"] / max(out["sa"]["jobs_per_s"], 1e-9), 3)
+    return out
+
+
 def reference_arm(args, mix):
     """--impl reference: the reference's path on host cores (C port)."""
     from oracle import oracle as O
@@ -392,6 +425,8 @@ def drive(args, devices, torch, barrier):
             sa_e2e = summarize(sr2, st2)
         W.unstage()
 
+    cfg2 = None if args.skip_cfg2 else cfg2_block(W, C, devices, workers, args.cfg2_jobs, 1)
+
     # ---- CPU leg: oracle on a bounded sample = cpu_baseline + parity ----
     cpu_rate, outs, cpu_dt = cpu_sample(mix, args.cpu_budget)
     parity = parity_check(W, mix, last_records, outs, devices[0])
@@ -401,6 +436,14 @@ def drive(args, devices, torch, barrier):
                   "checked_against": "oracle/gs_oracle.c (golden-pinned restatement of schedulers.py)"}
 
     value = rate(ours["completed_per_step"], ours["ms_per_step"])
+    # per-kernel slowdown of the co-located jobs (metrics.py:75-79): device
+    # time of each job's kernels in the last timed step vs the same template
+    # alone on an idle GPU
+    sl = [(r["compute_ms"] / solo_ms[mix[i].template] - 1.0) * 100.0 for i, r in enumerate(last_records)
+          if r["state"] == "done" and solo_ms.get(mix[i].template, 0) > 0]
+    slowdown = {"mean_pct": round(statistics.fmean(sl), 2) if sl else None,
+                "median_pct": round(statistics.median(sl), 2) if sl else None,
+                "jobs": len(sl), "solo": "same template alone on an idle GPU (kernel device time)"}
     # dominant kind: the largest share of the mix's solo device time
     share = {}
     for mj in mix:
@@ -441,6 +484,7 @@ def drive(args, devices, torch, barrier):
         "gpu_launches": ours["kernel_launches"] + ours["decision_launches"],
         "decision_launches": ours["decision_launches"],
         "decision_ms_per_step": round(ours["decision_ms"] / args.steps, 3),
+        "kernel_slowdown": slowdown,
         "roofline": roof,
         "mix_hbm_frac": round(mix_frac, 4),
         "parity": parity,
@@ -469,6 +513,8 @@ def drive(args, devices, torch, barrier):
             sv = rate(sa_e2e["completed_per_step"], sa_e2e["ms_per_step"])
             line["e2e"]["sa_value"] = round(sv, 4)
             line["e2e"]["speedup_vs_sa"] = round(line["e2e"]["value"] / sv, 3)
+    if cfg2:
+        line["cfg2"] = cfg2
     line["clocks"] = clk.summary()
     names = [mix[i].template for i, _ in outs]
     line["cpu_baseline"] = {"value": round(cpu_rate, 4), "unit": UNIT, "cores": os.cpu_count() or 1,
@@ -491,6 +537,8 @@ def main() -> int:
     ap.add_argument("--cpu-budget", type=float, default=12.0)
     ap.add_argument("--skip-e2e", action="store_true")
     ap.add_argument("--skip-sa", action="store_true")
+    ap.add_argument("--skip-cfg2", action="store_true")
+    ap.add_argument("--cfg2-jobs", type=int, default=32, help="cfg 2 Darknet jobs per GPU")
     args = ap.parse_args()
     from paper_2107_08538_b200.multi import dist_env, fleet_mix, fleet_plan, max_over_ranks
 

@@ -61,7 +61,7 @@ typedef struct gs_job_record {
     int64_t h2d_bytes, d2h_bytes;
     uint64_t checksum;    /* order-independent digest of the job's outputs */
     int32_t n_kernels;
-    int32_t pad;
+    int32_t sm_share;     /* SMs of the green-context partition the job ran on (0 = whole device) */
     /* where a job's wall time goes (diagnostics): host time from admission
      * to the inputs' launches returning, device time from the job's first
      * queued op to its first kernel (input fill / generation, including
@@ -146,6 +146,22 @@ int gs_gemm_bf16(const void *A, int64_t lda, const void *B, int64_t ldb, const f
 int gs_exec_stage(const gs_job_desc *jobs, int32_t n_jobs, const int32_t *cuda_devices, int32_t n_devices,
                   int32_t mode);
 void gs_exec_unstage(void);
+
+/* SM shares of co-located jobs (the paper's MPS
+ * partitions): parts > 1 splits every device's SMs into `parts` disjoint
+ * green-context partitions (cuDevSmResourceSplitByCount in 8-SM groups,
+ * cuGreenCtxCreate); a job placed on a device runs on a free partition's
+ * streams with its grids sized to the partition's SM count, waiting for
+ * one when all are taken.  parts <= 1 (the default) runs every job on
+ * ordinary streams over the whole device.  Applies to later gs_exec_run*
+ * calls; *sms_out (optional) gets the partitions' SM counts on device 0
+ * once they are built by a run. */
+int gs_exec_set_sm_parts(int32_t parts);
+/* Give back the executor's idle per-device job arenas (the slab a run
+ * allocates once, sized to its ledger capacity, and keeps for later runs;
+ * csrc/gs_arena.h).  Later runs allocate a new one. */
+void gs_exec_release_memory(void);
+int gs_exec_sm_parts_layout(int32_t cuda_device, int32_t parts, int32_t *sms_out, int32_t cap, int32_t *n_out);
 
 /* Measured FP32 FMA throughput of `cuda_device` in TFLOP/s (8 independent
  * FFMA chains per thread, 8 x 256-thread blocks per SM): the roofline

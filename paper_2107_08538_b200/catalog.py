@@ -21,14 +21,19 @@ from dataclasses import dataclass
 
 from .workloads import Job
 
-# kind -> (small kwargs, large kwargs)
+# kind -> (small kwargs, large kwargs).  Footprints (host_footprint) follow
+# the reference catalog's classes, small 1-4 GiB and large 4-13 GiB
+# (catalog.json:3): bfs 1.8 / 7.2, hotspot 3.0 / 6.8, srad 2.0 / 4.5, kmeans
+# 1.1 / 4.2, backprop 2.0 / 5.9, needle 2.0 / 4.5 GiB.  lud is the exception
+# (0.06 / 0.15 GiB): its work is O(n^3) — a 1 GiB matrix (n = 16384) is
+# 2.9 TFLOP, ~150 ms on a B200 and minutes on the CPU oracle.
 RODINIA = {
-    "bfs": (dict(n=16_000_000), dict(n=48_000_000)),
-    "hotspot": (dict(n=8192, iters=40), dict(n=16384, iters=40)),
-    "srad": (dict(n=8192, iters=10), dict(n=16384, iters=10)),
-    "kmeans": (dict(n=4_000_000, m=34, iters=5), dict(n=8_000_000, m=34, iters=10)),
-    "backprop": (dict(n=16_000_000, m=16, iters=2), dict(n=32_000_000, m=16, iters=2)),
-    "needle": (dict(n=8192), dict(n=16384)),
+    "bfs": (dict(n=32_000_000), dict(n=128_000_000)),
+    "hotspot": (dict(n=16384, iters=40), dict(n=24576, iters=40)),
+    "srad": (dict(n=16384, iters=10), dict(n=24576, iters=10)),
+    "kmeans": (dict(n=8_000_000, m=34, iters=10), dict(n=32_000_000, m=34, iters=10)),
+    "backprop": (dict(n=16_000_000, m=16, iters=2), dict(n=48_000_000, m=16, iters=2)),
+    "needle": (dict(n=16384), dict(n=24576)),
     "lud": (dict(n=4096), dict(n=6144)),
 }
 
@@ -226,3 +231,23 @@ def algorithmic_work(job: Job) -> tuple[float, str]:
     if job.kind == "resnet":
         return resnet_flops(n, m) * it, "TC_FLOP"
     return 0.0, "B"
+
+
+def darknet_mix(n: int, seed: int, sizes=(416, 608, 832, 1024), batches=(1, 2, 4, 8, 16, 32, 64),
+                resnet_sizes=(224, 448)) -> list[Job]:
+    """Half YOLOv3-tiny, half ResNet-50 inference jobs (BASELINE cfg 2)."""
+    rng = random.Random(f"{seed}|darknet|{n}")
+    out = []
+    for i in range(n):
+        B = rng.choice(batches)
+        if rng.random() < 0.5:
+            out.append(Job("yolo", n=rng.choice(sizes), m=B, iters=1, seed=seed * 1000 + i))
+        else:
+            out.append(Job("resnet", n=rng.choice(resnet_sizes), m=B, iters=1, seed=seed * 1000 + i))
+    return out
+
+
+# cfg 2: jobs large enough that 8 co-running ones exceed the device (Darknet
+# keeps every layer's output resident: 8-33 GB per YOLO job, 7-28 GB per
+# ResNet-50 job at these sizes)
+CFG2_SIZES, CFG2_BATCHES, CFG2_RESNET = (1280, 1536, 1792), (32, 64), (896, 1152)

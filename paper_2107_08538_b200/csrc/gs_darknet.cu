@@ -479,7 +479,7 @@ ViewArgs vargs(const TView &v, const std::vector<void *> &buf) {
 // mgb-sm places a job by its widest launch under the most demanding
 // kernel's occupancy (task_builder.py:272-289 aggregation), so no grid may
 // exceed 2 x 148.
-int grid_for(int64_t total) { return (int)std::min<int64_t>((total + kThr - 1) / kThr, 2 * kSMs); }
+int grid_for(int64_t total) { return (int)std::min<int64_t>((total + kThr - 1) / kThr, 2 * sm_count()); }
 
 }  // namespace
 
@@ -505,7 +505,7 @@ std::vector<Shape> gemm_launches(const gs_job_desc &j) {
     if (L.type == CONV)
       bn_max = std::max(bn_max, gemm_pick_bn((int)((int64_t)L.out.n * L.out.h * L.out.w), L.cout));
   const int64_t pix0 = (int64_t)j.m * j.n * j.n;
-  Shape g{gemm_kernel_fn(bn_max), 2 * kSMs, gemm_block_threads()};
+  Shape g{gemm_kernel_fn(bn_max), 2 * sm_count(), gemm_block_threads()};
   g.dsmem = (int)gemm_smem_for(bn_max);
   std::vector<Shape> v = {g, {(const void *)im2row, grid_for(pix0 * 4), kThr},
                           {(const void *)maxpool, grid_for(pix0), kThr}};
@@ -572,7 +572,7 @@ int gemm_run(const gs_job_desc &j, std::vector<void *> &buf, cudaStream_t st, in
         A = in.p;  // 1x1 / stride 1: the activation is already the im2row matrix
         lda = L.in.pitch;
       } else {
-        const int grid = (int)std::min<int64_t>((int64_t)L.in.n * L.out.h, 2 * kSMs);  // blocks walk output rows
+        const int grid = (int)std::min<int64_t>((int64_t)L.in.n * L.out.h, 2 * sm_count());  // blocks walk output rows
         im2row<<<grid, kThr, 0, st>>>(in, (__nv_bfloat16 *)buf[B_WS], L.k, L.stride, L.pad, L.out.h, L.out.w,
                                       L.kdim, L.kpad);
         ++*launches;
@@ -582,7 +582,7 @@ int gemm_run(const gs_job_desc &j, std::vector<void *> &buf, cudaStream_t st, in
       void *out = L.out.f32 ? (void *)((float *)buf[L.out.buf] + L.out.off) : (void *)obf;
       const void *res = L.res.buf >= 0 ? (const void *)((const __nv_bfloat16 *)buf[L.res.buf] + L.res.off) : nullptr;
       int rc = gemm_bf16(A, lda, (const __nv_bfloat16 *)buf[B_W] + L.woff, L.kpad, (const float *)buf[B_BIAS] + L.boff,
-                         out, L.out.pitch, (int)opix, L.cout, L.kpad, L.out.f32 ? 1 : 0, L.act, 2 * kSMs, st, res,
+                         out, L.out.pitch, (int)opix, L.cout, L.kpad, L.out.f32 ? 1 : 0, L.act, 2 * sm_count(), st, res,
                          L.res.pitch, tk);
       if (rc) return rc;
       ++*launches;

@@ -14,6 +14,7 @@
 //     allocate without checks and can (a failed allocation is an "oom"
 //     crash record, sim_engine.py:342-350);
 //   * completion releases the task's ledger entry and re-drives the queue.
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <string.h>
@@ -23,6 +24,7 @@
 #include <chrono>
 #include <condition_variable>
 #include <functional>
+#include <map>
 #include <mutex>
 #include <string>
 #include <thread>
@@ -30,6 +32,7 @@
 
 #include "../../include/gs.h"
 #include "../../include/gs_work.h"
+#include "gs_arena.h"
 #include "gs_cache.h"
 #include "gs_work_internal.h"
 
@@ -113,6 +116,73 @@ bool staged_on(const gs_job_desc &d, int device, bool host) {
   return false;
 }
 
+// Per-device job arenas (gs_arena.h), process-lifetime: the slab is
+// allocated once and reused by every later run whose ledger capacity fits
+// in it (a run limits it to its own capacity); a larger capacity replaces
+// it between runs.  GS_ARENA=0 falls back to the stream-ordered pool.
+std::mutex g_arena_mu;
+std::map<int, gsa::Arena *> g_arenas;
+
+static bool arena_enabled() {
+  const char *e = getenv("GS_ARENA");
+  return !(e && e[0] == '0');
+}
+
+static int64_t arena_idle_bytes(int device) {
+  std::lock_guard<std::mutex> g(g_arena_mu);
+  auto it = g_arenas.find(device);
+  return it != g_arenas.end() && it->second->in_use() == 0 ? it->second->size() : 0;
+}
+
+// free an idle arena (staging or another allocator needs the memory)
+void arena_drop_idle(int device) {
+  std::lock_guard<std::mutex> g(g_arena_mu);
+  auto it = g_arenas.find(device);
+  if (it == g_arenas.end() || it->second->in_use()) return;
+  int prev = 0;
+  cudaGetDevice(&prev);
+  cudaSetDevice(device);
+  cudaDeviceSynchronize();
+  cudaFree(it->second->base());
+  delete it->second;
+  g_arenas.erase(it);
+  cudaSetDevice(prev);
+}
+
+static gsa::Arena *arena_for(int device, int64_t capacity) {
+  std::lock_guard<std::mutex> g(g_arena_mu);
+  gsa::Arena *&a = g_arenas[device];
+  capacity = capacity / gsa::kGranule * gsa::kGranule;  // whole granules
+  if (a && a->size() >= capacity && a->reset(capacity)) return a;
+  int prev = 0;
+  cudaGetDevice(&prev);
+  cudaSetDevice(device);
+  if (a) {
+    if (a->in_use()) {
+      cudaSetDevice(prev);
+      return nullptr;
+    }
+    cudaFree(a->base());
+    delete a;
+    a = nullptr;
+  }
+  // memory the stream-ordered pool keeps (solo runs) goes back first
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+    cudaDeviceSynchronize();
+    cudaMemPoolTrimTo(pool, 0);
+  }
+  char *base = nullptr;
+  const int64_t size = capacity;
+  if (size > 0 && cudaMalloc((void **)&base, (size_t)size) == cudaSuccess) {
+    a = new gsa::Arena(device, base, size);
+  } else {
+    cudaGetLastError();
+  }
+  cudaSetDevice(prev);
+  return a;
+}
+
 int stage_one(const gs_job_desc &j, int device, int mode, Staged &out) {
   CUE(cudaSetDevice(device));
   const std::vector<Buf> bufs = job_buffers(j);
@@ -124,7 +194,13 @@ int stage_one(const gs_job_desc &j, int device, int mode, Staged &out) {
   cudaStream_t st;
   CUE(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
   for (size_t i = 0; i < bufs.size(); ++i)
-    if (bufs[i].role == IN || bufs[i].role == INOUT) CUE(cudaMalloc(&dev[i], bufs[i].bytes));
+    if (bufs[i].role == IN || bufs[i].role == INOUT) {
+      if (cudaMalloc(&dev[i], bufs[i].bytes) != cudaSuccess) {
+        cudaGetLastError();  // an idle job arena holds the memory: give it back and retry
+        arena_drop_idle(device);
+        CUE(cudaMalloc(&dev[i], bufs[i].bytes));
+      }
+    }
   int rc = generate_inputs(j, dev, st);
   if (rc) return rc;
   for (size_t i = 0; i < bufs.size(); ++i) {
@@ -152,19 +228,41 @@ int stage_one(const gs_job_desc &j, int device, int mode, Staged &out) {
 // device pool refused an allocation.
 int run_job(const gs_job_desc &j, const Staged *stg, int mode, cudaStream_t st, gs_job_record &rec, bool *oom,
             void *host_out, int64_t host_out_bytes, int32_t *host_scalar, std::atomic<int64_t> *kernel_count,
-            unsigned long long *host_sum, int device) {
+            unsigned long long *host_sum, int device, gsa::Arena *arena = nullptr, bool wait_mem = false) {
   *oom = false;
   const auto t_admit = Clock::now();
   const std::vector<Buf> bufs = job_buffers(j);
   std::vector<void *> buf(bufs.size(), nullptr);
   unsigned long long *dsum = nullptr;
+  // arena requests: every buffer, then the control block (one granule of
+  // the job's heap allowance)
+  std::vector<int64_t> req;
+  std::vector<void *> got;
   auto release = [&]() {
+    if (arena) {
+      cudaStreamSynchronize(st);
+      if (!got.empty()) arena->free_all(got, req);
+      got.clear();
+      return;
+    }
     for (void *p : buf)
       if (p) cudaFreeAsync(p, st);
     if (dsum) cudaFreeAsync(dsum, st);
     cudaStreamSynchronize(st);
   };
-  for (size_t i = 0; i < bufs.size(); ++i) {
+  if (arena) {
+    for (const Buf &b : bufs) req.push_back(b.bytes);
+    req.push_back(32);
+    double waited = 0;
+    if (!arena->alloc_all(req, got, wait_mem, &waited)) {
+      got.clear();
+      *oom = true;
+      return GS_OK;
+    }
+    for (size_t i = 0; i < bufs.size(); ++i) buf[i] = got[i];
+    dsum = (unsigned long long *)got.back();
+  }
+  for (size_t i = 0; i < bufs.size() && !arena; ++i) {
     const auto ta = Clock::now();
     cudaError_t e = cudaMallocAsync(&buf[i], bufs[i].bytes, st);
     if (g_alloc_log && ms_since(ta) > 5.0)
@@ -193,7 +291,7 @@ int run_job(const gs_job_desc &j, const Staged *stg, int mode, cudaStream_t st, 
     }
   }
   // 32 B of job control: [0] the output digest, [1..] the kernels' tile tickets
-  if (cudaMallocAsync((void **)&dsum, 32, st) != cudaSuccess) {
+  if (!arena && cudaMallocAsync((void **)&dsum, 32, st) != cudaSuccess) {
     cudaGetLastError();
     dsum = nullptr;
     release();
@@ -341,6 +439,144 @@ void gs_exec_unstage(void) {
   g_staged.clear();
 }
 
+// ---- green-context SM partitions (gs_exec_set_sm_parts) -------------------
+// Built once per (device, parts) and kept for the process: the device's SMs
+// are split into 8-SM groups (plus the remainder group the split leaves),
+// and the groups are dealt to the partitions largest-first onto the
+// partition with the fewest SMs so far.  Each partition has a default- and
+// a high-priority stream created in its green context; runtime-API work
+// (cudaMallocAsync, copies, launches, events) issued to those streams runs
+// on the partition's SMs only (measured: tools/green_probe.cu).
+struct GreenPart {
+  CUgreenCtx g = nullptr;
+  cudaStream_t lo = nullptr, hi = nullptr;
+  int sms = 0;
+};
+struct GreenSet {
+  std::vector<GreenPart> parts;
+  std::vector<char> busy;
+  std::mutex mu;
+  std::condition_variable cv;
+  int acquire() {
+    std::unique_lock<std::mutex> lk(mu);
+    for (;;) {
+      for (size_t i = 0; i < busy.size(); ++i)
+        if (!busy[i]) {
+          busy[i] = 1;
+          return (int)i;
+        }
+      cv.wait(lk);
+    }
+  }
+  void release(int i) {
+    {
+      std::lock_guard<std::mutex> g(mu);
+      busy[i] = 0;
+    }
+    cv.notify_one();
+  }
+};
+std::mutex g_green_mu;
+std::map<std::pair<int, int>, GreenSet *> g_green;
+std::atomic<int> g_sm_parts{0};
+
+#define CUD(call)                                                                  \
+  do {                                                                             \
+    CUresult r_ = (call);                                                          \
+    if (r_ != CUDA_SUCCESS) {                                                      \
+      const char *s_ = nullptr;                                                    \
+      green_api().getErrorString(r_, &s_);                                         \
+      return err(GS_ERR_CUDA, std::string(#call ": ") + (s_ ? s_ : "?"));          \
+    }                                                                              \
+  } while (0)
+
+// Driver entry points, resolved through the runtime (libgs does not link
+// libcuda: the library must load on hosts without a driver).
+struct GreenApi {
+  CUresult (*getErrorString)(CUresult, const char **) = nullptr;
+  CUresult (*deviceGet)(CUdevice *, int) = nullptr;
+  CUresult (*getDevResource)(CUdevice, CUdevResource *, CUdevResourceType) = nullptr;
+  CUresult (*split)(CUdevResource *, unsigned *, const CUdevResource *, CUdevResource *, unsigned, unsigned) = nullptr;
+  CUresult (*genDesc)(CUdevResourceDesc *, CUdevResource *, unsigned) = nullptr;
+  CUresult (*create)(CUgreenCtx *, CUdevResourceDesc, CUdevice, unsigned) = nullptr;
+  CUresult (*streamCreate)(CUstream *, CUgreenCtx, unsigned, int) = nullptr;
+  bool ok = false;
+};
+static const GreenApi &green_api() {
+  static GreenApi a = [] {
+    GreenApi g;
+    auto get = [](const char *name, void **fn) {
+      cudaDriverEntryPointQueryResult q;
+      if (cudaGetDriverEntryPoint(name, fn, cudaEnableDefault, &q) != cudaSuccess || q != cudaDriverEntryPointSuccess)
+        *fn = nullptr;
+      return *fn != nullptr;
+    };
+    g.ok = get("cuGetErrorString", (void **)&g.getErrorString) && get("cuDeviceGet", (void **)&g.deviceGet) &&
+           get("cuDeviceGetDevResource", (void **)&g.getDevResource) &&
+           get("cuDevSmResourceSplitByCount", (void **)&g.split) &&
+           get("cuDevResourceGenerateDesc", (void **)&g.genDesc) && get("cuGreenCtxCreate", (void **)&g.create) &&
+           get("cuGreenCtxStreamCreate", (void **)&g.streamCreate);
+    return g;
+  }();
+  return a;
+}
+
+static int green_for(int device, int parts, GreenSet **out) {
+  std::lock_guard<std::mutex> g(g_green_mu);
+  GreenSet *&gs = g_green[{device, parts}];
+  if (gs) {
+    *out = gs;
+    return GS_OK;
+  }
+  CUE(cudaSetDevice(device));
+  CUE(cudaFree(0));  // the driver and the primary context exist before the green ones
+  const GreenApi &A = green_api();
+  if (!A.ok) return err(GS_ERR_CUDA, "green-context driver entry points unavailable");
+  CUdevice dev;
+  CUD(A.deviceGet(&dev, device));
+  CUdevResource all;
+  CUD(A.getDevResource(dev, &all, CU_DEV_RESOURCE_TYPE_SM));
+  unsigned ng = 0;
+  CUD(A.split(nullptr, &ng, &all, nullptr, 0, 8));
+  std::vector<CUdevResource> grp(ng + 1);
+  CUdevResource rem;
+  CUD(A.split(grp.data(), &ng, &all, &rem, 0, 8));
+  grp.resize(ng);
+  if (rem.sm.smCount > 0) grp.push_back(rem);
+  if (parts < 1 || parts > (int)grp.size()) return err(GS_ERR_CONFIG, "more SM partitions than 8-SM groups");
+  std::vector<int> order(grp.size());
+  for (size_t i = 0; i < order.size(); ++i) order[i] = (int)i;
+  std::stable_sort(order.begin(), order.end(),
+                   [&](int a, int b) { return grp[a].sm.smCount > grp[b].sm.smCount; });
+  std::vector<std::vector<CUdevResource>> deal(parts);
+  std::vector<int> sms(parts, 0);
+  for (int i : order) {
+    const int p = (int)(std::min_element(sms.begin(), sms.end()) - sms.begin());
+    deal[p].push_back(grp[i]);
+    sms[p] += grp[i].sm.smCount;
+  }
+  int lo = 0, hi = 0;
+  CUE(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+  auto *set = new GreenSet;
+  set->parts.resize(parts);
+  set->busy.assign(parts, 0);
+  for (int p = 0; p < parts; ++p) {
+    CUdevResourceDesc desc;
+    CUD(A.genDesc(&desc, deal[p].data(), (unsigned)deal[p].size()));
+    GreenPart &gp = set->parts[p];
+    CUD(A.create(&gp.g, desc, dev, CU_GREEN_CTX_DEFAULT_STREAM));
+    CUstream a, b;
+    CUD(A.streamCreate(&a, gp.g, CU_STREAM_NON_BLOCKING, 0));
+    CUD(A.streamCreate(&b, gp.g, CU_STREAM_NON_BLOCKING, hi));
+    gp.lo = (cudaStream_t)a;
+    gp.hi = (cudaStream_t)b;
+    gp.sms = sms[p];
+  }
+  gs = set;
+  *out = set;
+  return GS_OK;
+}
+
 // The device pool jobs allocate from.  Growing a stream-ordered pool maps
 // fresh physical memory (measured ~5.5 ms per GiB on B200) under a driver
 // lock every worker thread then waits on, and a pool grown piecemeal by
@@ -373,6 +609,30 @@ static void prepare_pool(int device, int64_t need) {
   cudaSetDevice(prev);
 }
 
+void gs_exec_release_memory(void) {
+  std::vector<int> devs;
+  {
+    std::lock_guard<std::mutex> g(g_arena_mu);
+    for (auto &kv : g_arenas) devs.push_back(kv.first);
+  }
+  for (int d : devs) arena_drop_idle(d);
+}
+
+int gs_exec_set_sm_parts(int32_t parts) {
+  if (parts < 0 || parts > 64) return err(GS_ERR_CONFIG, "sm parts must be 0..64");
+  g_sm_parts = parts;
+  return GS_OK;
+}
+
+int gs_exec_sm_parts_layout(int32_t cuda_device, int32_t parts, int32_t *sms_out, int32_t cap, int32_t *n_out) {
+  GreenSet *set = nullptr;
+  int rc = green_for(cuda_device, parts, &set);
+  if (rc) return rc;
+  if (n_out) *n_out = (int32_t)set->parts.size();
+  for (int i = 0; i < (int)set->parts.size() && i < cap; ++i) sms_out[i] = set->parts[i].sms;
+  return GS_OK;
+}
+
 int gs_exec_ledger_capacity(int32_t cuda_device, int64_t *bytes) {
   CUE(cudaSetDevice(cuda_device));
   size_t free_b = 0, total_b = 0;
@@ -385,6 +645,7 @@ int gs_exec_ledger_capacity(int32_t cuda_device, int64_t *bytes) {
   CUE(cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &reserved));
   CUE(cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &used));
   if (reserved > used) free_b += (size_t)(reserved - used);
+  free_b += (size_t)arena_idle_bytes(cuda_device);  // the idle job arena is this run's to use
   *bytes = (int64_t)free_b - (int64_t)(6ll << 30);  // 6 GiB reserve (context, other allocators)
   return GS_OK;
 }
@@ -412,8 +673,16 @@ int gs_job_run_solo(const gs_job_desc *job, int cuda_device, int mode, void *hos
     gs_probe pr;
     if (gs_job_probe(job, &pr) == GS_OK) prepare_pool(cuda_device, pr.mem_bytes);
   }
+  // an idle job arena on the device (kept by an earlier run) holds most of
+  // its memory: a solo run allocates from it
+  gsa::Arena *ar = nullptr;
+  {
+    std::lock_guard<std::mutex> g(g_arena_mu);
+    auto it = g_arenas.find(cuda_device);
+    if (it != g_arenas.end() && it->second->reset(it->second->size())) ar = it->second;
+  }
   const auto t0 = Clock::now();
-  rc = run_job(*job, stg, mode, st, *rec, &oom, host_out, host_out_bytes, scalar, &kc, hsum, cuda_device);
+  rc = run_job(*job, stg, mode, st, *rec, &oom, host_out, host_out_bytes, scalar, &kc, hsum, cuda_device, ar, false);
   rec->end_ms = ms_since(t0);
   rec->device = cuda_device;
   rec->state = oom ? 1 : 0;
@@ -451,6 +720,14 @@ int gs_exec_run_arrivals(const gs_job_desc *jobs, int32_t n_jobs, const double *
   if (rc) return err(rc, gs_last_error());
   phase("engine open");
   std::vector<gs_device *> ledgers(n_devices, nullptr);
+  std::vector<gsa::Arena *> arenas(n_devices, nullptr);
+  std::vector<GreenSet *> greens(n_devices, nullptr);
+  const int sm_parts = g_sm_parts.load();
+  if (sm_parts > 1)
+    for (int d = 0; d < n_devices; ++d) {
+      int rc2 = green_for(cuda_devices[d], sm_parts, &greens[d]);
+      if (rc2) return rc2;
+    }
   std::vector<gs_spec> specs(n_devices);
   for (int d = 0; d < n_devices; ++d) {
     const cudaDeviceProp &prop = gscache::device_props(cuda_devices[d]);
@@ -479,6 +756,10 @@ int gs_exec_run_arrivals(const gs_job_desc *jobs, int32_t n_jobs, const double *
     if (rc) return err(rc, gs_last_error());
     specs[d] = spec;
     phase("ledger created");
+    if (arena_enabled()) {
+      arenas[d] = arena_for(cuda_devices[d], spec.mem_bytes);
+      if (arenas[d]) continue;  // jobs allocate from the arena: no pool growth
+    }
     // at most `workers` jobs hold memory at once: the pool needs the sum of
     // the largest `workers` footprints, capped by the ledger
     std::vector<int64_t> foot;
@@ -665,10 +946,23 @@ int gs_exec_run_arrivals(const gs_job_desc *jobs, int32_t n_jobs, const double *
       bool oom = false;
       const bool chain = jobs[j].kind == GS_JOB_BFS || jobs[j].kind == GS_JOB_LUD || jobs[j].kind == GS_JOB_NEEDLE;
       cudaStream_t js = chain ? hi_streams[dev] : streams[dev];
+      int part = -1;
+      if (greens[dev]) {  // an SM partition of the device for the job's whole run
+        part = greens[dev]->acquire();
+        const GreenPart &gp = greens[dev]->parts[part];
+        js = chain ? gp.hi : gp.lo;
+        set_job_sms(gp.sms);
+        rec.sm_share = gp.sms;
+      }
+      // memory-safe policies wait out arena fragmentation; sa / cg OOM
       int r = run_job(jobs[j], stg, mode, js, rec, &oom, host_out, out_cap, scalar, &kernels, hsum,
-                      cuda_devices[dev]);
+                      cuda_devices[dev], arenas[dev], task_level);
       rec.end_ms = ms_since(t0);
       rec.state = oom ? 1 : 0;
+      if (part >= 0) {
+        set_job_sms(0);
+        greens[dev]->release(part);
+      }
       std::unique_lock<std::mutex> lk(mu);
       if (r < 0 && !first_err) {
         first_err = r;

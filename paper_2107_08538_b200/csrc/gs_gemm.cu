@@ -397,7 +397,7 @@ int gemm_bf16(const void *A, int64_t lda, const void *B, int64_t ldb, const floa
   g.res = reinterpret_cast<const __nv_bfloat16 *>(res);
   g.ldr = ldr;
   g.tk = tk;
-  if (max_ctas <= 0) max_ctas = 2 * kSMs;
+  if (max_ctas <= 0) max_ctas = 2 * sm_count();
   switch (bn) {
     case 32: return launch_bn<32>(ta, tb, g, max_ctas, st);
     case 64: return launch_bn<64>(ta, tb, g, max_ctas, st);

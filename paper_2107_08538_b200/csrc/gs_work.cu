@@ -21,6 +21,7 @@
 #include <vector>
 
 #include "../../include/gs_work.h"
+#include "gs_cache.h"
 #include "gs_kernels.cuh"
 #include "gs_work_internal.h"
 
@@ -58,6 +59,15 @@ constexpr int kThreads = 256;
 
 // bitmap length of a bfs job in uint4s (n + 1 bits, whole uint4s)
 static int64_t bfs_words4(int64_t n) { return (n / 32 + 1 + 3) / 4; }
+
+thread_local int t_job_sms = 0;
+void set_job_sms(int n) { t_job_sms = n; }
+int sm_count() {
+  if (t_job_sms > 0) return t_job_sms;
+  int d = 0;
+  cudaGetDevice(&d);
+  return gscache::device_props(d).multiProcessorCount;
+}
 
 int64_t round_granule(int64_t b) { return (b + kGranule - 1) / kGranule * kGranule; }
 
@@ -139,14 +149,14 @@ int validate(const gs_job_desc &j) {
 int job_grid(const gs_job_desc &j) {
   // srad's fused kernel and kmeans' assignment are issue / latency bound:
   // 3 CTAs per SM (<= 85 registers) hide more latency than 2
-  if (j.kind == GS_JOB_SRAD) return 4 * kSMs;
-  return j.kind == GS_JOB_KMEANS ? 3 * kSMs : 2 * kSMs;
+  if (j.kind == GS_JOB_SRAD) return 4 * sm_count();
+  return j.kind == GS_JOB_KMEANS ? 3 * sm_count() : 2 * sm_count();
 }
 
 // needle: one warp per 32-row band in flight, at most the job's SM share
 int needle_grid(const gs_job_desc &j) {
   const int bands = (int)(j.n / 64);
-  return std::min(bands, 4 * kSMs);
+  return std::min(bands, 4 * sm_count());
 }
 
 std::vector<Shape> job_launches(const gs_job_desc &j) {
@@ -286,7 +296,7 @@ namespace gsw {
 // Generate a job's IN/INOUT buffers into `dst` (device pointers, one per
 // buffer; nullptr for other roles).
 int generate_inputs(const gs_job_desc &j, const std::vector<void *> &dst, cudaStream_t st) {
-  const int g = 4 * kSMs;
+  const int g = 4 * sm_count();
   const int64_t n = j.n;
   switch (j.kind) {
     case GS_JOB_BFS:
@@ -519,7 +529,7 @@ int run_kernels(const gs_job_desc &j, std::vector<void *> &buf, cudaStream_t st,
 int digest(const void *p, int64_t bytes, unsigned long long *dsum, cudaStream_t st) {
   CUW(cudaMemsetAsync(dsum, 0, 8, st));
   // dsum[1..] are the job's tile tickets (zero between kernels)
-  checksum_words<<<2 * kSMs, kThreads, 0, st>>>((const uint32_t *)p, bytes / 4, dsum,
+  checksum_words<<<2 * sm_count(), kThreads, 0, st>>>((const uint32_t *)p, bytes / 4, dsum,
                                                 reinterpret_cast<unsigned *>(dsum + 1));
   CUW(cudaGetLastError());
   return GS_OK;

@@ -13,7 +13,11 @@
 
 namespace gsw {
 
-constexpr int kSMs = 148;  // B200
+// SMs the current job's kernels may use (grids are sized from it): the
+// current device's SM count, or the job's green-context partition when the
+// executor runs it on one (set_job_sms, per worker thread; 0 = the device)
+int sm_count();
+void set_job_sms(int n);
 
 // IN staged input, INOUT staged input that is also an output, OUT output,
 // SCR zeroed scratch, WRK uninitialized workspace (fully overwritten)

@@ -32,7 +32,7 @@ class GsJobRecord(ctypes.Structure):
                 ("admit_ms", c_double),
                 ("end_ms", c_double), ("wait_ms", c_double), ("compute_ms", c_double),
                 ("mem_bytes", c_int64), ("h2d_bytes", c_int64), ("d2h_bytes", c_int64),
-                ("checksum", c_uint64), ("n_kernels", c_int32), ("pad", c_int32),
+                ("checksum", c_uint64), ("n_kernels", c_int32), ("sm_share", c_int32),
                 ("setup_ms", c_double), ("gen_ms", c_double), ("tail_ms", c_double)]
 
 
@@ -74,6 +74,9 @@ WORK_SIGNATURES = {
     "gs_exec_ledger_capacity": (c_int32, [c_int32, POINTER(c_int64)]),
     "gs_exec_unstage": (None, []),
     "gs_measure_fp32_peak": (c_int32, [c_int32, POINTER(c_double)]),
+    "gs_exec_set_sm_parts": (c_int32, [c_int32]),
+    "gs_exec_release_memory": (None, []),
+    "gs_exec_sm_parts_layout": (c_int32, [c_int32, c_int32, POINTER(c_int32), c_int32, POINTER(c_int32)]),
     "gs_exec_log": (c_int32, [c_void_p, c_int64, POINTER(c_int64), c_void_p, c_int32, POINTER(c_int32),
                               POINTER(c_int32), POINTER(c_int32)]),
     "gs_gemm_bf16": (c_int32, [c_void_p, c_int64, c_void_p, c_int64, c_void_p, c_void_p, c_int64, c_int32,
@@ -253,6 +256,25 @@ def exec_log() -> ExecLog:
     return ExecLog(list(evs)[: n.value], list(specs)[: nd.value], pol.value, ratio.value)
 
 
+def release_memory() -> None:
+    """Free the executor's idle job arenas (gs_exec_release_memory)."""
+    lib().gs_exec_release_memory()
+
+
+def set_sm_parts(parts: int) -> None:
+    """Run later jobs on `parts` disjoint green-context SM partitions per
+    device (<= 1: whole-device streams) — gs_exec_set_sm_parts."""
+    nat.check(lib().gs_exec_set_sm_parts(int(parts)))
+
+
+def sm_parts_layout(parts: int, device: int = 0) -> list[int]:
+    """SM count of each of the `parts` partitions of `device`."""
+    out = (c_int32 * 64)()
+    n = c_int32()
+    nat.check(lib().gs_exec_sm_parts_layout(device, parts, out, 64, ctypes.byref(n)))
+    return list(out)[: n.value]
+
+
 def run_jobs(jobs: list[Job], policy: str = "mgb-warps", devices: list[int] = (0,), workers: int = 8,
              mode: int = MODE_DEVICE, ledger_bytes: int = 0, arrivals_ms=None) -> ExecResult:
     """Run a job list under `policy` (wall clock; see module docstring).
@@ -274,7 +296,7 @@ def run_jobs(jobs: list[Job], policy: str = "mgb-warps", devices: list[int] = (0
                      "admit_ms": r.admit_ms, "end_ms": r.end_ms, "turnaround_ms": r.end_ms - r.arrival_ms,
                      "wait_ms": r.wait_ms, "compute_ms": r.compute_ms,
                      "mem_bytes": r.mem_bytes, "h2d_bytes": r.h2d_bytes, "d2h_bytes": r.d2h_bytes,
-                     "checksum": r.checksum, "n_kernels": r.n_kernels,
+                     "checksum": r.checksum, "n_kernels": r.n_kernels, "sm_share": r.sm_share,
                      "setup_ms": r.setup_ms, "gen_ms": r.gen_ms, "tail_ms": r.tail_ms})
     return ExecResult(rows, st.makespan_ms, st.completed, st.crashed, st.oom, st.rejected,
                       st.kernel_launches, st.decision_launches, st.decision_ms)

@@ -16,6 +16,12 @@
 __global__ void smids(int *out) {
   if (threadIdx.x == 0) { unsigned s; asm volatile("mov.u32 %0, %%smid;" : "=r"(s)); out[blockIdx.x] = (int)s; }
 }
+__global__ void big_smem(float *out) {
+  extern __shared__ float sm[];
+  sm[threadIdx.x] = threadIdx.x;
+  __syncthreads();
+  out[blockIdx.x * blockDim.x + threadIdx.x] = sm[(threadIdx.x + 1) % blockDim.x] + 100000.f / 4 * 0;
+}
 __global__ void copy4(const float4 *__restrict__ a, float4 *__restrict__ b, long n) {
   for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x) b[i] = a[i];
 }
@@ -70,6 +76,34 @@ int main() {
   RK(cudaEventRecord(e1, (cudaStream_t)s1)); RK(cudaEventRecord(f1, (cudaStream_t)s2)); RK(cudaDeviceSynchronize());
   float m1, m2; RK(cudaEventElapsedTime(&m1, e0, e1)); RK(cudaEventElapsedTime(&m2, f0, f1));
   printf("concurrent halves: %.0f + %.0f GB/s\n", 3 * 2.0 * n * 16 / (m1 * 1e-3) / 1e9, 3 * 2.0 * n * 16 / (m2 * 1e-3) / 1e9);
+  // runtime API inside a green-context stream: >48 KB dynamic smem after
+  // cudaFuncSetAttribute in the primary context, stream-ordered alloc,
+  // async copies, events, a high-priority green stream
+  {
+    int lo = 0, hi = 0;
+    RK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    std::vector<CUdevResource> r(g.begin(), g.begin() + 4);
+    CUdevResourceDesc desc; CK(cuDevResourceGenerateDesc(&desc, r.data(), 4));
+    CUgreenCtx gc; CK(cuGreenCtxCreate(&gc, desc, dev, CU_GREEN_CTX_DEFAULT_STREAM));
+    CUstream sh; CK(cuGreenCtxStreamCreate(&sh, gc, CU_STREAM_NON_BLOCKING, hi));
+    cudaStream_t st = (cudaStream_t)sh;
+    RK(cudaFuncSetAttribute(big_smem, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024));
+    float *o = nullptr;
+    RK(cudaMallocAsync((void **)&o, 1 << 20, st));
+    big_smem<<<64, 256, 100 * 1024, st>>>(o);
+    cudaError_t le = cudaGetLastError();
+    printf("big-smem launch in green stream: %s\n", cudaGetErrorString(le));
+    RK(cudaMemcpyAsync(o, a, 1 << 20, cudaMemcpyDeviceToDevice, st));
+    cudaEvent_t x0, x1; RK(cudaEventCreate(&x0)); RK(cudaEventCreate(&x1));
+    RK(cudaEventRecord(x0, st)); copy4<<<64, 512, 0, st>>>(a, b, n); RK(cudaEventRecord(x1, st));
+    RK(cudaFreeAsync(o, st));
+    cudaError_t se = cudaStreamSynchronize(st);
+    float ms = 0; RK(cudaEventElapsedTime(&ms, x0, x1));
+    printf("green stream (hi prio %d): malloc/copy/events ok=%s, 32-SM copy %.0f GB/s\n", hi,
+           se == cudaSuccess ? "yes" : cudaGetErrorString(se), 2.0 * n * 16 / (ms * 1e-3) / 1e9);
+    CUcontext cc; CK(cuCtxFromGreenCtx(&cc, gc));
+    printf("cuCtxFromGreenCtx ok\n");
+  }
   printf("ok\n");
   return 0;
 }

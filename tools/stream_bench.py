@@ -32,29 +32,10 @@ import sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
 from paper_2107_08538_b200 import catalog as C  # noqa: E402
+from paper_2107_08538_b200.catalog import CFG2_BATCHES, CFG2_RESNET, CFG2_SIZES, darknet_mix  # noqa: E402
 from paper_2107_08538_b200 import workloads as W  # noqa: E402
 
 GIB = 1 << 30
-
-
-def darknet_mix(n: int, seed: int, sizes=(416, 608, 832, 1024), batches=(1, 2, 4, 8, 16, 32, 64),
-                resnet_sizes=(224, 448)) -> list[W.Job]:
-    """Half YOLOv3-tiny, half ResNet-50 inference jobs (BASELINE cfg 2)."""
-    rng = random.Random(f"{seed}|darknet|{n}")
-    out = []
-    for i in range(n):
-        B = rng.choice(batches)
-        if rng.random() < 0.5:
-            out.append(W.Job("yolo", n=rng.choice(sizes), m=B, iters=1, seed=seed * 1000 + i))
-        else:
-            out.append(W.Job("resnet", n=rng.choice(resnet_sizes), m=B, iters=1, seed=seed * 1000 + i))
-    return out
-
-
-# cfg 2: jobs large enough that 8 co-running ones exceed the device (Darknet
-# keeps every layer's output resident: 8-33 GB per YOLO job, 7-28 GB per
-# ResNet-50 job at these sizes)
-CFG2_SIZES, CFG2_BATCHES, CFG2_RESNET = (1280, 1536, 1792), (32, 64), (896, 1152)
 
 
 def summarize(res, solo=None) -> dict:
