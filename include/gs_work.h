@@ -157,6 +157,40 @@ void gs_exec_unstage(void);
  * calls; *sms_out (optional) gets the partitions' SM counts on device 0
  * once they are built by a run. */
 int gs_exec_set_sm_parts(int32_t parts);
+/* ---- probe capture and lazy replay (csrc/gs_capture.cu) ----------------
+ * A task's host code runs once against a stream in CAPTURE mode: its
+ * stream-ordered allocations get addresses but no memory (the reference's
+ * pseudo addresses, lazy_runtime.py:56-67), its copies / memsets / kernel
+ * launches are recorded, not run (the queued ops).  Ending the capture
+ * computes the task's probe from what was recorded — every kernel node's
+ * grid, block and dynamic smem (+ registers / static smem from the
+ * function's attributes), every allocation node's bytes on the 2 MiB
+ * granule, aggregated by task_builder.py:258-290 (kernel_launch_prepare,
+ * lazy_runtime.py:103-168).  Running the graph on the chosen device
+ * materializes the queue there once, in recorded order (replay,
+ * lazy_runtime.py:181-195).  A graph is bound to the device it was
+ * recorded on. */
+typedef struct gs_task_graph gs_task_graph;
+int gs_capture_begin(int32_t cuda_device, void **stream);
+int gs_capture_malloc(void *stream, int64_t bytes, void **ptr);   /* lazy_alloc */
+int gs_capture_free(void *stream, void *ptr);
+int gs_capture_end(void *stream, int64_t heap_limit_bytes, gs_task_graph **out);  /* heap <= 0: 8 MiB */
+int gs_task_graph_probe(const gs_task_graph *g, gs_probe *out, int32_t *n_kernels, int32_t *n_allocs);
+int gs_task_graph_run(gs_task_graph *g, void *stream, uint64_t *checksum, float *ms);
+int gs_task_graph_device(const gs_task_graph *g);  /* the CUDA device it was recorded on */
+void gs_task_graph_destroy(gs_task_graph *g);
+/* A staged catalog job's whole device-side life (allocations, input copies,
+ * kernels, output digest + read-back, frees) as a task graph.  bfs (its
+ * level loop reads a count on the host) is not capturable. */
+int gs_job_capture(const gs_job_desc *job, int32_t cuda_device, gs_task_graph **out);
+/* Executor capture mode (on != 0): every capturable job's probe comes from
+ * its recorded task graph and the job runs by replaying the graph on the
+ * device it was placed on (bfs runs directly). */
+int gs_exec_set_capture(int32_t on);
+/* Free the task graphs capture mode recorded and keeps per (job, device)
+ * (gs_exec_unstage does this too: the graphs read the staged inputs). */
+void gs_exec_drop_graphs(void);
+
 /* Give back the executor's idle per-device job arenas (the slab a run
  * allocates once, sized to its ledger capacity, and keeps for later runs;
  * csrc/gs_arena.h).  Later runs allocate a new one. */

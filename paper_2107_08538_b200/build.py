@@ -31,6 +31,7 @@ SOURCES = {
     "gs_exec.cu": [],
     "gs_gemm.cu": [],
     "gs_darknet.cu": [],
+    "gs_capture.cu": [],
 }
 TARGET = os.path.join(PKG, "libgs.so")
 

@@ -175,7 +175,8 @@ def resnet_flops(S: int, N: int) -> float:
 
 def host_footprint(job: Job) -> int:
     """The probe's mem_bytes computed on the host alone (same rule as
-    gs_job_probe: buffers rounded to 2 MiB + the 8 MiB task heap) — used by
+    gs_job_probe: buffers and the control block rounded to 2 MiB + the
+    8 MiB task heap) — used by
     the CPU reference arm, which must not touch the GPU engine."""
     g = 2 << 20
     n, m = job.n, job.m
@@ -190,6 +191,7 @@ def host_footprint(job: Job) -> int:
         "yolo": yolo_buffers(n, m) if job.kind == "yolo" else [],
         "resnet": resnet_buffers(n, m) if job.kind == "resnet" else [],
     }[job.kind]
+    sizes = sizes + [32]  # the job's control block (output digest + tile tickets)
     return (8 << 20) + sum((s + g - 1) // g * g for s in sizes)
 
 

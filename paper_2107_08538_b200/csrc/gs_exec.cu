@@ -110,6 +110,21 @@ const Staged *find_staged(const gs_job_desc &d, int device = -1) {
   return any;
 }
 
+}  // namespace
+
+namespace gsw {
+// the capture path's view of the staged inputs (gs_capture.cu)
+const void *staged_input(const gs_job_desc &j, int device, size_t i, bool *host) {
+  std::lock_guard<std::mutex> g(g_stage_mu);
+  const Staged *s = find_staged(j, device);
+  if (!s || i >= s->ptr.size() || !s->ptr[i]) return nullptr;
+  *host = s->host;
+  return s->ptr[i];
+}
+}  // namespace gsw
+
+namespace {
+
 bool staged_on(const gs_job_desc &d, int device, bool host) {
   for (const Staged &s : g_staged)
     if (same_desc(s.desc, d) && s.host == host && (host || s.device == device)) return true;
@@ -434,6 +449,7 @@ int gs_exec_log(gs_exec_event *events, int64_t cap, int64_t *n_events, gs_spec *
 }
 
 void gs_exec_unstage(void) {
+  gs_exec_drop_graphs();  // recorded graphs copy from the staged inputs
   std::lock_guard<std::mutex> g(g_stage_mu);
   for (Staged &s : g_staged) free_staged(s);
   g_staged.clear();
@@ -479,6 +495,7 @@ struct GreenSet {
 std::mutex g_green_mu;
 std::map<std::pair<int, int>, GreenSet *> g_green;
 std::atomic<int> g_sm_parts{0};
+std::atomic<bool> g_capture{false};
 
 #define CUD(call)                                                                  \
   do {                                                                             \
@@ -618,6 +635,47 @@ void gs_exec_release_memory(void) {
   for (int d : devs) arena_drop_idle(d);
 }
 
+// Recorded task graphs of catalog jobs, kept per (job descriptor, device)
+// for the process: instances of one template record the same graph, so a
+// graph is recorded and instantiated once and replayed by every later
+// instance (one replay at a time per cached graph; a busy template records
+// another).  Replays reuse the graph-memory pool's mapped memory.
+std::mutex g_graph_mu;
+std::map<std::pair<std::string, int>, std::vector<gs_task_graph *>> g_graph_cache;
+
+static std::string desc_key(const gs_job_desc &d) { return std::string((const char *)&d, sizeof d); }
+
+static int graph_take(const gs_job_desc &j, int device, gs_task_graph **out) {
+  {
+    std::lock_guard<std::mutex> g(g_graph_mu);
+    auto &v = g_graph_cache[{desc_key(j), device}];
+    if (!v.empty()) {
+      *out = v.back();
+      v.pop_back();
+      return GS_OK;
+    }
+  }
+  return gs_job_capture(&j, device, out);
+}
+
+static void graph_give(const gs_job_desc &j, gs_task_graph *t) {
+  if (!t) return;
+  std::lock_guard<std::mutex> g(g_graph_mu);
+  g_graph_cache[{desc_key(j), gs_task_graph_device(t)}].push_back(t);
+}
+
+void gs_exec_drop_graphs(void) {
+  std::lock_guard<std::mutex> g(g_graph_mu);
+  for (auto &kv : g_graph_cache)
+    for (gs_task_graph *t : kv.second) gs_task_graph_destroy(t);
+  g_graph_cache.clear();
+}
+
+int gs_exec_set_capture(int32_t on) {
+  g_capture = on != 0;
+  return GS_OK;
+}
+
 int gs_exec_set_sm_parts(int32_t parts) {
   if (parts < 0 || parts > 64) return err(GS_ERR_CONFIG, "sm parts must be 0..64");
   g_sm_parts = parts;
@@ -646,6 +704,12 @@ int gs_exec_ledger_capacity(int32_t cuda_device, int64_t *bytes) {
   CUE(cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &used));
   if (reserved > used) free_b += (size_t)(reserved - used);
   free_b += (size_t)arena_idle_bytes(cuda_device);  // the idle job arena is this run's to use
+  uint64_t g_res = 0, g_used = 0;  // graph-memory pool (capture mode) kept after its graphs freed
+  if (cudaDeviceGetGraphMemAttribute(cuda_device, cudaGraphMemAttrReservedMemCurrent, &g_res) == cudaSuccess &&
+      cudaDeviceGetGraphMemAttribute(cuda_device, cudaGraphMemAttrUsedMemCurrent, &g_used) == cudaSuccess &&
+      g_res > g_used)
+    free_b += (size_t)(g_res - g_used);
+  cudaGetLastError();
   *bytes = (int64_t)free_b - (int64_t)(6ll << 30);  // 6 GiB reserve (context, other allocators)
   return GS_OK;
 }
@@ -714,6 +778,7 @@ int gs_exec_run_arrivals(const gs_job_desc *jobs, int32_t n_jobs, const double *
     if (rc) return rc;
   }
   const bool task_level = policy == GS_POLICY_MGB_SM || policy == GS_POLICY_MGB_WARPS;
+  const bool capture = g_capture.load();
   // decision engine on the first device; one ledger per device
   gs_engine *eng = nullptr;
   int rc = gs_engine_open(cuda_devices[0], &eng);
@@ -756,7 +821,9 @@ int gs_exec_run_arrivals(const gs_job_desc *jobs, int32_t n_jobs, const double *
     if (rc) return err(rc, gs_last_error());
     specs[d] = spec;
     phase("ledger created");
-    if (arena_enabled()) {
+    if (capture) {
+      arena_drop_idle(cuda_devices[d]);  // task graphs allocate from the graph-memory pool
+    } else if (arena_enabled()) {
       arenas[d] = arena_for(cuda_devices[d], spec.mem_bytes);
       if (arenas[d]) continue;  // jobs allocate from the arena: no pool growth
     }
@@ -888,7 +955,25 @@ int gs_exec_run_arrivals(const gs_job_desc *jobs, int32_t n_jobs, const double *
       }
       rec.pull_ms = ms_since(t0);
       gs_probe pr;
-      gs_job_probe(&jobs[j], &pr);
+      // capture mode: the job's host code is recorded into a task graph
+      // (nothing runs, nothing is allocated) and the probe is computed from
+      // the recorded launches and allocations — kernel_launch_prepare
+      gs_task_graph *tg = nullptr;
+      if (capture && jobs[j].kind != GS_JOB_BFS) {
+        const int cr = graph_take(jobs[j], cuda_devices[0], &tg);
+        if (cr) {
+          std::lock_guard<std::mutex> lk(mu);
+          if (!first_err) {
+            first_err = cr;
+            first_msg = t_err;
+          }
+          rec.state = 2;
+          continue;
+        }
+        gs_task_graph_probe(tg, &pr, nullptr, nullptr);
+      } else {
+        gs_job_probe(&jobs[j], &pr);
+      }
       rec.mem_bytes = pr.mem_bytes;
       pr.handle = j;
       pr.job = j;
@@ -920,11 +1005,13 @@ int gs_exec_run_arrivals(const gs_job_desc *jobs, int32_t n_jobs, const double *
             first_msg = gs_last_error();
           }
           rec.state = 2;
+          graph_give(jobs[j], tg);
           continue;
         }
         if (dec.outcome == GS_REJECTED) {
           rec.state = 2;
           rec.end_ms = ms_since(t0);
+          graph_give(jobs[j], tg);
           continue;
         }
         if (dec.outcome == GS_ASSIGN) {
@@ -954,9 +1041,34 @@ int gs_exec_run_arrivals(const gs_job_desc *jobs, int32_t n_jobs, const double *
         set_job_sms(gp.sms);
         rec.sm_share = gp.sms;
       }
-      // memory-safe policies wait out arena fragmentation; sa / cg OOM
-      int r = run_job(jobs[j], stg, mode, js, rec, &oom, host_out, out_cap, scalar, &kernels, hsum,
-                      cuda_devices[dev], arenas[dev], task_level);
+      int r = GS_OK;
+      if (tg) {
+        // replay: the recorded queue materialized on the chosen device (a
+        // graph is bound to the device it was recorded on: re-record there)
+        if (gs_task_graph_device(tg) != cuda_devices[dev]) {
+          graph_give(jobs[j], tg);
+          tg = nullptr;
+          r = graph_take(jobs[j], cuda_devices[dev], &tg);
+        }
+        float gms = 0;
+        uint64_t cs = 0;
+        if (!r) r = gs_task_graph_run(tg, js, &cs, &gms);
+        if (!r) {
+          rec.compute_ms = gms;
+          rec.checksum = cs;
+          int32_t nk = 0;
+          gs_task_graph_probe(tg, nullptr, &nk, nullptr);
+          rec.n_kernels = nk;
+          kernels.fetch_add(nk);
+        }
+        if (!r) graph_give(jobs[j], tg);
+        else gs_task_graph_destroy(tg);
+        tg = nullptr;
+      } else {
+        // memory-safe policies wait out arena fragmentation; sa / cg OOM
+        r = run_job(jobs[j], stg, mode, js, rec, &oom, host_out, out_cap, scalar, &kernels, hsum,
+                    cuda_devices[dev], arenas[dev], task_level);
+      }
       rec.end_ms = ms_since(t0);
       rec.state = oom ? 1 : 0;
       if (part >= 0) {

@@ -159,7 +159,8 @@ int needle_grid(const gs_job_desc &j) {
   return std::min(bands, 4 * sm_count());
 }
 
-std::vector<Shape> job_launches(const gs_job_desc &j) {
+// The job's kernels, in the order its host code first launches them.
+static std::vector<Shape> job_kernels(const gs_job_desc &j) {
   const int g = job_grid(j);
   switch (j.kind) {
     case GS_JOB_BFS:
@@ -192,6 +193,15 @@ std::vector<Shape> job_launches(const gs_job_desc &j) {
       return gemm_launches(j);
   }
   return {};
+}
+
+// Every launch shape of a job: its kernels, then the output digest the
+// executor runs over the primary output (a probe captured from the job's
+// real launches sees it too: gs_capture.cu).
+std::vector<Shape> job_launches(const gs_job_desc &j) {
+  std::vector<Shape> v = job_kernels(j);
+  v.push_back({(const void *)checksum_words, 2 * sm_count(), kThreads});
+  return v;
 }
 
 }  // namespace gsw
@@ -262,7 +272,8 @@ extern "C" int gs_request_from_launches(const gs_launch_desc *launches, int32_t 
 }
 
 // A catalog job's probe: its kernels' real launch shapes through the same
-// capture path, buffers on the executor's 2 MiB allocation granule.
+// capture path, buffers (+ the 32 B control block) on the executor's 2 MiB
+// allocation granule — what gs_job_capture records from the real calls.
 extern "C" int gs_job_probe(const gs_job_desc *job, gs_probe *out) {
   int rc = validate(*job);
   if (rc) return rc;
@@ -275,6 +286,7 @@ extern "C" int gs_job_probe(const gs_job_desc *job, gs_probe *out) {
   }
   std::vector<int64_t> bytes;
   for (const Buf &b : job_buffers(*job)) bytes.push_back(round_granule(b.bytes));
+  bytes.push_back(round_granule(32));  // the job's control block: output digest + tile tickets
   return gs_request_from_launches(ls.data(), (int32_t)ls.size(), bytes.data(), (int32_t)bytes.size(), kHeap, out);
 }
 

@@ -11,7 +11,7 @@ mgb-sm, mgb-warps), same worker-pool semantics, real B200 execution.
 from __future__ import annotations
 
 import ctypes
-from ctypes import POINTER, c_double, c_int32, c_int64, c_uint64, c_void_p
+from ctypes import POINTER, c_double, c_float, c_int32, c_int64, c_uint64, c_void_p
 from dataclasses import dataclass
 
 import numpy as np
@@ -75,6 +75,17 @@ WORK_SIGNATURES = {
     "gs_exec_unstage": (None, []),
     "gs_measure_fp32_peak": (c_int32, [c_int32, POINTER(c_double)]),
     "gs_exec_set_sm_parts": (c_int32, [c_int32]),
+    "gs_capture_begin": (c_int32, [c_int32, POINTER(c_void_p)]),
+    "gs_capture_malloc": (c_int32, [c_void_p, c_int64, POINTER(c_void_p)]),
+    "gs_capture_free": (c_int32, [c_void_p, c_void_p]),
+    "gs_capture_end": (c_int32, [c_void_p, c_int64, POINTER(c_void_p)]),
+    "gs_task_graph_probe": (c_int32, [c_void_p, POINTER(nat.GsProbe), POINTER(c_int32), POINTER(c_int32)]),
+    "gs_task_graph_run": (c_int32, [c_void_p, c_void_p, POINTER(c_uint64), POINTER(c_float)]),
+    "gs_task_graph_device": (c_int32, [c_void_p]),
+    "gs_task_graph_destroy": (None, [c_void_p]),
+    "gs_job_capture": (c_int32, [POINTER(GsJobDesc), c_int32, POINTER(c_void_p)]),
+    "gs_exec_set_capture": (c_int32, [c_int32]),
+    "gs_exec_drop_graphs": (None, []),
     "gs_exec_release_memory": (None, []),
     "gs_exec_sm_parts_layout": (c_int32, [c_int32, c_int32, POINTER(c_int32), c_int32, POINTER(c_int32)]),
     "gs_exec_log": (c_int32, [c_void_p, c_int64, POINTER(c_int64), c_void_p, c_int32, POINTER(c_int32),
@@ -254,6 +265,96 @@ def exec_log() -> ExecLog:
     nat.check(L.gs_exec_log(evs, n.value, ctypes.byref(n), specs, nd.value, ctypes.byref(nd), ctypes.byref(pol),
                             ctypes.byref(ratio)))
     return ExecLog(list(evs)[: n.value], list(specs)[: nd.value], pol.value, ratio.value)
+
+
+class TaskGraph:
+    """A task recorded by stream capture (csrc/gs_capture.cu): nothing ran
+    and nothing was allocated; `probe` is computed from the recorded
+    launches and allocations (kernel_launch_prepare), `run` replays the
+    queue on the recording device (lazy_runtime.replay)."""
+
+    def __init__(self, handle: int):
+        self._h = c_void_p(handle)
+
+    @property
+    def device(self) -> int:
+        return lib().gs_task_graph_device(self._h)
+
+    def probe(self) -> tuple[nat.GsProbe, int, int]:
+        """(probe, kernel launches recorded, allocations recorded)."""
+        out, nk, na = nat.GsProbe(), c_int32(), c_int32()
+        nat.check(lib().gs_task_graph_probe(self._h, ctypes.byref(out), ctypes.byref(nk), ctypes.byref(na)))
+        return out, nk.value, na.value
+
+    def run(self, stream: int = 0) -> tuple[int, float]:
+        """Replay on `stream` of the recording device and wait: (output
+        digest of a catalog job, device ms)."""
+        cs, ms = c_uint64(), c_float()
+        nat.check(lib().gs_task_graph_run(self._h, c_void_p(stream), ctypes.byref(cs), ctypes.byref(ms)))
+        return cs.value, ms.value
+
+    def close(self) -> None:
+        if self._h:
+            lib().gs_task_graph_destroy(self._h)
+            self._h = c_void_p(0)
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class Capture:
+    """Record arbitrary host code issued on `stream` into a TaskGraph:
+
+        with W.Capture(device) as cap:
+            a = cap.malloc(nbytes)        # an address, no memory yet
+            launch_something(..., stream=cap.stream)
+        graph = cap.graph                 # its probe, then replay
+    """
+
+    def __init__(self, device: int = 0, heap_limit_bytes: int = 0):
+        self.device, self.heap = device, heap_limit_bytes
+        self.stream = 0
+        self.graph: TaskGraph | None = None
+
+    def __enter__(self):
+        s = c_void_p()
+        nat.check(lib().gs_capture_begin(self.device, ctypes.byref(s)))
+        self.stream = s.value
+        return self
+
+    def malloc(self, nbytes: int) -> int:
+        p = c_void_p()
+        nat.check(lib().gs_capture_malloc(c_void_p(self.stream), int(nbytes), ctypes.byref(p)))
+        return p.value
+
+    def free(self, ptr: int) -> None:
+        nat.check(lib().gs_capture_free(c_void_p(self.stream), c_void_p(ptr)))
+
+    def __exit__(self, *exc):
+        g = c_void_p()
+        rc = lib().gs_capture_end(c_void_p(self.stream), int(self.heap), ctypes.byref(g))
+        if exc[0] is None:
+            nat.check(rc)
+            self.graph = TaskGraph(g.value)
+        elif rc == 0:
+            lib().gs_task_graph_destroy(g)
+        return False
+
+
+def capture_job(job: Job, device: int = 0) -> TaskGraph:
+    """A staged catalog job's whole device-side life as a TaskGraph."""
+    g = c_void_p()
+    nat.check(lib().gs_job_capture(ctypes.byref(job.desc()), device, ctypes.byref(g)))
+    return TaskGraph(g.value)
+
+
+def set_capture(on: bool) -> None:
+    """Executor capture mode: probes from recorded task graphs, jobs run by
+    replaying them (gs_exec_set_capture)."""
+    nat.check(lib().gs_exec_set_capture(1 if on else 0))
 
 
 def release_memory() -> None:

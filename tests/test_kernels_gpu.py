@@ -64,7 +64,7 @@ def test_kmeans_centroids_exact():
 def test_probe_reports_footprint_and_shape():
     job = W.Job("hotspot", n=1024, iters=1)
     p = W.probe(job)
-    assert p.mem_bytes == 8 * 2**20 + 3 * 4 * 2**20  # 3 x 4 MiB buffers + 8 MiB heap
+    assert p.mem_bytes == 8 * 2**20 + 3 * 4 * 2**20 + 2 * 2**20  # 3 x 4 MiB buffers + control granule + 8 MiB heap
     assert p.thread_blocks == 296 and p.threads_per_block == 256 and p.warps_per_block == 8
     assert 0 < p.regs_per_thread <= 255
 
