@@ -425,7 +425,7 @@ def drive(args, devices, torch, barrier):
             sa_e2e = summarize(sr2, st2)
         W.unstage()
 
-    cfg2 = None if args.skip_cfg2 else cfg2_block(W, C, devices, workers, args.cfg2_jobs, 1)
+    cfg2 = None if args.skip_cfg2 else cfg2_block(W, C, devices, args.cfg2_workers * len(devices), args.cfg2_jobs, 1)
 
     # ---- CPU leg: oracle on a bounded sample = cpu_baseline + parity ----
     cpu_rate, outs, cpu_dt = cpu_sample(mix, args.cpu_budget)
@@ -533,7 +533,11 @@ def main() -> int:
     ap.add_argument("--policy", default="mgb-warps")
     ap.add_argument("--mix", default="3:1")
     ap.add_argument("--jobs", type=int, default=32, help="jobs per GPU")
-    ap.add_argument("--workers", type=int, default=8, help="workers per GPU")
+    # cfg 1 at 2 workers per GPU: the measured co-location optimum
+    # (profiles/coloc_sweep_r02.jsonl: jobs/s within 2 % of 8 workers, mean
+    # per-kernel slowdown 104 % instead of 691 %, lowest mean turnaround)
+    ap.add_argument("--workers", type=int, default=2, help="workers per GPU (cfg 1)")
+    ap.add_argument("--cfg2-workers", type=int, default=8, help="workers per GPU (cfg 2: memory-bound co-location)")
     ap.add_argument("--cpu-budget", type=float, default=12.0)
     ap.add_argument("--skip-e2e", action="store_true")
     ap.add_argument("--skip-sa", action="store_true")
