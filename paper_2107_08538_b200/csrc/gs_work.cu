@@ -174,7 +174,11 @@ static std::vector<Shape> job_kernels(const gs_job_desc &j) {
     case GS_JOB_SRAD:
       return {{(const void *)srad_stats, 1, kThreads}, {(const void *)srad_fused, g, kThreads}};
     case GS_JOB_KMEANS:
-      return {{(const void *)kmeans_assign_fn((int)j.m), g, kThreads}, {(const void *)kmeans_recenter, 1, kThreads}};
+    {
+      Shape a{(const void *)kmeans_assign_fn((int)j.m), g, kThreads};
+      a.dsmem = kKmSmem;
+      return {a, {(const void *)kmeans_recenter, 1, kThreads}};
+    }
     case GS_JOB_BACKPROP:
       return {{(const void *)bp_forward, g, kThreads}, {(const void *)bp_output, 1, 32 * kMaxHid},
               {(const void *)bp_adjust, g, kThreads}};
@@ -456,8 +460,9 @@ int run_kernels(const gs_job_desc &j, std::vector<void *> &buf, cudaStream_t st,
       for (int f = 0; f < nf; ++f)  // initial centroids: the first K points
         CUW(cudaMemcpy2DAsync(cent + f, nf * 4, x + (int64_t)f * n, 4, 4, GS_KMEANS_K, cudaMemcpyDeviceToDevice,
                               st));
+      CUW(cudaFuncSetAttribute(kmeans_assign_fn(nf), cudaFuncAttributeMaxDynamicSharedMemorySize, kKmSmem));
       for (int it = 0; it < j.iters; ++it) {
-        kmeans_assign_fn(nf)<<<g, kThreads, 0, st>>>(x, n, nf, cent, mem, sumq, cnt, tk);
+        kmeans_assign_fn(nf)<<<g, kThreads, kKmSmem, st>>>(x, n, nf, cent, mem, sumq, cnt, tk);
         kmeans_recenter<<<1, kThreads, 0, st>>>(cent, sumq, cnt, nf);
         launches += 2;
       }
