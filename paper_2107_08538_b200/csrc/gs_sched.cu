@@ -90,6 +90,9 @@ struct Ring {
   long long pad1[7];
   int32_t alive;
   int32_t pad2[15];
+  // globaltimer stamps of the last command (diagnostics, GS_RING_STAMPS):
+  // [0] tail seen, [1] command read, [2] executed, [3] written back, [4] done published
+  unsigned long long stamp[8];
   Cmd cmds[kRingSlots];
   gs_decision results[kRingSlots];
 };
@@ -142,7 +145,7 @@ struct KParams {
   Ring *ring;
   long long ring_idle_ns;
   int ring_sleep_ns;  // poll interval of the idle decision warp
-  int pad2;
+  int wb_mode;        // diagnostics (GS_RING_WB): 2 = system fence inside the per-command write-back
 };
 
 struct SLed {
@@ -318,36 +321,43 @@ __device__ __forceinline__ gs_residency *entry(const KDev &D, int h) {
 
 // ---- ledger staging -----------------------------------------------------
 
-__device__ __forceinline__ int dev_of_q(const KParams &p, int q) {
-  int d = 0;
-  while (d + 1 < p.n_dev && q >= (p.dev[d + 1].smem_off >> 2)) ++d;
-  return d;
-}
 
 // Copy every staged ledger block mapped->smem (in) or smem->mapped (out,
-// dirty devices only) with 16-byte accesses, 8 in flight per lane.
+// dirty devices only) with 16-byte accesses, 8 in flight per lane.  The
+// loop runs per device (warp-uniform base pointers: the device table is a
+// kernel parameter, and indexing it per lane with divergent devices
+// serialized the constant-cache reads — a dirty 64 B header cost 24 us of
+// per-command write-back in ring mode, tools/ring_bench.cpp).
 __device__ void stage(const KParams &p, int *dyn, const Smem &S, bool in, int lane) {
   int4 *sm4 = reinterpret_cast<int4 *>(dyn);
-  for (int base = 0; base < p.stage_q; base += 32 * 8) {
-    int4 r[8];
-#pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      const int q = base + k * 32 + lane;
-      if (q < p.stage_q) {
-        const int d = dev_of_q(p, q);
-        int4 *g = reinterpret_cast<int4 *>(p.dev[d].led) + (q - (p.dev[d].smem_off >> 2));
-        // write-back: the 64 B header when it changed, the per-SM arrays
-        // only when they did (mgb-warps never touches them: a 2.4 KB
-        // write-back over PCIe per command became 64 B)
-        if (in) r[k] = *g;
-        else if ((S.led[d].dirty & 2) || ((S.led[d].dirty & 1) && q - (p.dev[d].smem_off >> 2) < 4)) *g = sm4[q];
-      }
+  for (int d = 0; d < p.n_dev; ++d) {
+    const int q0 = p.dev[d].smem_off >> 2;
+    const int nq = (kLedHdrWords + 4 * p.dev[d].arr_pad) >> 2;
+    int4 *g = reinterpret_cast<int4 *>(p.dev[d].led);
+    int cnt = nq;
+    if (!in) {
+      // write-back: the 64 B header when it changed, the per-SM arrays only
+      // when they did (mgb-warps never touches them: a 2.4 KB write-back over
+      // PCIe per command became 64 B)
+      const int dirty = S.led[d].dirty;
+      cnt = (dirty & 2) ? nq : ((dirty & 1) ? 4 : 0);
     }
-    if (in) {
+    for (int base = 0; base < cnt; base += 32 * 8) {
+      int4 r[8];
 #pragma unroll
       for (int k = 0; k < 8; ++k) {
         const int q = base + k * 32 + lane;
-        if (q < p.stage_q) sm4[q] = r[k];
+        if (q < cnt) {
+          if (in) r[k] = g[q];
+          else g[q] = sm4[q0 + q];
+        }
+      }
+      if (in) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const int q = base + k * 32 + lane;
+          if (q < cnt) sm4[q0 + q] = r[k];
+        }
       }
     }
   }
@@ -1129,7 +1139,7 @@ __device__ void exec_cmd(const KParams &p, Smem &S, int *dyn, const Cmd &c, gs_d
 }
 
 // Write dirty ledgers and the scheduler state back to mapped memory.
-__device__ void writeback(const KParams &p, int *dyn, Smem &S, int lane) {
+__device__ void writeback(const KParams &p, int *dyn, Smem &S, int lane, bool fence = true) {
   led_to_stage(p, dyn, S, lane);
   stage(p, dyn, S, false, lane);
   // every lane must have read the dirty flags (inside stage) before any lane
@@ -1140,7 +1150,7 @@ __device__ void writeback(const KParams &p, int *dyn, Smem &S, int lane) {
   for (int i = lane; i < nw; i += 32)
     reinterpret_cast<int32_t *>(p.st)[i] = reinterpret_cast<const int32_t *>(&S.st)[i];
   if (lane < p.n_dev) S.led[lane].dirty = 0;
-  __threadfence_system();
+  if (fence) __threadfence_system();
   __syncwarp();
 }
 
@@ -1416,9 +1426,10 @@ __global__ void __launch_bounds__(kThreads, 1) gs_interp_kernel(KParams p) {
       long long t = 0;
       if (lane == 0) {
         const unsigned long long t0 = globaltimer();
-        // relaxed polling (no per-poll acquire fence); one acquire once the
-        // tail moved orders the command reads after it
-        while ((t = ld_relaxed_sys(&ring->tail)) <= processed) {
+        // each poll is an acquire load of the tail: the command reads are
+        // ordered after the poll that saw it (one PCIe round trip fewer than
+        // relaxed polling + a separate acquire)
+        while ((t = ld_acquire_sys(&ring->tail)) <= processed) {
           __nanosleep(p.ring_sleep_ns);
           if (globaltimer() - t0 > (unsigned long long)p.ring_idle_ns) {
             t = -1;
@@ -1426,7 +1437,8 @@ __global__ void __launch_bounds__(kThreads, 1) gs_interp_kernel(KParams p) {
           }
         }
       }
-      if (lane == 0 && t >= 0) t = ld_acquire_sys(&ring->tail);
+      unsigned long long ts[5];
+      ts[0] = globaltimer();
       t = __shfl_sync(kFull, t, 0);
       if (t < 0) break;  // idle watchdog: the host relaunches on demand
       const int slot = (int)(processed % kRingSlots);
@@ -1434,14 +1446,23 @@ __global__ void __launch_bounds__(kThreads, 1) gs_interp_kernel(KParams p) {
         reinterpret_cast<int32_t *>(&S.cmd)[lane] =
             reinterpret_cast<const volatile int32_t *>(ring->cmds + slot)[lane];
       __syncwarp();
+      ts[1] = globaltimer();
       if (S.cmd.op == OP_STOP) {
         processed++;
         break;
       }
       exec_cmd(p, S, dyn, S.cmd, ring->results + slot, lane);
-      writeback(p, dyn, S, lane);
+      ts[2] = globaltimer();
+      // no system fence here: lane 0's st.release.sys of `done` below is
+      // cumulative over the write-back the warp made before the __syncwarp
+      // ending writeback(), so the host sees ledgers and results first
+      // (GS_RING_WB=2 restores the fence, for measurement)
+      writeback(p, dyn, S, lane, p.wb_mode == 2);
+      ts[3] = globaltimer();
       processed++;
       if (lane == 0) st_release_sys(&ring->done, processed);
+      ts[4] = globaltimer();
+      if (lane < 5) ring->stamp[lane] = ts[lane];
       __syncwarp();
     }
     writeback(p, dyn, S, lane);
@@ -2225,6 +2246,13 @@ int gs_submit_batch(gs_sched *s, const gs_probe *reqs, int32_t n, gs_decision *o
 
 int gs_submit(gs_sched *s, const gs_probe *req, gs_decision *out) { return gs_submit_batch(s, req, 1, out); }
 
+// diagnostics (not in gs.h): globaltimer stamps of the ring's last command
+int gs_ring_stamps(gs_sched *s, unsigned long long *out5) {
+  if (!s || !s->ring_active) return set_err(GS_ERR_CONFIG, "ring not running");
+  for (int i = 0; i < 5; ++i) out5[i] = s->ring.h->stamp[i];
+  return GS_OK;
+}
+
 int gs_on_release(gs_sched *s, gs_decision *out, int32_t out_cap, int32_t *n_tried, int32_t *n_admitted) {
   gs_engine *eng = s->eng;
   EngineLock g(eng);
@@ -2333,7 +2361,9 @@ int gs_sched_ring_start(gs_sched *s, int32_t max_pending, int32_t max_handles, i
   s->ring_params.ring_idle_ns = 200LL * 1000 * 1000;
   {
     const char *sl = getenv("GS_RING_SLEEP_NS");
-    s->ring_params.ring_sleep_ns = sl ? atoi(sl) : 1000;
+    s->ring_params.ring_sleep_ns = sl ? atoi(sl) : 0;
+    const char *wb = getenv("GS_RING_WB");
+    s->ring_params.wb_mode = wb ? atoi(wb) : 0;
   }
   s->ring_smem = L.smem;
   if (!s->ring_stream) {
