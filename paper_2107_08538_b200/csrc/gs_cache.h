@@ -14,8 +14,11 @@ namespace gscache {
 // pinned, mapped + portable host memory (cudaHostAllocMapped | Portable)
 cudaError_t host_alloc(void **p, size_t bytes);
 void host_free(void *p, size_t bytes);
-// device memory on the current device
+// device memory on the current device; a cudaMalloc that runs out of
+// memory calls the OOM hook (the executor frees its idle job arena) and
+// retries once
 cudaError_t dev_alloc(void **p, size_t bytes);
+void set_oom_hook(void (*hook)(int device));
 void dev_free(void *p, size_t bytes, int device);
 // cudaGetDeviceProperties, queried once per device
 const cudaDeviceProp &device_props(int device);

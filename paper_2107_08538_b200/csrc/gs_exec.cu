@@ -164,6 +164,12 @@ void arena_drop_idle(int device) {
   cudaSetDevice(prev);
 }
 
+// engine-internal allocations that find the device full give the idle
+// arena back first (gs_cache.h)
+struct ArenaOomHook {
+  ArenaOomHook() { gscache::set_oom_hook(arena_drop_idle); }
+} g_arena_oom_hook;
+
 static gsa::Arena *arena_for(int device, int64_t capacity) {
   std::lock_guard<std::mutex> g(g_arena_mu);
   gsa::Arena *&a = g_arenas[device];
@@ -740,11 +746,18 @@ int gs_job_run_solo(const gs_job_desc *job, int cuda_device, int mode, void *hos
   // an idle job arena on the device (kept by an earlier run) holds most of
   // its memory: a solo run allocates from it
   gsa::Arena *ar = nullptr;
+  bool drop = false;
   {
+    gs_probe pr;
+    const int64_t need = gs_job_probe(job, &pr) == GS_OK ? pr.mem_bytes : INT64_MAX;
     std::lock_guard<std::mutex> g(g_arena_mu);
     auto it = g_arenas.find(cuda_device);
-    if (it != g_arenas.end() && it->second->reset(it->second->size())) ar = it->second;
+    if (it != g_arenas.end()) {
+      if (it->second->size() >= need && it->second->reset(it->second->size())) ar = it->second;
+      else drop = true;  // too small for this job: give its memory to the pool
+    }
   }
+  if (drop) arena_drop_idle(cuda_device);
   const auto t0 = Clock::now();
   rc = run_job(*job, stg, mode, st, *rec, &oom, host_out, host_out_bytes, scalar, &kc, hsum, cuda_device, ar, false);
   rec->end_ms = ms_since(t0);
@@ -821,14 +834,8 @@ int gs_exec_run_arrivals(const gs_job_desc *jobs, int32_t n_jobs, const double *
     if (rc) return err(rc, gs_last_error());
     specs[d] = spec;
     phase("ledger created");
-    if (capture) {
-      arena_drop_idle(cuda_devices[d]);  // task graphs allocate from the graph-memory pool
-    } else if (arena_enabled()) {
-      arenas[d] = arena_for(cuda_devices[d], spec.mem_bytes);
-      if (arenas[d]) continue;  // jobs allocate from the arena: no pool growth
-    }
-    // at most `workers` jobs hold memory at once: the pool needs the sum of
-    // the largest `workers` footprints, capped by the ledger
+    // at most `workers` jobs hold memory at once: the pool (or the arena)
+    // needs the sum of the largest `workers` footprints, capped by the ledger
     std::vector<int64_t> foot;
     foot.reserve(n_jobs);
     for (int i = 0; i < n_jobs; ++i) {
@@ -839,6 +846,15 @@ int gs_exec_run_arrivals(const gs_job_desc *jobs, int32_t n_jobs, const double *
     std::partial_sort(foot.begin(), foot.begin() + k, foot.end(), std::greater<int64_t>());
     int64_t need = 0;
     for (size_t i = 0; i < k; ++i) need += foot[i];
+    if (capture) {
+      arena_drop_idle(cuda_devices[d]);  // task graphs allocate from the graph-memory pool
+    } else if (arena_enabled()) {
+      // the slab: what the run can hold at once, capped by the ledger (a
+      // policy without a memory check then OOMs exactly when its
+      // co-running jobs exceed the ledger capacity)
+      arenas[d] = arena_for(cuda_devices[d], std::min<int64_t>(need, spec.mem_bytes));
+      if (arenas[d]) continue;  // jobs allocate from the arena: no pool growth
+    }
     // ... unless that is most of the device: one chunk that large fragments
     // under jobs of 7-42 GB (cfg 2) and, with no physical memory left to
     // grow into, an allocation that does not fit a hole stalls; such runs
