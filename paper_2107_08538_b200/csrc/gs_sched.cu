@@ -1983,13 +1983,15 @@ int sched_params(gs_sched *s, Launch &L) {
   p.drain_out = s->drain.d;
   p.drain_cap = (int32_t)s->drain.n;
   // mgb-sm: helper warps score candidate devices in parallel, each device's
-  // per-SM caps in its own buffer (GS_SM_HELPERS=0 disables, for A/B runs)
+  // per-SM caps in its own buffer.  Opt-in (GS_SM_HELPERS=n): measured on
+  // the cfg 4 sweep it did not pay — 7.77 vs 7.85 us per probe, the helpers
+  // idle at their barrier ~78 % of the samples (profiles/r02_sweep_sm_helpers.txt)
   static const int helpers_env = [] {
     const char *e = getenv("GS_SM_HELPERS");
-    return e ? atoi(e) : -1;
+    return e ? atoi(e) : 0;
   }();
   const int want = s->policy == GS_POLICY_MGB_SM && p.n_dev >= 2 ? std::min(p.n_dev, kMaxHelpers) : 0;
-  p.n_help = helpers_env >= 0 ? std::min(want, helpers_env) : want;
+  p.n_help = std::min(want, std::max(helpers_env, 0));
   if (p.n_help > 0) {
     p.help_off = p.fifo_off;
     p.fifo_off += p.n_dev * p.max_sm_pad;
