@@ -18,20 +18,20 @@ cap() {  # name regex skip cmd...
   timeout 300 $NCU -k regex:$rx -s $skip -c 1 -o $OUT/prof_$name -f "$@" > $OUT/prof_$name.log 2>&1 \
     || echo "capture $name failed/timeout" >> $OUT/prof_errors.log
 }
-cap hotspot hotspot_step2 2 python tools/debug_job.py hotspot 16384 8
-cap srad srad_fused 3 python tools/debug_job.py srad 16384 5
-cap kmeans kmeans_assign 2 python tools/debug_job.py kmeans 8000000 4 34
-cap bfs bfs_expand 8 python tools/debug_job.py bfs 48000000
-cap needle needle_bands 0 python tools/debug_job.py needle 16384
+cap hotspot hotspot_step2 2 python tools/debug_job.py hotspot 24576 8
+cap srad srad_fused 3 python tools/debug_job.py srad 24576 5
+cap kmeans kmeans_assign 2 python tools/debug_job.py kmeans 32000000 4 34
+cap bfs bfs_expand 9 python tools/debug_job.py bfs 128000000
+cap needle needle_bands 0 python tools/debug_job.py needle 24576
 cap lud lud_internal 20 python tools/debug_job.py lud 6144
 cap ludp lud_panel 20 python tools/debug_job.py lud 6144
-cap bpfwd bp_forward 1 python tools/debug_job.py backprop 32000000 2 16
-cap bpadj bp_adjust 1 python tools/debug_job.py backprop 32000000 2 16
+cap bpfwd bp_forward 1 python tools/debug_job.py backprop 48000000 2 16
+cap bpadj bp_adjust 1 python tools/debug_job.py backprop 48000000 2 16
 cap gemm gemm_bf16_tc 4 python tools/debug_job.py yolo 608 1 32
 cap decide gs_interp 0 python -c "import __graft_entry__ as g; g.smoke()"
 case " $WANT " in *" launches "*)
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 6000 --csv \
-  --log-file $OUT/launches_$TAG.csv python bench.py --steps 1 --warmup 0 --skip-e2e --skip-sa \
+  --log-file $OUT/launches_$TAG.csv python bench.py --steps 1 --warmup 0 --skip-e2e --skip-sa --skip-cfg2 \
   --cpu-budget 1 > $OUT/launches_bench_$TAG.log 2>&1 || echo "launch list failed" >> $OUT/prof_errors.log ;;
 esac
 # per-capture DRAM traffic + duration summary (for profiles/)
