@@ -335,6 +335,50 @@ def cfg2_block(W, C, devices, workers, jobs_n, seed):
     return out
 
 
+def cfg3_block(W, C, devices, workers, jobs_n, load, seed):
+    """BASELINE cfg 3 beside the headline: a stream of cfg 1 Rodinia jobs and
+    Darknet inference jobs (half each) with seeded Poisson arrivals at
+    `load` of the fleet's solo service rate; jobs synthesize their inputs
+    on the device.  Per policy: jobs/s, mean turnaround / wait and the
+    per-kernel slowdown against each job alone (metrics.py:75-79)."""
+    import random
+
+    n = jobs_n * len(devices)
+    rod = [m.job for m in C.gen_mix("3:1", n // 2, seed=seed)]
+    jobs = rod + C.darknet_mix(n - len(rod), seed + 1)
+    rng = random.Random(f"{seed}|cfg3|{n}")
+    rng.shuffle(jobs)
+    solo = {}
+    for j in jobs:
+        if j not in solo:
+            W.run_solo(j, devices[0])
+            solo[j] = W.run_solo(j, devices[0])[1].compute_ms
+    mean_ms = statistics.fmean(solo[j] for j in jobs)
+    lam = load * len(devices) / mean_ms  # jobs per ms over the fleet
+    t, arrivals = 0.0, []
+    for _ in jobs:
+        t += rng.expovariate(lam)
+        arrivals.append(t)
+    out = {"workload": f"cfg3: {n} jobs (cfg 1 Rodinia + Darknet), Poisson arrivals at {load:.0%} offered load "
+                       f"on {len(devices)} GPU(s)", "arrival_span_ms": round(arrivals[-1], 1),
+           "mean_solo_ms": round(mean_ms, 2), "workers": workers}
+    for policy in ("mgb-warps", "sa"):
+        W.run_jobs(jobs, policy=policy, devices=devices, workers=workers, arrivals_ms=arrivals)
+        res = W.run_jobs(jobs, policy=policy, devices=devices, workers=workers, arrivals_ms=arrivals)
+        done = [(j, r) for j, r in zip(jobs, res.records) if r["state"] == "done"]
+        sl = [(r["compute_ms"] / solo[j] - 1.0) * 100.0 for j, r in done if solo[j] > 0]
+        out[policy] = {"jobs_per_s": round(res.completed / (res.makespan_ms / 1000.0), 3),
+                       "completed": res.completed, "oom": res.oom,
+                       "mean_turnaround_ms": round(statistics.fmean(r["turnaround_ms"] for _, r in done), 2),
+                       "mean_wait_ms": round(statistics.fmean(r["wait_ms"] for _, r in done), 2),
+                       "kernel_slowdown_mean_pct": round(statistics.fmean(sl), 1),
+                       "kernel_slowdown_median_pct": round(statistics.median(sl), 1)}
+        log(f"cfg3 {policy}: {out[policy]}")
+    out["turnaround_speedup_vs_sa"] = round(out["sa"]["mean_turnaround_ms"] /
+                                            max(out["mgb-warps"]["mean_turnaround_ms"], 1e-9), 3)
+    return out
+
+
 def reference_arm(args, mix):
     """--impl reference: the reference's path on host cores (C port)."""
     from oracle import oracle as O
@@ -427,6 +471,7 @@ def drive(args, devices, torch, barrier):
         W.unstage()
 
     cfg2 = None if args.skip_cfg2 else cfg2_block(W, C, devices, args.cfg2_workers * len(devices), args.cfg2_jobs, 1)
+    cfg3 = None if args.skip_cfg3 else cfg3_block(W, C, devices, workers, args.cfg3_jobs, 0.7, 1)
 
     # ---- CPU leg: oracle on a bounded sample = cpu_baseline + parity ----
     cpu_rate, outs, cpu_dt = cpu_sample(mix, args.cpu_budget)
@@ -517,6 +562,8 @@ def drive(args, devices, torch, barrier):
             line["e2e"]["speedup_vs_sa"] = round(line["e2e"]["value"] / sv, 3)
     if cfg2:
         line["cfg2"] = cfg2
+    if cfg3:
+        line["cfg3"] = cfg3
     line["clocks"] = clk.summary()
     names = [mix[i].template for i, _ in outs]
     line["cpu_baseline"] = {"value": round(cpu_rate, 4), "unit": UNIT, "cores": os.cpu_count() or 1,
@@ -548,6 +595,8 @@ def main() -> int:
     ap.add_argument("--skip-sa", action="store_true")
     ap.add_argument("--skip-cfg2", action="store_true")
     ap.add_argument("--cfg2-jobs", type=int, default=32, help="cfg 2 Darknet jobs per GPU")
+    ap.add_argument("--skip-cfg3", action="store_true")
+    ap.add_argument("--cfg3-jobs", type=int, default=128, help="cfg 3 stream jobs per GPU")
     args = ap.parse_args()
     from paper_2107_08538_b200.multi import dist_env, fleet_mix, fleet_plan, max_over_ranks
 

@@ -31,7 +31,7 @@ cap gemm gemm_bf16_tc 4 python tools/debug_job.py yolo 608 1 32
 cap decide gs_interp 0 python -c "import __graft_entry__ as g; g.smoke()"
 case " $WANT " in *" launches "*)
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 6000 --csv \
-  --log-file $OUT/launches_$TAG.csv python bench.py --steps 1 --warmup 0 --skip-e2e --skip-sa --skip-cfg2 \
+  --log-file $OUT/launches_$TAG.csv python bench.py --steps 1 --warmup 0 --skip-e2e --skip-sa --skip-cfg2 --skip-cfg3 \
   --cpu-budget 1 > $OUT/launches_bench_$TAG.log 2>&1 || echo "launch list failed" >> $OUT/prof_errors.log ;;
 esac
 # per-capture DRAM traffic + duration summary (for profiles/)
