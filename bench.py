@@ -255,16 +255,31 @@ def pcie_h2d_gbps(torch) -> float:
     return 4.0 * n / (best * 1e-3) / 1e9
 
 
-def cpu_sample(mix, budget_s: float):
+def sample_order(mix) -> list[int]:
+    """Mix indices for the CPU sample: one job of every kind first (its
+    smallest template in the mix, cheapest kinds first), then the rest in mix
+    order — so a bounded sample checks every kind's parity."""
+    from paper_2107_08538_b200.catalog import host_footprint
+
+    best = {}
+    for i, mj in enumerate(mix):
+        k = mj.job.kind
+        if k not in best or host_footprint(mj.job) < host_footprint(mix[best[k]].job):
+            best[k] = i
+    first = sorted(best.values(), key=lambda i: host_footprint(mix[i].job))
+    return first + [i for i in range(len(mix)) if i not in first]
+
+
+def cpu_sample(mix, budget_s: float, order=None):
     """The oracle's CPU kernels on all host threads over a bounded sample of
-    the mix (jobs in mix order until the time budget is spent).  Returns
+    the mix (jobs in `order` until the time budget is spent).  Returns
     (jobs/s, [(mix index, oracle output)], seconds)."""
     from oracle import kernels as K
 
     t0 = time.perf_counter()
     outs = []
-    for i, mj in enumerate(mix):
-        j = mj.job
+    for i in (order if order is not None else range(len(mix))):
+        j = mix[i].job
         outs.append((i, K.run(j.kind, n=j.n, iters=j.iters, m=j.m, seed=j.seed)))
         if time.perf_counter() - t0 > budget_s:
             break
@@ -338,9 +353,9 @@ def cfg2_block(W, C, devices, workers, jobs_n, seed):
 def cfg3_block(W, C, devices, workers, jobs_n, load, seed):
     """BASELINE cfg 3 beside the headline: a stream of cfg 1 Rodinia jobs and
     Darknet inference jobs (half each) with seeded Poisson arrivals at
-    `load` of the fleet's solo service rate; jobs synthesize their inputs
-    on the device.  Per policy: jobs/s, mean turnaround / wait and the
-    per-kernel slowdown against each job alone (metrics.py:75-79)."""
+    `load` of the fleet's solo service rate; inputs staged in HBM.  Per
+    policy: jobs/s, mean turnaround / wait and the per-kernel slowdown
+    against each job alone (metrics.py:75-79)."""
     import random
 
     n = jobs_n * len(devices)
@@ -348,6 +363,10 @@ def cfg3_block(W, C, devices, workers, jobs_n, load, seed):
     jobs = rod + C.darknet_mix(n - len(rod), seed + 1)
     rng = random.Random(f"{seed}|cfg3|{n}")
     rng.shuffle(jobs)
+    # inputs resident in HBM, as for cfg 1 (unstaged jobs would time their
+    # synthetic input generation: bfs builds its transposed CSR)
+    W.stage(jobs, devices, W.MODE_DEVICE)
+    cap = min(W.ledger_capacity(d) for d in devices)
     solo = {}
     for j in jobs:
         if j not in solo:
@@ -363,8 +382,9 @@ def cfg3_block(W, C, devices, workers, jobs_n, load, seed):
                        f"on {len(devices)} GPU(s)", "arrival_span_ms": round(arrivals[-1], 1),
            "mean_solo_ms": round(mean_ms, 2), "workers": workers}
     for policy in ("mgb-warps", "sa"):
-        W.run_jobs(jobs, policy=policy, devices=devices, workers=workers, arrivals_ms=arrivals)
-        res = W.run_jobs(jobs, policy=policy, devices=devices, workers=workers, arrivals_ms=arrivals)
+        W.run_jobs(jobs, policy=policy, devices=devices, workers=workers, arrivals_ms=arrivals, ledger_bytes=cap)
+        res = W.run_jobs(jobs, policy=policy, devices=devices, workers=workers, arrivals_ms=arrivals,
+                         ledger_bytes=cap)
         done = [(j, r) for j, r in zip(jobs, res.records) if r["state"] == "done"]
         sl = [(r["compute_ms"] / solo[j] - 1.0) * 100.0 for j, r in done if solo[j] > 0]
         out[policy] = {"jobs_per_s": round(res.completed / (res.makespan_ms / 1000.0), 3),
@@ -376,6 +396,7 @@ def cfg3_block(W, C, devices, workers, jobs_n, load, seed):
         log(f"cfg3 {policy}: {out[policy]}")
     out["turnaround_speedup_vs_sa"] = round(out["sa"]["mean_turnaround_ms"] /
                                             max(out["mgb-warps"]["mean_turnaround_ms"], 1e-9), 3)
+    W.unstage()
     return out
 
 
@@ -474,7 +495,7 @@ def drive(args, devices, torch, barrier):
     cfg3 = None if args.skip_cfg3 else cfg3_block(W, C, devices, workers, args.cfg3_jobs, 0.7, 1)
 
     # ---- CPU leg: oracle on a bounded sample = cpu_baseline + parity ----
-    cpu_rate, outs, cpu_dt = cpu_sample(mix, args.cpu_budget)
+    cpu_rate, outs, cpu_dt = cpu_sample(mix, args.cpu_budget, sample_order(mix))
     parity = parity_check(W, mix, last_records, outs, devices[0])
     n_dec, bad = O.replay_exec_log(xlog)
     placements = {"decisions": n_dec, "mismatches": len(bad), "detail": bad[:3],
@@ -590,7 +611,7 @@ def main() -> int:
     # e2e is PCIe-bound: more jobs in flight keep the copy engines busy
     # (8 workers: 88 % of the measured H2D peak, 2 workers: 79 %)
     ap.add_argument("--e2e-workers", type=int, default=8, help="workers per GPU (e2e mode)")
-    ap.add_argument("--cpu-budget", type=float, default=12.0)
+    ap.add_argument("--cpu-budget", type=float, default=20.0)
     ap.add_argument("--skip-e2e", action="store_true")
     ap.add_argument("--skip-sa", action="store_true")
     ap.add_argument("--skip-cfg2", action="store_true")

@@ -259,6 +259,14 @@ int run_job(const gs_job_desc &j, const Staged *stg, int mode, cudaStream_t st, 
   // the job's heap allowance)
   std::vector<int64_t> req;
   std::vector<void *> got;
+  std::vector<int> slot(bufs.size(), -1);  // buffer -> arena request index
+  // Read-only inputs (IN) of a job whose inputs are resident on its own
+  // GPU are read in place: the job's kernels never write an IN buffer, so
+  // copying 50 GB of them per cfg 1 step D2D was pure HBM traffic.  INOUT
+  // buffers (modified in place) still get a private copy.
+  std::vector<char> alias(bufs.size(), 0);
+  if (stg && !stg->host && stg->device == device)
+    for (size_t i = 0; i < bufs.size(); ++i) alias[i] = bufs[i].role == IN && stg->ptr[i] != nullptr;
   auto release = [&]() {
     if (arena) {
       cudaStreamSynchronize(st);
@@ -266,13 +274,17 @@ int run_job(const gs_job_desc &j, const Staged *stg, int mode, cudaStream_t st, 
       got.clear();
       return;
     }
-    for (void *p : buf)
-      if (p) cudaFreeAsync(p, st);
+    for (size_t i = 0; i < buf.size(); ++i)
+      if (buf[i] && !alias[i]) cudaFreeAsync(buf[i], st);
     if (dsum) cudaFreeAsync(dsum, st);
     cudaStreamSynchronize(st);
   };
   if (arena) {
-    for (const Buf &b : bufs) req.push_back(b.bytes);
+    for (size_t i = 0; i < bufs.size(); ++i)
+      if (!alias[i]) {
+        slot[i] = (int)req.size();
+        req.push_back(bufs[i].bytes);
+      }
     req.push_back(32);
     double waited = 0;
     if (!arena->alloc_all(req, got, wait_mem, &waited)) {
@@ -280,10 +292,14 @@ int run_job(const gs_job_desc &j, const Staged *stg, int mode, cudaStream_t st, 
       *oom = true;
       return GS_OK;
     }
-    for (size_t i = 0; i < bufs.size(); ++i) buf[i] = got[i];
+    for (size_t i = 0; i < bufs.size(); ++i) buf[i] = alias[i] ? stg->ptr[i] : got[slot[i]];
     dsum = (unsigned long long *)got.back();
   }
   for (size_t i = 0; i < bufs.size() && !arena; ++i) {
+    if (alias[i]) {
+      buf[i] = stg->ptr[i];
+      continue;
+    }
     const auto ta = Clock::now();
     cudaError_t e = cudaMallocAsync(&buf[i], bufs[i].bytes, st);
     if (g_alloc_log && ms_since(ta) > 5.0)
@@ -338,6 +354,7 @@ int run_job(const gs_job_desc &j, const Staged *stg, int mode, cudaStream_t st, 
   CUE(cudaMemsetAsync(dsum, 0, 32, st));
   // inputs in
   for (size_t i = 0; i < bufs.size(); ++i) {
+    if (alias[i]) continue;  // read in place
     if (bufs[i].role == IN || bufs[i].role == INOUT) {
       if (stg) {
         if (stg->host) {
