@@ -53,7 +53,9 @@ def test_live_placements_with_deferrals_match_oracle(policy):
 
 def test_live_placements_two_ledgers_and_arrivals_match_oracle():
     cap = W.ledger_capacity(0) // 4
-    arrivals = [3.0 * i for i in range(len(MIX))]
+    # a batch of four at t = 0 (co-resident: mgb-warps spreads them over both
+    # ledgers), then one arrival every 3 ms
+    arrivals = [0.0 if i < 4 else 3.0 * i for i in range(len(MIX))]
     res = W.run_jobs(MIX, policy="mgb-warps", devices=[0, 0], workers=8, ledger_bytes=cap, arrivals_ms=arrivals)
     assert res.completed == len(MIX)
     log = _check(res, len(MIX))
