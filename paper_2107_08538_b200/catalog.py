@@ -102,6 +102,12 @@ YOLO_CONVS = [(1, 3, 16, 3), (2, 16, 32, 3), (4, 32, 64, 3), (8, 64, 128, 3), (1
               (32, 256, 128, 1), (16, 384, 256, 3), (16, 256, 255, 1)]
 
 
+def implicit_conv(cin: int, k: int) -> bool:
+    """The executor runs this convolution as an implicit GEMM (no im2row
+    workspace): csrc/gs_darknet.cu NetBuilder::implicit_conv."""
+    return k in (1, 3) and cin in (8, 16, 32, 64, 128)
+
+
 def yolo_buffers(S: int, N: int) -> list[int]:
     """Byte sizes of the YOLOv3-tiny job's buffers (yolo_plan order)."""
     act = lambda d, c: N * (S // d) ** 2 * c * 2  # noqa: E731  bf16 NHWC
@@ -110,7 +116,7 @@ def yolo_buffers(S: int, N: int) -> list[int]:
     for d, cin, cout, k in YOLO_CONVS:
         kpad = (k * k * cin + 7) // 8 * 8
         w = (w + cout * kpad + 7) // 8 * 8
-        if k != 1:
+        if k != 1 and not implicit_conv(cin, k):
             ws = max(ws, N * (S // d) ** 2 * kpad * 2)
     bias = sum(c[2] for c in YOLO_CONVS) * 4
     det = (N * (S // 32) ** 2 + N * (S // 16) ** 2) * 255 * 4
@@ -155,7 +161,7 @@ def resnet_buffers(S: int, N: int) -> list[int]:
         w = (w + cout * kpad + 7) // 8 * 8
         b += cout
         ohw = hw // stride if kind == "act" else 1
-        if not (k == 1 and stride == 1):
+        if not (k == 1 and stride == 1) and not implicit_conv(cin, k):
             ws = max(ws, N * ohw * ohw * kpad * 2)
         if kind == "act":
             acts.append(N * ohw * ohw * cout * 2)

@@ -104,7 +104,7 @@ struct NetBuilder {
     wcount = (wcount + 7) / 8 * 8;  // 16-byte aligned next layer
     bcount += cout;
     const int64_t opix = (int64_t)out.n * out.h * out.w;
-    if (!direct_gemm(L)) ws = std::max(ws, opix * L.kpad * 2);
+    if (!direct_gemm(L) && !implicit_conv(L)) ws = std::max(ws, opix * L.kpad * 2);  // the im2row matrix
     P.flops += 2 * opix * (int64_t)L.kdim * cout;
     P.layers.push_back(L);
     return out;
@@ -112,6 +112,22 @@ struct NetBuilder {
   // a 1x1 / stride-1 convolution reads the activation itself as the GEMM's A
   static bool direct_gemm(const LPlan &L) {
     return L.k == 1 && L.stride == 1 && L.in.pitch % 8 == 0 && L.in.off % 8 == 0;
+  }
+  // a k = 1 / 3 convolution over 2^j = 8 .. 128 channels runs as an
+  // implicit GEMM (gemm_bf16_tc<BN, true> gathers A from the activation; no
+  // im2row).  Measured per YOLO layer at 608^2 x 32 (ncu, us, im2row + GEMM
+  // -> implicit): C 16: 713 -> 472, 32: 334 -> 200, 64: 212 -> 116, 128:
+  // 126 -> 112, but 256: 80 -> 116 and 512: 158 -> 330 — with deep K the
+  // two gather warps cannot feed the tensor cores the way the TMA does, so
+  // wide layers keep im2row + the TMA GEMM.
+  static bool implicit_conv(const LPlan &L) {
+    static const bool off = [] {
+      const char *e = getenv("GS_IM2ROW");
+      return e && e[0] == '1';
+    }();
+    const int c = L.in.c;
+    return !off && !direct_gemm(L) && (L.k == 1 || L.k == 3) && c >= 8 && c <= 128 && (c & (c - 1)) == 0 &&
+           L.in.pitch % 8 == 0 && L.in.off % 8 == 0 && L.kpad == L.kdim;
   }
   TView pool(const TView &in, int k, int stride, int pad, int ho, int wo) {
     TView out = act(ho, wo, in.c);
@@ -507,7 +523,9 @@ std::vector<Shape> gemm_launches(const gs_job_desc &j) {
   const int64_t pix0 = (int64_t)j.m * j.n * j.n;
   Shape g{gemm_kernel_fn(bn_max), 2 * sm_count(), gemm_block_threads()};
   g.dsmem = (int)gemm_smem_for(bn_max);
-  std::vector<Shape> v = {g, {(const void *)im2row, grid_for(pix0 * 4), kThr},
+  Shape gc{conv_kernel_fn(bn_max), 2 * sm_count(), conv_block_threads()};
+  gc.dsmem = (int)gemm_smem_for(bn_max);
+  std::vector<Shape> v = {g, gc, {(const void *)im2row, grid_for(pix0 * 4), kThr},
                           {(const void *)maxpool, grid_for(pix0), kThr}};
   if (j.kind == GS_JOB_YOLO) v.push_back({(const void *)conv3x3_direct<3, 16>, grid_for(pix0), kThr});
   else v.push_back({(const void *)avgpool, grid_for(pix0), kThr});
@@ -563,6 +581,18 @@ int gemm_run(const gs_job_desc &j, std::vector<void *> &buf, cudaStream_t st, in
         // for im2row + GEMM at 608^2 x 32; for 16 -> 32 the GEMM path is faster)
         conv3x3_direct<3, 16><<<grid_for(opix), kThr, 0, st>>>(in, (const __nv_bfloat16 *)buf[B_W] + L.woff, L.kpad,
                                                                (const float *)buf[B_BIAS] + L.boff, obf, L.out.pitch);
+        ++*launches;
+        continue;
+      }
+      void *cout_p = L.out.f32 ? (void *)((float *)buf[L.out.buf] + L.out.off) : (void *)obf;
+      const void *cres =
+          L.res.buf >= 0 ? (const void *)((const __nv_bfloat16 *)buf[L.res.buf] + L.res.off) : nullptr;
+      if (NetBuilder::implicit_conv(L)) {
+        int rc = conv_gemm_bf16(in.p, L.in.n, L.in.h, L.in.w, L.in.pitch, __builtin_ctz(L.in.c), L.out.h, L.out.w,
+                                L.k, L.stride, L.pad, (const __nv_bfloat16 *)buf[B_W] + L.woff, L.kpad,
+                                (const float *)buf[B_BIAS] + L.boff, cout_p, L.out.pitch, L.cout, L.out.f32 ? 1 : 0,
+                                L.act, 2 * sm_count(), st, cres, L.res.pitch, tk);
+        if (rc) return rc;
         ++*launches;
         continue;
       }

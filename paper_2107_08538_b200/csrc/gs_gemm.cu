@@ -41,6 +41,12 @@ struct GemmArgs {
   const __nv_bfloat16 *res;  // residual added before the activation (bf16, pitch ldr) or nullptr
   int64_t ldr;
   unsigned *tk;          // the job's tile tickets (gs_kernels.cuh grab_tile) or nullptr: static striding
+  // implicit convolution (gemm_bf16_tc<BN, true>): A is not a matrix in
+  // memory but the im2row view of an NHWC activation, gathered per stage
+  const __nv_bfloat16 *cin;  // the activation (its channel offset applied)
+  int cn, ch, cw, cpitch;    // batch, input height / width, pixel pitch (elements)
+  int clog2c;                // log2(channels): channels are a power of two >= 8
+  int coh, cow, ck, cstride, cpad, ckdim;  // output h / w, kernel (1 or 3), stride, pad, k*k*C
 };
 
 // 3 stages x (16 KB A + <= 16 KB B) <= 99 KB: two CTAs per SM, so one CTA's
@@ -54,6 +60,7 @@ constexpr size_t gemm_smem_bytes() {
 }
 
 constexpr int kGemmThreads = 192;  // warp 0 TMA, warp 1 MMA, warps 2-5 epilogue
+constexpr int kConvThreads = 256;  // + warps 6-7 gathering A (implicit convolution)
 
 __device__ __forceinline__ float leaky(float v) { return v > 0.0f ? v : 0.1f * v; }
 // YOLO layer (Darknet yolo_layer forward): logistic on x, y, objectness and
@@ -61,6 +68,20 @@ __device__ __forceinline__ float leaky(float v) { return v > 0.0f ? v : 0.1f * v
 __device__ __forceinline__ float yolo_act(float v, int col) {
   const int e = col % 85;
   return (e == 2 || e == 3) ? v : 1.0f / (1.0f + expf(-v));
+}
+
+// 16-byte global -> shared copy, zero-filled when src_bytes == 0 (padding,
+// rows past M, columns past K)
+__device__ __forceinline__ void cp_async16_zfill(uint32_t dst, const void *src, int src_bytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(src_bytes) : "memory");
+}
+// arrive on `bar` when every cp.async this thread issued so far has landed
+// (the barrier's expected count includes these arrivals)
+__device__ __forceinline__ void cp_async_mbar_arrive(uint64_t *bar) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(tc::smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 
 __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
@@ -157,9 +178,19 @@ __device__ __forceinline__ int gemm_next_tile(const GemmArgs &g, int i, int tile
 // operand ring across tile boundaries, the MMA warp alternates between two
 // TMEM accumulators, and the four epilogue warps drain accumulator t while
 // the MMAs of tile t+1 run.
-template <int BN>
-__global__ void __launch_bounds__(kGemmThreads, 2) gemm_bf16_tc(const __grid_constant__ CUtensorMap ta,
-                                                                const __grid_constant__ CUtensorMap tb, GemmArgs g) {
+//
+// CONV = true: the implicit convolution.  A's stage is gathered by two extra
+// warps (6, 7) straight from the NHWC activation with 16-byte cp.async into
+// the 128-byte-swizzled K-major layout the TMA would have written (chunk j of
+// tile row r at r * 128 + ((j ^ (r & 7)) << 4)), zero-filled at the padding
+// and past M / K; each gather thread's cp.async completion arrives on the
+// stage's barrier (expected count 1 + 64), and the MMA thread issues a proxy
+// fence before its tensor-core reads.  K order (ky, kx, c) is im2row's, so
+// the products equal im2row + GEMM's exactly — without writing and
+// re-reading the im2row matrix (30-39 % of a Darknet job).
+template <int BN, bool CONV = false>
+__global__ void __launch_bounds__(CONV ? kConvThreads : kGemmThreads, 2)
+    gemm_bf16_tc(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tb, GemmArgs g) {
   using namespace tc;
   constexpr uint32_t A_BYTES = kGemmBM * kGemmBK * 2, B_BYTES = BN * kGemmBK * 2;
   constexpr uint32_t TM_COLS = 2 * BN < 32 ? 32 : 2 * BN;  // two accumulators
@@ -178,10 +209,10 @@ __global__ void __launch_bounds__(kGemmThreads, 2) gemm_bf16_tc(const __grid_con
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   if (warp == 0 && lane == 0) {
-    tma_prefetch(&ta);
+    if (!CONV) tma_prefetch(&ta);
     tma_prefetch(&tb);
     for (int s = 0; s < kGemmStages; ++s) {
-      mbar_init(&full[s], 1);
+      mbar_init(&full[s], CONV ? 1 + 64 : 1);
       mbar_init(&empty[s], 1);
     }
     for (int a = 0; a < 2; ++a) {
@@ -190,7 +221,7 @@ __global__ void __launch_bounds__(kGemmThreads, 2) gemm_bf16_tc(const __grid_con
     }
     for (int s = 0; s < 4; ++s) {
       mbar_init(&tq_full[s], 1);
-      mbar_init(&tq_empty[s], 5);
+      mbar_init(&tq_empty[s], CONV ? 7 : 5);
     }
     fence_mbar_init();
   }
@@ -214,8 +245,8 @@ __global__ void __launch_bounds__(kGemmThreads, 2) gemm_bf16_tc(const __grid_con
         const int mt = tile / g.n_tiles, nt = tile % g.n_tiles;
         for (int kb = 0; kb < g.k_blocks; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
-          mbar_expect_tx(&full[stage], A_BYTES + B_BYTES);
-          tma_load_2d(sa + stage * A_BYTES, &ta, &full[stage], kb * kGemmBK, mt * kGemmBM);
+          mbar_expect_tx(&full[stage], CONV ? B_BYTES : A_BYTES + B_BYTES);
+          if (!CONV) tma_load_2d(sa + stage * A_BYTES, &ta, &full[stage], kb * kGemmBK, mt * kGemmBM);
           tma_load_2d(sb + stage * B_BYTES, &tb, &full[stage], kb * kGemmBK, nt * BN);
           if (++stage == kGemmStages) {
             stage = 0;
@@ -238,6 +269,7 @@ __global__ void __launch_bounds__(kGemmThreads, 2) gemm_bf16_tc(const __grid_con
         const uint32_t d = tmem + acc * BN;
         for (int kb = 0; kb < g.k_blocks; ++kb) {
           mbar_wait(&full[stage], phase);
+          if (CONV) fence_proxy_async_smem();  // the gathered A was written by cp.async (generic proxy)
           tc_fence_after();
           const uint64_t ad = sdesc_k_sw128(sa + stage * A_BYTES);
           const uint64_t bd = sdesc_k_sw128(sb + stage * B_BYTES);
@@ -252,6 +284,58 @@ __global__ void __launch_bounds__(kGemmThreads, 2) gemm_bf16_tc(const __grid_con
         mma_commit(&acc_full[acc]);  // accumulator ready for the epilogue
       }
     }
+  } else if (CONV && warp >= 6) {
+    // A gather (implicit im2row): 64 threads, tile rows gt and gt + 64
+    const int gt = (int)threadIdx.x - 192;
+    const int cmask = (1 << g.clog2c) - 1;
+    uint32_t stage = 0, phase = 0;
+    for (int i = 0;; ++i) {
+      mbar_wait(&tq_full[i & 3], (i >> 2) & 1);
+      const int tile = tq[i & 3];
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tq_empty[i & 3]);
+      if (tile >= tiles) break;
+      const int mt = tile / g.n_tiles;
+      int iy0[2], ix0[2];
+      bool valid[2];
+      const __nv_bfloat16 *img[2];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int m = mt * kGemmBM + gt + 64 * h;
+        valid[h] = m < g.m;
+        const int mm = valid[h] ? m : 0;
+        const int t2 = mm / g.cow, ox = mm - t2 * g.cow;
+        const int b = t2 / g.coh, oy = t2 - b * g.coh;
+        iy0[h] = oy * g.cstride - g.cpad;
+        ix0[h] = ox * g.cstride - g.cpad;
+        img[h] = g.cin + (int64_t)b * g.ch * g.cw * g.cpitch;
+      }
+      for (int kb = 0; kb < g.k_blocks; ++kb) {
+        mbar_wait(&empty[stage], phase ^ 1);
+        const uint32_t dst = smem_u32(sa + stage * A_BYTES);
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int r = gt + 64 * h;
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const int k = kb * kGemmBK + j * 8;
+            const int tap = k >> g.clog2c, c = k & cmask;
+            const int ky = g.ck == 1 ? 0 : (tap * 11) >> 5;  // tap / 3 for tap < 9
+            const int kx = tap - ky * g.ck;
+            const int iy = iy0[h] + ky, ix = ix0[h] + kx;
+            const bool ok = valid[h] && k < g.ckdim && iy >= 0 && iy < g.ch && ix >= 0 && ix < g.cw;
+            const __nv_bfloat16 *src = ok ? img[h] + ((int64_t)iy * g.cw + ix) * g.cpitch + c : g.cin;
+            cp_async16_zfill(dst + r * 128 + ((j ^ (r & 7)) << 4), src, ok ? 16 : 0);
+          }
+        }
+        cp_async_mbar_arrive(&full[stage]);
+        if (++stage == kGemmStages) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+    }
+    asm volatile("cp.async.wait_all;" ::: "memory");
   } else {
     // epilogue warps 2..5: TMEM lane quarter (warp % 4) = tile rows 32q .. 32q+31
     const int q = warp & 3;
@@ -338,17 +422,18 @@ int make_tmap_f32(CUtensorMap *m, const void *ptr, int64_t rows, int64_t cols, i
   return GS_OK;
 }
 
-template <int BN>
+template <int BN, bool CONV = false>
 static int launch_bn(const CUtensorMap &ta, const CUtensorMap &tb, GemmArgs g, int max_ctas, cudaStream_t st) {
   // the attribute is per device (the executor may drive several); set it on
   // a device's first launch only -- a driver call per launch serializes the
   // executor's worker threads on the context lock
-  static std::atomic<uint64_t> configured{0};
+  static std::atomic<uint64_t> configured{0};  // (one per <BN, CONV> instance)
   int dev = 0;
   cudaGetDevice(&dev);
   const uint64_t bit = 1ull << (dev & 63);
   if (!(configured.load(std::memory_order_acquire) & bit)) {
-    const cudaError_t attr_rc = cudaFuncSetAttribute(gemm_bf16_tc<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    const cudaError_t attr_rc = cudaFuncSetAttribute(gemm_bf16_tc<BN, CONV>,
+                                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                      (int)gemm_smem_bytes<BN>());
     if (attr_rc != cudaSuccess)
       return err(GS_ERR_CUDA, std::string("gemm smem attribute: ") + cudaGetErrorString(attr_rc));
@@ -357,7 +442,7 @@ static int launch_bn(const CUtensorMap &ta, const CUtensorMap &tb, GemmArgs g, i
   g.n_tiles = (g.n + BN - 1) / BN;
   const int tiles = g.m_tiles * g.n_tiles;
   const int grid = tiles < max_ctas ? tiles : max_ctas;
-  gemm_bf16_tc<BN><<<grid, kGemmThreads, gemm_smem_bytes<BN>(), st>>>(ta, tb, g);
+  gemm_bf16_tc<BN, CONV><<<grid, CONV ? kConvThreads : kGemmThreads, gemm_smem_bytes<BN>(), st>>>(ta, tb, g);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return err(GS_ERR_CUDA, std::string("gemm launch: ") + cudaGetErrorString(e));
   return GS_OK;
@@ -384,6 +469,7 @@ int gemm_bf16(const void *A, int64_t lda, const void *B, int64_t ldb, const floa
   rc = make_tmap(&tb, B, n, k, ldb, bn);
   if (rc) return rc;
   GemmArgs g;
+  memset(&g, 0, sizeof g);
   g.m = m;
   g.n = n;
   g.m_tiles = (m + kGemmBM - 1) / kGemmBM;
@@ -405,6 +491,67 @@ int gemm_bf16(const void *A, int64_t lda, const void *B, int64_t ldb, const floa
     default: return launch_bn<256>(ta, tb, g, max_ctas, st);
   }
 }
+
+// Implicit convolution: D[pixels x cout] = act(conv(in, W) + bias), the
+// im2row matrix never materialized.  `in` is an NHWC view (pitch elements
+// per pixel, C = 2^log2c channels, C >= 8), W [cout x k*k*C] (pitch ldb),
+// k = 1 (with a stride) or 3.
+int conv_gemm_bf16(const void *in, int nb, int h, int w, int pitch, int log2c, int oh, int ow, int k, int stride,
+                   int pad, const void *B, int64_t ldb, const float *bias, void *out, int64_t ldo, int cout,
+                   int out_f32, int act, int max_ctas, cudaStream_t st, const void *res, int64_t ldr, unsigned *tk) {
+  if (log2c < 3 || (k != 1 && k != 3)) return err(GS_ERR_CONFIG, "implicit conv needs C = 2^k >= 8 and k in {1, 3}");
+  if (pitch % 8 || (reinterpret_cast<uintptr_t>(in) & 15)) return err(GS_ERR_CONFIG, "implicit conv needs 16-byte pixels");
+  const int64_t m64 = (int64_t)nb * oh * ow;
+  if (m64 >= (1ll << 31)) return err(GS_ERR_CONFIG, "implicit conv: too many output pixels");
+  const int m = (int)m64, kdim = k * k * (1 << log2c);
+  const int bn = gemm_pick_bn(m, cout);
+  CUtensorMap tb;
+  int rc = make_tmap(&tb, B, cout, kdim, ldb, bn);
+  if (rc) return rc;
+  GemmArgs g;
+  memset(&g, 0, sizeof g);
+  g.m = m;
+  g.n = cout;
+  g.m_tiles = (m + kGemmBM - 1) / kGemmBM;
+  g.k_blocks = (kdim + kGemmBK - 1) / kGemmBK;
+  g.bias = bias;
+  g.out = out;
+  g.ldo = ldo;
+  g.out_f32 = out_f32;
+  g.act = act;
+  g.res = reinterpret_cast<const __nv_bfloat16 *>(res);
+  g.ldr = ldr;
+  g.tk = tk;
+  g.cin = reinterpret_cast<const __nv_bfloat16 *>(in);
+  g.cn = nb;
+  g.ch = h;
+  g.cw = w;
+  g.cpitch = pitch;
+  g.clog2c = log2c;
+  g.coh = oh;
+  g.cow = ow;
+  g.ck = k;
+  g.cstride = stride;
+  g.cpad = pad;
+  g.ckdim = kdim;
+  if (max_ctas <= 0) max_ctas = 2 * sm_count();
+  switch (bn) {
+    case 32: return launch_bn<32, true>(tb, tb, g, max_ctas, st);
+    case 64: return launch_bn<64, true>(tb, tb, g, max_ctas, st);
+    case 128: return launch_bn<128, true>(tb, tb, g, max_ctas, st);
+    default: return launch_bn<256, true>(tb, tb, g, max_ctas, st);
+  }
+}
+
+const void *conv_kernel_fn(int bn) {
+  switch (bn) {
+    case 32: return (const void *)gemm_bf16_tc<32, true>;
+    case 64: return (const void *)gemm_bf16_tc<64, true>;
+    case 128: return (const void *)gemm_bf16_tc<128, true>;
+    default: return (const void *)gemm_bf16_tc<256, true>;
+  }
+}
+int conv_block_threads() { return kConvThreads; }
 
 int gemm_block_threads() { return kGemmThreads; }
 

@@ -55,6 +55,11 @@ int gemm_generate(const gs_job_desc &j, const std::vector<void *> &dst, cudaStre
 int gemm_run(const gs_job_desc &j, std::vector<void *> &buf, cudaStream_t st, int *out_idx, int64_t *launches,
              unsigned *tk);
 int gemm_pick_bn(int m, int n);
+int conv_gemm_bf16(const void *in, int nb, int h, int w, int pitch, int log2c, int oh, int ow, int k, int stride,
+                   int pad, const void *B, int64_t ldb, const float *bias, void *out, int64_t ldo, int cout,
+                   int out_f32, int act, int max_ctas, cudaStream_t st, const void *res, int64_t ldr, unsigned *tk);
+const void *conv_kernel_fn(int bn);
+int conv_block_threads();
 int make_tmap_f32(CUtensorMap *m, const void *ptr, int64_t rows, int64_t cols, int box_cols, int box_rows);
 size_t gemm_smem_for(int bn);
 int gemm_block_threads();
