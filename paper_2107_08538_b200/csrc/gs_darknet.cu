@@ -125,8 +125,12 @@ struct NetBuilder {
       const char *e = getenv("GS_IM2ROW");
       return e && e[0] == '1';
     }();
+    static const int cmax = [] {  // widest layer run implicitly (GS_IMPLICIT_CMAX, for measurement)
+      const char *e = getenv("GS_IMPLICIT_CMAX");
+      return e ? atoi(e) : 128;
+    }();
     const int c = L.in.c;
-    return !off && !direct_gemm(L) && (L.k == 1 || L.k == 3) && c >= 8 && c <= 128 && (c & (c - 1)) == 0 &&
+    return !off && !direct_gemm(L) && (L.k == 1 || L.k == 3) && c >= 8 && c <= cmax && (c & (c - 1)) == 0 &&
            L.in.pitch % 8 == 0 && L.in.off % 8 == 0 && L.kpad == L.kdim;
   }
   TView pool(const TView &in, int k, int stride, int pad, int ho, int wo) {

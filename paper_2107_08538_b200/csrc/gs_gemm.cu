@@ -60,7 +60,10 @@ constexpr size_t gemm_smem_bytes() {
 }
 
 constexpr int kGemmThreads = 192;  // warp 0 TMA, warp 1 MMA, warps 2-5 epilogue
-constexpr int kConvThreads = 256;  // + warps 6-7 gathering A (implicit convolution)
+constexpr int kGatherWarps = 2;    // implicit convolution: warps 6.. gather A (4 measured no faster)
+constexpr int kGatherThreads = 32 * kGatherWarps;
+constexpr int kGatherRows = kGemmBM / kGatherThreads;  // tile rows per gather thread
+constexpr int kConvThreads = kGemmThreads + kGatherThreads;
 
 __device__ __forceinline__ float leaky(float v) { return v > 0.0f ? v : 0.1f * v; }
 // YOLO layer (Darknet yolo_layer forward): logistic on x, y, objectness and
@@ -179,12 +182,12 @@ __device__ __forceinline__ int gemm_next_tile(const GemmArgs &g, int i, int tile
 // TMEM accumulators, and the four epilogue warps drain accumulator t while
 // the MMAs of tile t+1 run.
 //
-// CONV = true: the implicit convolution.  A's stage is gathered by two extra
-// warps (6, 7) straight from the NHWC activation with 16-byte cp.async into
+// CONV = true: the implicit convolution.  A's stage is gathered by
+// kGatherWarps extra warps (6, ...) straight from the NHWC activation with 16-byte cp.async into
 // the 128-byte-swizzled K-major layout the TMA would have written (chunk j of
 // tile row r at r * 128 + ((j ^ (r & 7)) << 4)), zero-filled at the padding
 // and past M / K; each gather thread's cp.async completion arrives on the
-// stage's barrier (expected count 1 + 64), and the MMA thread issues a proxy
+// stage's barrier (expected count 1 + kGatherThreads), and the MMA thread issues a proxy
 // fence before its tensor-core reads.  K order (ky, kx, c) is im2row's, so
 // the products equal im2row + GEMM's exactly — without writing and
 // re-reading the im2row matrix (30-39 % of a Darknet job).
@@ -212,7 +215,7 @@ __global__ void __launch_bounds__(CONV ? kConvThreads : kGemmThreads, 2)
     if (!CONV) tma_prefetch(&ta);
     tma_prefetch(&tb);
     for (int s = 0; s < kGemmStages; ++s) {
-      mbar_init(&full[s], CONV ? 1 + 64 : 1);
+      mbar_init(&full[s], CONV ? 1 + kGatherThreads : 1);
       mbar_init(&empty[s], 1);
     }
     for (int a = 0; a < 2; ++a) {
@@ -221,7 +224,7 @@ __global__ void __launch_bounds__(CONV ? kConvThreads : kGemmThreads, 2)
     }
     for (int s = 0; s < 4; ++s) {
       mbar_init(&tq_full[s], 1);
-      mbar_init(&tq_empty[s], CONV ? 7 : 5);
+      mbar_init(&tq_empty[s], CONV ? 5 + kGatherWarps : 5);
     }
     fence_mbar_init();
   }
@@ -285,7 +288,7 @@ __global__ void __launch_bounds__(CONV ? kConvThreads : kGemmThreads, 2)
       }
     }
   } else if (CONV && warp >= 6) {
-    // A gather (implicit im2row): 64 threads, tile rows gt and gt + 64
+    // A gather (implicit im2row): kGatherThreads threads, tile rows gt + kGatherThreads * h
     const int gt = (int)threadIdx.x - 192;
     const int cmask = (1 << g.clog2c) - 1;
     uint32_t stage = 0, phase = 0;
@@ -296,12 +299,12 @@ __global__ void __launch_bounds__(CONV ? kConvThreads : kGemmThreads, 2)
       if (lane == 0) mbar_arrive(&tq_empty[i & 3]);
       if (tile >= tiles) break;
       const int mt = tile / g.n_tiles;
-      int iy0[2], ix0[2];
-      bool valid[2];
-      const __nv_bfloat16 *img[2];
+      int iy0[kGatherRows], ix0[kGatherRows];
+      bool valid[kGatherRows];
+      const __nv_bfloat16 *img[kGatherRows];
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int m = mt * kGemmBM + gt + 64 * h;
+      for (int h = 0; h < kGatherRows; ++h) {
+        const int m = mt * kGemmBM + gt + kGatherThreads * h;
         valid[h] = m < g.m;
         const int mm = valid[h] ? m : 0;
         const int t2 = mm / g.cow, ox = mm - t2 * g.cow;
@@ -314,8 +317,8 @@ __global__ void __launch_bounds__(CONV ? kConvThreads : kGemmThreads, 2)
         mbar_wait(&empty[stage], phase ^ 1);
         const uint32_t dst = smem_u32(sa + stage * A_BYTES);
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const int r = gt + 64 * h;
+        for (int h = 0; h < kGatherRows; ++h) {
+          const int r = gt + kGatherThreads * h;
 #pragma unroll
           for (int j = 0; j < 8; ++j) {
             const int k = kb * kGemmBK + j * 8;
