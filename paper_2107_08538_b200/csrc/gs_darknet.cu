@@ -490,6 +490,105 @@ __global__ void __launch_bounds__(kThr, 2) conv3x3_direct(ViewArgs in, const __n
   }
 }
 
+// YOLO layer 0 fused with the 2x2/2 max-pool that follows it: a thread owns
+// one pooled pixel, i.e. a 2 x 2 block of conv outputs.  The block's 4 x 4 x 3
+// input window is loaded once (48 values), every filter row of the shared
+// fp32 weights (2 x float4 per 8-channel pass) feeds the 4 pixels at once
+// (32 FMAs per 2 shared loads, not 8), and the pooled maximum is taken from the
+// bf16 conv outputs in registers — the max-pool's re-read of the 378 MB conv
+// output (608^2 x 32) is gone.  Per output pixel the FMA chain is
+// conv3x3_direct's exactly (taps in order, channels inner, padding taps
+// skipped), so both outputs are bit-identical to conv3x3_direct + maxpool.
+template <int CIN, int COUT>
+__global__ void __launch_bounds__(128, 2) conv3x3_pool2(ViewArgs in, const __nv_bfloat16 *__restrict__ w, int kpad,
+                                                     const float *__restrict__ bias, __nv_bfloat16 *out, int opitch,
+                                                     __nv_bfloat16 *pout, int ppitch) {
+  __shared__ __align__(16) float sW[9 * CIN][COUT];
+  __shared__ float sb[COUT];
+  for (int i = threadIdx.x; i < 9 * CIN * COUT; i += blockDim.x) {
+    const int k = i / COUT, co = i % COUT;
+    sW[k][co] = __bfloat162float(w[(int64_t)co * kpad + k]);
+  }
+  if (threadIdx.x < COUT) sb[threadIdx.x] = bias[threadIdx.x];
+  __syncthreads();
+  const int ph = in.h / 2, pw = in.w / 2;
+  const unsigned pix = (unsigned)((int64_t)in.n * ph * pw);
+  for (unsigned p = blockIdx.x * blockDim.x + threadIdx.x; p < pix; p += gridDim.x * blockDim.x) {
+    const unsigned q = p / (unsigned)pw;
+    const int px = (int)(p - q * (unsigned)pw);
+    const unsigned bq = q / (unsigned)ph;
+    const int py = (int)(q - bq * (unsigned)ph);
+    const int64_t b = bq;
+    const int y0 = 2 * py - 1, x0 = 2 * px - 1;  // window origin (4 x 4)
+    bool rin[4], cin[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      rin[i] = y0 + i >= 0 && y0 + i < in.h;
+      cin[i] = x0 + i >= 0 && x0 + i < in.w;
+    }
+    float win[4][4][CIN];
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const bool ok = rin[r] && cin[c];
+        const __nv_bfloat16 *src = in.p + (((b * in.h + (ok ? y0 + r : 0)) * in.w) + (ok ? x0 + c : 0)) * in.pitch;
+#pragma unroll
+        for (int ch = 0; ch < CIN; ++ch) win[r][c][ch] = ok ? __bfloat162float(src[ch]) : 0.0f;
+      }
+    auto bits = [](__nv_bfloat162 v) {
+      return (uint32_t)__bfloat16_as_ushort(v.x) | ((uint32_t)__bfloat16_as_ushort(v.y) << 16);
+    };
+    // 8 output channels per pass (64 accumulators for all 16 spilled)
+#pragma unroll 1
+    for (int h8 = 0; h8 < COUT / 8; ++h8) {
+      float acc[4][8];
+#pragma unroll
+      for (int o = 0; o < 4; ++o)
+#pragma unroll
+        for (int co = 0; co < 8; ++co) acc[o][co] = 0.0f;
+#pragma unroll
+      for (int tap = 0; tap < 9; ++tap) {
+        const int ky = tap / 3, kx = tap % 3;
+#pragma unroll
+        for (int ch = 0; ch < CIN; ++ch) {
+          const float4 *wr = reinterpret_cast<const float4 *>(&sW[tap * CIN + ch][8 * h8]);
+          const float4 t0 = wr[0], t1 = wr[1];
+          const float ww[8] = {t0.x, t0.y, t0.z, t0.w, t1.x, t1.y, t1.z, t1.w};
+#pragma unroll
+          for (int o = 0; o < 4; ++o) {
+            const int r = (o >> 1) + ky, c = (o & 1) + kx;
+            if (!(rin[r] && cin[c])) continue;  // conv3x3_direct skips padding taps
+            const float v = win[r][c][ch];
+#pragma unroll
+            for (int co = 0; co < 8; ++co) acc[o][co] = fmaf(v, ww[co], acc[o][co]);
+          }
+        }
+      }
+      __nv_bfloat162 mx[4];
+#pragma unroll
+      for (int o = 0; o < 4; ++o) {
+        const int oy = 2 * py + (o >> 1), ox = 2 * px + (o & 1);
+        uint32_t ow[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const int c0 = 8 * h8 + 2 * e;
+          float a0 = acc[o][2 * e] + sb[c0], a1 = acc[o][2 * e + 1] + sb[c0 + 1];
+          a0 = a0 > 0.0f ? a0 : 0.1f * a0;
+          a1 = a1 > 0.0f ? a1 : 0.1f * a1;
+          const __nv_bfloat162 v = __floats2bfloat162_rn(a0, a1);
+          mx[e] = o == 0 ? v : __hmax2(mx[e], v);
+          ow[e] = bits(v);
+        }
+        reinterpret_cast<uint4 *>(out + ((b * in.h + oy) * (int64_t)in.w + ox) * opitch)[h8] =
+            make_uint4(ow[0], ow[1], ow[2], ow[3]);
+      }
+      reinterpret_cast<uint4 *>(pout + ((b * ph + py) * (int64_t)pw + px) * ppitch)[h8] =
+          make_uint4(bits(mx[0]), bits(mx[1]), bits(mx[2]), bits(mx[3]));
+    }
+  }
+}
+
 ViewArgs vargs(const TView &v, const std::vector<void *> &buf) {
   return {reinterpret_cast<const __nv_bfloat16 *>(buf[v.buf]) + v.off, v.n, v.h, v.w, v.c, v.pitch};
 }
@@ -531,7 +630,11 @@ std::vector<Shape> gemm_launches(const gs_job_desc &j) {
   gc.dsmem = (int)gemm_smem_for(bn_max);
   std::vector<Shape> v = {g, gc, {(const void *)im2row, grid_for(pix0 * 4), kThr},
                           {(const void *)maxpool, grid_for(pix0), kThr}};
-  if (j.kind == GS_JOB_YOLO) v.push_back({(const void *)conv3x3_direct<3, 16>, grid_for(pix0), kThr});
+  if (j.kind == GS_JOB_YOLO) {
+    v.push_back({(const void *)conv3x3_direct<3, 16>, grid_for(pix0), kThr});
+    v.push_back({(const void *)conv3x3_pool2<3, 16>,
+                 (int)std::min<int64_t>((pix0 / 4 + 127) / 128, 2 * sm_count()), 128});
+  }
   else v.push_back({(const void *)avgpool, grid_for(pix0), kThr});
   return v;
 }
@@ -554,11 +657,27 @@ int gemm_generate(const gs_job_desc &j, const std::vector<void *> &dst, cudaStre
   return GS_OK;
 }
 
+// the YOLO layer-0 convolution followed by a 2x2/2 max-pool of its output
+static bool fuse_pool(const LPlan &L, const LPlan &M) {
+  static const bool off = [] {
+    const char *e = getenv("GS_NO_POOL_FUSION");
+    return e && e[0] == '1';
+  }();
+  return !off && M.type == MAXPOOL && M.k == 2 && M.stride == 2 && M.pad == 0 && M.in.buf == L.out.buf &&
+         M.in.off == L.out.off && L.in.h % 2 == 0 && L.in.w % 2 == 0 && !M.out.f32 && M.out.off % 8 == 0 &&
+         M.out.pitch % 8 == 0;
+}
+static int pool2_grid(const LPlan &L) {
+  const int64_t units = (int64_t)L.in.n * (L.in.h / 2) * (L.in.w / 2);
+  return (int)std::min<int64_t>((units + 127) / 128, 2 * sm_count());
+}
+
 int gemm_run(const gs_job_desc &j, std::vector<void *> &buf, cudaStream_t st, int *out_idx, int64_t *launches,
              unsigned *tk) {
   const NetPlan P = net_plan(j);
   for (int pass = 0; pass < j.iters; ++pass) {
-    for (const LPlan &L : P.layers) {
+    for (size_t li = 0; li < P.layers.size(); ++li) {
+      const LPlan &L = P.layers[li];
       const ViewArgs in = vargs(L.in, buf);
       __nv_bfloat16 *obf = L.out.f32 ? nullptr : (__nv_bfloat16 *)buf[L.out.buf] + L.out.off;
       if (L.type == MAXPOOL) {
@@ -583,6 +702,15 @@ int gemm_run(const gs_job_desc &j, std::vector<void *> &buf, cudaStream_t st, in
           L.in.c == 3 && L.cout == 16) {
         // YOLO layer 0 (K = 27): direct convolution (measured 0.6 ms vs 4.2 ms
         // for im2row + GEMM at 608^2 x 32; for 16 -> 32 the GEMM path is faster)
+        if (li + 1 < P.layers.size() && fuse_pool(L, P.layers[li + 1])) {
+          const LPlan &M = P.layers[li + 1];
+          conv3x3_pool2<3, 16><<<pool2_grid(L), 128, 0, st>>>(
+              in, (const __nv_bfloat16 *)buf[B_W] + L.woff, L.kpad, (const float *)buf[B_BIAS] + L.boff, obf,
+              L.out.pitch, (__nv_bfloat16 *)buf[M.out.buf] + M.out.off, M.out.pitch);
+          ++*launches;
+          ++li;  // the max-pool's output is written too
+          continue;
+        }
         conv3x3_direct<3, 16><<<grid_for(opix), kThr, 0, st>>>(in, (const __nv_bfloat16 *)buf[B_W] + L.woff, L.kpad,
                                                                (const float *)buf[B_BIAS] + L.boff, obf, L.out.pitch);
         ++*launches;
