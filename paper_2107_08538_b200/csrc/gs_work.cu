@@ -159,6 +159,14 @@ int needle_grid(const gs_job_desc &j) {
   return std::min(bands, 4 * sm_count());
 }
 
+bool hotspot_four_steps() {
+  static const bool four = [] {
+    const char *e = getenv("GS_HOTSPOT_STEPS");
+    return e && e[0] == '4';
+  }();
+  return four;
+}
+
 // The job's kernels, in the order its host code first launches them.
 static std::vector<Shape> job_kernels(const gs_job_desc &j) {
   const int g = job_grid(j);
@@ -169,7 +177,10 @@ static std::vector<Shape> job_kernels(const gs_job_desc &j) {
     {
       Shape s2{(const void *)hotspot_step2, g, kThreads};
       s2.dsmem = kHs2Smem;
-      return {s2, {(const void *)hotspot_step, g, kThreads}};
+      if (j.iters < 4 || !hotspot_four_steps()) return {s2, {(const void *)hotspot_step, g, kThreads}};
+      Shape s4{(const void *)hotspot_step4, g, kThreads};
+      s4.dsmem = kHs4Smem;
+      return {s4, s2, {(const void *)hotspot_step, g, kThreads}};
     }
     case GS_JOB_SRAD:
       return {{(const void *)srad_stats, 1, kThreads}, {(const void *)srad_fused, g, kThreads}};
@@ -423,6 +434,27 @@ int run_kernels(const gs_job_desc &j, std::vector<void *> &buf, cudaStream_t st,
       if (rc) return rc;
       const CUtensorMap *min = &mt, *min2 = &mt2;
       int it = 0;
+      // GS_HOTSPOT_STEPS=4: four steps per pass while four remain (~3 B per
+      // cell-step).  Opt-in: measured 28.7 vs 23.7 ms at 24576^2 x 40 — the
+      // four barrier-separated steps at 16 warps per SM issue at 53 % and
+      // ~20 instructions per cell update (ncu, profiles/r02_hotspot_step4.txt),
+      // so it is issue bound above the two-step pass's HBM time
+      if (hotspot_four_steps() && it + 3 < j.iters) {
+        CUW(cudaFuncSetAttribute(hotspot_step4, cudaFuncAttributeMaxDynamicSharedMemorySize, kHs4Smem));
+        CUtensorMap m4, m42, mp4;
+        rc = make_tmap_f32(&m4, t, n, n, kHs4W, kHs4H);
+        if (!rc) rc = make_tmap_f32(&m42, t2, n, n, kHs4W, kHs4H);
+        if (!rc) rc = make_tmap_f32(&mp4, p, n, n, kHs4W, kHs4H);
+        if (rc) return rc;
+        const CUtensorMap *q = &m4, *q2 = &m42;
+        for (; it + 3 < j.iters; it += 4) {
+          hotspot_step4<<<g, 256, kHs4Smem, st>>>(*q, mp4, t2, (int)n, cc, rx1, ry1, rz1, tk);
+          ++launches;
+          std::swap(t, t2);
+          std::swap(q, q2);
+          std::swap(min, min2);  // the two-step maps follow the buffers
+        }
+      }
       for (; it + 1 < j.iters; it += 2) {
         hotspot_step2<<<g, 256, kHs2Smem, st>>>(*min, mp, t2, (int)n, cc, rx1, ry1, rz1, tk);
         ++launches;
