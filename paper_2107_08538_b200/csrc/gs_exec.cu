@@ -885,13 +885,16 @@ int gs_exec_run_arrivals(const gs_job_desc *jobs, int32_t n_jobs, const double *
   phase("sched created");
   rc = gs_engine_reserve_handles(eng, n_jobs + 1);
   if (rc) return err(rc, gs_last_error());
-  // Placement calls: one decision launch per call by default.  GS_RING=1
-  // serves them from the resident decision warp over the host-mapped command
-  // ring instead (lower decision latency, but measured 2-3x slower job
-  // mixes: the resident kernel delays co-located jobs' kernels — see
-  // DESIGN.md §4); never under ncu, which serializes kernels.
+  // Placement calls: the single decision authority serializes every
+  // worker's calls under its lock.  On one GPU they go as one decision
+  // launch each (~40 us; the resident ring measured the same makespan).  A
+  // fleet has N x workers callers behind that lock, so runs over several GPUs
+  // serve them from the resident decision warp over the host-mapped command
+  // ring (~7 us per decision, tools/ring_bench.cpp).  GS_RING=0 / 1 forces
+  // either; never under ncu, which serializes kernels.
   const char *ring_env = getenv("GS_RING");
-  if (ring_env && ring_env[0] == '1') {
+  const bool use_ring = ring_env ? ring_env[0] == '1' : n_devices > 1;
+  if (use_ring) {
     rc = gs_sched_ring_start(sched, n_jobs + 1, n_jobs + 1, n_jobs + 1);
     if (rc) return err(rc, gs_last_error());
   }
