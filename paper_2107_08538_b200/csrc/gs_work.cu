@@ -86,10 +86,10 @@ std::vector<Buf> job_buffers(const gs_job_desc &j) {
            {(n + 1) * 4, IN}, {n * GS_BFS_DEGREE * 4, IN}};
       break;
     case GS_JOB_HOTSPOT:
-      b = {{n * n * 4, INOUT}, {n * n * 4, IN}, {n * n * 4, SCR}};
+      b = {{n * n * 4, INOUT}, {n * n * 4, IN}, {n * n * 4, PING}};  // T, P, T ping-pong (every pass writes all of it)
       break;
     case GS_JOB_SRAD:
-      b = {{n * n * 4, INOUT}, {n * n * 4, SCR}, {16, SCR}};  // J, J ping-pong, q0
+      b = {{n * n * 4, INOUT}, {n * n * 4, PING}, {16, SCR}};  // J, J ping-pong (written in full), q0
       break;
     case GS_JOB_KMEANS:
       b = {{n * j.m * 4, IN}, {n * 4, OUT}, {(int64_t)GS_KMEANS_K * j.m * 4, OUT},

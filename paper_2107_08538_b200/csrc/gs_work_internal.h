@@ -20,8 +20,9 @@ int sm_count();
 void set_job_sms(int n);
 
 // IN staged input, INOUT staged input that is also an output, OUT output,
-// SCR zeroed scratch, WRK uninitialized workspace (fully overwritten)
-enum Role { IN = 0, INOUT = 1, OUT = 2, SCR = 3, WRK = 4 };
+// SCR zeroed scratch, WRK uninitialized workspace (fully overwritten), PING
+// uninitialized ping-pong buffer that may end up holding the output
+enum Role { IN = 0, INOUT = 1, OUT = 2, SCR = 3, WRK = 4, PING = 5 };
 
 struct Buf {
   int64_t bytes;
