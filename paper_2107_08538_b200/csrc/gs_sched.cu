@@ -51,7 +51,6 @@
 namespace {
 
 constexpr int kThreads = 32;  // the decision chain runs on one warp
-constexpr int kMaxHelpers = 8;  // + up to 8 helper warps that score mgb-sm devices in parallel
 constexpr unsigned kFull = 0xffffffffu;
 constexpr int kRowHdrWords = sizeof(gs_residency) / 4;  // 12
 constexpr int kLedHdrWords = sizeof(gs_ledger) / 4;     // 16
@@ -147,9 +146,6 @@ struct KParams {
   long long ring_idle_ns;
   int ring_sleep_ns;  // poll interval of the idle decision warp
   int wb_mode;        // diagnostics (GS_RING_WB): 2 = system fence inside the per-command write-back
-  int n_help;         // helper warps scoring mgb-sm candidate devices in parallel (0 = none)
-  int help_off;       // int offset of the per-device cap buffers (n_dev x max_sm_pad) in dyn smem
-  int pad3;
 };
 
 struct SLed {
@@ -719,79 +715,6 @@ __device__ void fifo_pop_release(const KParams &p, Smem &S, int *dyn, int lane) 
   __syncwarp();
 }
 
-// ---- helper warps (mgb-sm) ------------------------------------------------
-// The decision chain stays on warp 0.  Its costliest step under mgb-sm is
-// the exact per-SM capacity count of every candidate device, in index order,
-// until one fits (_try_mgb_sm, schedulers.py:137-153): 148 SMs over 32 lanes
-// per device.  With helper warps, warp 0 posts the shape and the candidate
-// mask, helper h counts devices h, h + H, ... (each into its own cap buffer,
-// which the plan then reuses) and warp 0 takes the first device in index
-// order whose count admits the request — the same device the sequential
-// scan finds.  Named barriers: 1 = job posted, 2 = job done.
-struct HelpJob {
-  int op;  // 1 score, 2 quit
-  unsigned mask;
-  Shape sh;
-};
-__shared__ HelpJob s_help;
-__shared__ long long s_tot[GS_MAX_DEVICES];
-__shared__ int s_mx[GS_MAX_DEVICES];
-
-__device__ __forceinline__ void named_bar(int id) {
-  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"((int)blockDim.x) : "memory");
-}
-__device__ __forceinline__ int *help_cap(const KParams &p, int *dyn, int d) {
-  return dyn + p.help_off + d * p.max_sm_pad;
-}
-
-__device__ __forceinline__ void helper_loop(const KParams &p, int *dyn, int h, int lane) {
-  for (;;) {
-    named_bar(1);
-    const int op = s_help.op;
-    if (op == 2) return;
-    const unsigned mask = s_help.mask;
-    const Shape sh = s_help.sh;
-    for (int d = h; d < p.n_dev; d += p.n_help) {
-      if (!((mask >> d) & 1)) continue;
-      int mx = 0;
-      const long long tot = warp_total_cap(p.dev[d], dyn, sh, help_cap(p, dyn, d), &mx, lane);
-      if (lane == 0) {
-        s_tot[d] = tot;
-        s_mx[d] = mx;
-      }
-    }
-    named_bar(2);
-  }
-}
-
-// warp 0: score every device in `mask` on the helpers; returns the first
-// (index order) whose count admits sh.T, or -1
-__device__ int help_score(const KParams &p, const Shape &sh, unsigned mask, int *mx_out, int lane) {
-  if (lane == 0) {
-    s_help.op = 1;
-    s_help.mask = mask;
-    s_help.sh = sh;
-  }
-  named_bar(1);
-  named_bar(2);
-  int chosen = -1;
-  for (unsigned m = mask; m; m &= m - 1) {
-    const int d = __ffs(m) - 1;
-    if (s_tot[d] >= sh.T) {
-      chosen = d;
-      *mx_out = s_mx[d];
-      break;
-    }
-  }
-  return chosen;
-}
-
-__device__ void help_quit(const KParams &p, int lane) {
-  if (p.n_help <= 0) return;
-  if (lane == 0) s_help.op = 2;
-  named_bar(1);
-}
-
 // One admission attempt (Scheduler._try, schedulers.py:127-135) over the
 // devices in `mask`.  Uniform result across the warp.
 __device__ Dec decide(const KParams &p, Smem &S, int *dyn, const gs_probe &pr, unsigned mask, bool allow_reject,
@@ -812,7 +735,6 @@ __device__ Dec decide(const KParams &p, Smem &S, int *dyn, const gs_probe &pr, u
       r_warps = row->warps;
     }
     int chosen = -1, caps_mx = -1;
-    int *cap_sel = dyn + p.scratch_off;  // the chosen device's per-SM caps
     if (p.policy == GS_POLICY_MGB_WARPS) {
       // _try_mgb_warps (schedulers.py:155-171): feasible = free_mem >= mem,
       // choose min((in_use_warps, idx))
@@ -830,17 +752,11 @@ __device__ Dec decide(const KParams &p, Smem &S, int *dyn, const gs_probe &pr, u
       const bool cand = lane < n_dev && ((mask >> lane) & 1) && S.led[lane].free_mem >= sh.mem &&
                         agg_admits(S, lane, sh);
       int *cap = dyn + p.scratch_off;
-      const unsigned cm = __ballot_sync(kFull, cand);
-      if (p.n_help > 0 && __popc(cm) >= 2) {
-        chosen = help_score(p, sh, cm, &caps_mx, lane);
-        if (chosen >= 0) cap_sel = help_cap(p, dyn, chosen);
-      } else {
-        for (unsigned m = cm; m; m &= m - 1) {
-          const int d = __ffs(m) - 1;
-          if (warp_total_cap(p.dev[d], dyn, sh, cap, &caps_mx, lane) >= sh.T) {
-            chosen = d;
-            break;
-          }
+      for (unsigned m = __ballot_sync(kFull, cand); m; m &= m - 1) {
+        const int d = __ffs(m) - 1;
+        if (warp_total_cap(p.dev[d], dyn, sh, cap, &caps_mx, lane) >= sh.T) {
+          chosen = d;
+          break;
         }
       }
     }
@@ -865,7 +781,8 @@ __device__ Dec decide(const KParams &p, Smem &S, int *dyn, const gs_probe &pr, u
     int *P = dyn + p.scratch_off + p.max_sm_pad;
     const bool sm_policy = p.policy == GS_POLICY_MGB_SM;
     if (sm_policy) {
-      const int cur = warp_plan(D, dyn, L, sh, cap_sel, P, lane, caps_mx);
+      int *cap = dyn + p.scratch_off;
+      const int cur = warp_plan(D, dyn, L, sh, cap, P, lane, caps_mx);
       warp_commit_blocks(D, dyn, L, h, sh, P, cur, lane);  // commit_placement
     }
     const long long new_mem = (present ? pm : 0) + sh.mem, new_warps = (present ? pw : 0) + sh.tw;
@@ -1458,21 +1375,10 @@ __device__ int sweep_warps_fast(const KParams &p, Smem &S, int *dyn, int lane) {
   return stop_at;
 }
 
-__device__ __forceinline__ void interp_main(const KParams &p, int *dyn, Smem &S, int lane);
-
-__global__ void __launch_bounds__(kThreads * (1 + kMaxHelpers), 1) gs_interp_kernel(KParams p) {
+__global__ void __launch_bounds__(kThreads, 1) gs_interp_kernel(KParams p) {
   extern __shared__ __align__(16) int dyn[];
   __shared__ Smem S;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  if (warp > 0) {
-    helper_loop(p, dyn, warp - 1, lane);
-    return;
-  }
-  interp_main(p, dyn, S, lane);
-  help_quit(p, lane);
-}
-
-__device__ __forceinline__ void interp_main(const KParams &p, int *dyn, Smem &S, int lane) {
+  const int lane = threadIdx.x;
 
   stage(p, dyn, S, true, lane);
   __syncwarp();
@@ -1551,7 +1457,8 @@ __device__ __forceinline__ void interp_main(const KParams &p, int *dyn, Smem &S,
       processed++;
       if (lane == 0) st_release_sys(&ring->done, processed);
       ts[4] = globaltimer();
-      if (lane < 5) ring->stamp[lane] = ts[lane];
+      if (lane == 0)  // lane 0's clock readings (the other lanes skip the poll loop)
+        for (int k = 0; k < 5; ++k) ring->stamp[k] = ts[k];
       __syncwarp();
     }
     writeback(p, dyn, S, lane);
@@ -1864,10 +1771,8 @@ int build_params(gs_engine *eng, gs_device *const *devs, int n, Launch &L) {
   return GS_OK;
 }
 
-inline int interp_threads(const KParams &p) { return kThreads * (1 + p.n_help); }
-
 int launch(gs_engine *eng, Launch &L) {
-  gs_interp_kernel<<<1, interp_threads(L.p), L.smem, eng->stream>>>(L.p);
+  gs_interp_kernel<<<1, kThreads, L.smem, eng->stream>>>(L.p);
   CU(cudaGetLastError());
   CU(cudaStreamSynchronize(eng->stream));
   eng->launches++;
@@ -1882,7 +1787,7 @@ int ring_launch(gs_sched *s) {
   __atomic_thread_fence(__ATOMIC_SEQ_CST);
   KParams p = s->ring_params;
   p.ring = s->ring.d;
-  gs_interp_kernel<<<1, interp_threads(p), s->ring_smem, s->ring_stream>>>(p);
+  gs_interp_kernel<<<1, kThreads, s->ring_smem, s->ring_stream>>>(p);
   CU(cudaGetLastError());
   s->eng->launches++;
   return GS_OK;
@@ -1982,22 +1887,6 @@ int sched_params(gs_sched *s, Launch &L) {
   p.job_cap = (int32_t)s->claims.n;
   p.drain_out = s->drain.d;
   p.drain_cap = (int32_t)s->drain.n;
-  // mgb-sm: helper warps score candidate devices in parallel, each device's
-  // per-SM caps in its own buffer.  Opt-in (GS_SM_HELPERS=n): measured on
-  // the cfg 4 sweep it did not pay — 7.77 vs 7.85 us per probe, the helpers
-  // idle at their barrier ~78 % of the samples (profiles/r02_sweep_sm_helpers.txt)
-  static const int helpers_env = [] {
-    const char *e = getenv("GS_SM_HELPERS");
-    return e ? atoi(e) : 0;
-  }();
-  const int want = s->policy == GS_POLICY_MGB_SM && p.n_dev >= 2 ? std::min(p.n_dev, kMaxHelpers) : 0;
-  p.n_help = std::min(want, std::max(helpers_env, 0));
-  if (p.n_help > 0) {
-    p.help_off = p.fifo_off;
-    p.fifo_off += p.n_dev * p.max_sm_pad;
-    L.smem += (size_t)p.n_dev * p.max_sm_pad * sizeof(int);
-    if ((int)L.smem > s->eng->max_smem) return set_err(GS_ERR_CONFIG, "fleet ledgers exceed shared memory");
-  }
   return GS_OK;
 }
 
@@ -2599,7 +2488,7 @@ int gs_sweep(gs_sched *s, const gs_probe *probes, int32_t n, int32_t max_residen
   CU(cudaEventCreate(&e0));
   CU(cudaEventCreate(&e1));
   CU(cudaEventRecord(e0, eng->stream));
-  gs_interp_kernel<<<1, interp_threads(L.p), L.smem, eng->stream>>>(L.p);
+  gs_interp_kernel<<<1, kThreads, L.smem, eng->stream>>>(L.p);
   CU(cudaGetLastError());
   CU(cudaEventRecord(e1, eng->stream));
   CU(cudaStreamSynchronize(eng->stream));
