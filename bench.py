@@ -400,6 +400,17 @@ def cfg3_block(W, C, devices, workers, jobs_n, load, seed):
     return out
 
 
+def bench_config(args, n_gpus: int) -> dict:
+    """The workload both arms report (the reference arm runs a bounded sample
+    of it, described in its cpu_baseline)."""
+    return {"workload": f"cfg1: {args.jobs}-job Rodinia mix {args.mix} per GPU "
+                        f"(bfs/hotspot/srad/kmeans/backprop/needle/lud), {args.jobs * n_gpus} jobs on "
+                        f"{n_gpus} GPU(s)",
+            "policy": args.policy, "workers_per_gpu": args.workers,
+            "inputs": "staged in HBM, larger than L2 (no flush needed)",
+            "parallelism": f"placement over {n_gpus} GPU(s), one decision authority"}
+
+
 def reference_arm(args, mix):
     """--impl reference: the reference's path on host cores (C port)."""
     from oracle import oracle as O
@@ -432,13 +443,12 @@ def reference_arm(args, mix):
     line = {
         "metric": METRIC, "value": round(v, 4), "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(1000.0 / v, 1) if v else None, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f32/i32", "data": "synthetic",
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32/i32", "data": "synthetic (seeded hash inputs)",
         "impl": "reference",
-        "config": {"workload": f"cfg1: {args.jobs}-job Rodinia mix {args.mix} per GPU x {args.gpus} "
-                               "(bounded CPU sample)",
-                   "policy": "mgb-warps (C port of schedulers.py)", "cpu_threads": threads},
+        "config": bench_config(args, args.gpus),
         "cpu_baseline": {"value": round(v, 4), "unit": UNIT, "cores": threads, "kind": "port",
-                         "sample": sample_desc},
+                         "sample": sample_desc + " per step; scheduler: the C port of schedulers.py "
+                                                "(oracle/gs_oracle.c), kernels: oracle/kernels_cpu.c"},
         "e2e": {"value": round(v, 4), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -535,14 +545,9 @@ def drive(args, devices, torch, barrier):
         "metric": METRIC, "value": round(value, 4), "unit": UNIT, "n_gpus": len(devices), "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(ours["ms_per_step"], 2), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f32/i32", "data": "synthetic (seeded hash inputs)",
-        "config": {"workload": f"cfg1: {args.jobs}-job Rodinia mix {args.mix} per GPU "
-                               f"(bfs/hotspot/srad/kmeans/backprop/needle/lud), {len(jobs)} jobs on "
-                               f"{len(devices)} GPU(s)",
-                   "policy": args.policy, "workers": workers,
-                   "decision_authority": f"one engine, {len(devices)} ledger(s) (rank 0 drives the fleet)",
-                   "ledger_bytes_per_gpu": cap,
-                   "inputs": "staged in HBM, larger than L2 (no flush needed)",
-                   "parallelism": f"placement over {len(devices)} GPU(s)"},
+        "config": bench_config(args, len(devices)),
+        "decision_authority": f"one engine, {len(devices)} ledger(s) (rank 0 drives the fleet)",
+        "ledger_bytes_per_gpu": cap,
         "jobs_submitted_per_step": ours["submitted_per_step"],
         "jobs_completed_per_step": ours["completed_per_step"],
         "mean_turnaround_ms": round(ours["mean_turnaround_ms"], 2),
