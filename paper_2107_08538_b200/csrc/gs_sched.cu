@@ -117,7 +117,7 @@ struct KDev {
   int32_t arr_pad;   // padded per-SM array length
   int32_t smem_off;  // int offset of this device's staged block in dyn smem
   int32_t fast;      // all spec per-SM limits < 2^22 (32-bit cap arithmetic)
-  int32_t pad;
+  int32_t t_small;   // INT_MAX / n_sm: shapes with T <= this sum per-SM counts in 32 bits
   gs_spec spec;
 };
 
@@ -275,7 +275,7 @@ __device__ __forceinline__ long long warp_sum_blocks(long long v, bool small) {
   return small ? (long long)__reduce_add_sync(kFull, (unsigned)v) : warp_sum64(v);
 }
 __device__ __forceinline__ bool blocks_small(const KDev &D, const Shape &sh) {
-  return sh.T >= 0 && sh.T <= INT_MAX / max(D.n_sm, 1);
+  return sh.T >= 0 && sh.T <= D.t_small;  // (a per-device constant: no division per reduction)
 }
 
 // Σ sm_cap over the device's SMs; also leaves every SM's cap in cap[] and
@@ -452,7 +452,8 @@ __device__ int warp_plan(const KDev &D, int *dyn, const SLed &L, const Shape &sh
   const unsigned lt = (1u << lane) - 1u;
   for (int base = 0; base < n; base += 32) {
     const int pos = base + lane;
-    const int s = pos < n ? (c0 + pos) % n : 0;
+    int s = c0 + pos;  // c0, pos < n: one conditional subtraction, not a modulo
+    s = pos < n ? (s >= n ? s - n : s) : 0;
     bool q = false;
     if (pos < n) q = rem > 0 ? (cap[s] > k) : (cap[s] >= k);
     const unsigned b = __ballot_sync(kFull, q);
@@ -465,7 +466,8 @@ __device__ int warp_plan(const KDev &D, int *dyn, const SLed &L, const Shape &sh
       run += __popc(b);
       if (run >= rem) break;
     } else if (b) {
-      last = (c0 + base + 31 - __clz(b)) % n;
+      last = c0 + base + 31 - __clz(b);
+      last = last >= n ? last - n : last;
     }
   }
   last = __reduce_max_sync(kFull, last);
@@ -1748,7 +1750,8 @@ int build_params(gs_engine *eng, gs_device *const *devs, int n, Launch &L) {
     {
       const gs_spec &sp = dv->spec;
       const int64_t lim = 1LL << 22;
-      k.fast = sp.max_tbs_per_sm >= 0 && sp.max_tbs_per_sm < lim && sp.max_warps_per_sm >= 0 &&
+      k.t_small = (int32_t)(INT_MAX / std::max<int64_t>(dv->spec.sm_count, 1));
+    k.fast = sp.max_tbs_per_sm >= 0 && sp.max_tbs_per_sm < lim && sp.max_warps_per_sm >= 0 &&
                sp.max_warps_per_sm < lim && sp.regs_per_sm >= 0 && sp.regs_per_sm < lim &&
                sp.smem_per_sm_bytes >= 0 && sp.smem_per_sm_bytes < lim;
     }
