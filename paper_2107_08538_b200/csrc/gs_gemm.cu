@@ -131,6 +131,26 @@ __device__ __forceinline__ void epilogue_store(const GemmArgs &g, int row, int c
     if (whole && ((reinterpret_cast<uintptr_t>(o) & 15) == 0)) {
 #pragma unroll
       for (int i = 0; i < 32; i += 4) *reinterpret_cast<float4 *>(o + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+    } else if (whole) {
+      // rows of an odd pitch (the YOLO heads: 255 fp32 columns): scalars up
+      // to the next 16-byte boundary, then float4s (32 scalar stores per row
+      // made the heads store-bound)
+      const int lead = (int)((16 - (reinterpret_cast<uintptr_t>(o) & 15)) & 15) >> 2;
+#pragma unroll
+      for (int i = 0; i < 3; ++i)
+        if (i < lead) o[i] = v[i];
+#pragma unroll
+      for (int q = 0; q < 7; ++q) {
+#pragma unroll
+        for (int a4 = 0; a4 < 4; ++a4)
+          if (lead == a4) {
+            const int i = a4 + 4 * q;
+            *reinterpret_cast<float4 *>(o + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+          }
+      }
+#pragma unroll
+      for (int i = 28; i < 32; ++i)
+        if (i >= lead + 28) o[i] = v[i];
     } else {
 #pragma unroll
       for (int i = 0; i < 32; ++i)
