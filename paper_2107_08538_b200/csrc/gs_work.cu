@@ -99,8 +99,9 @@ std::vector<Buf> job_buffers(const gs_job_desc &j) {
       b = {{(n + 1) * 4, IN}, {j.m * (n + 1) * 4, INOUT}, {j.m * (n + 1) * 4, SCR}, {80 * 4, INOUT},
            {((n + 1 + kBpTile - 1) / kBpTile) * kMaxHid * 8, SCR}};  // one partial per tile
       break;
-    case GS_JOB_NEEDLE:  // ref (n x n interior), score ((n+1) x (n+4) aligned), band edge rows
-      b = {{n * n * 4, IN}, {(n + 1) * (n + 4) * 4, INOUT}, {2 * n * 8, SCR}};
+    case GS_JOB_NEEDLE:  // ref (n x n interior), score ((n+1) x (n+4) aligned), band edge rows / chunk flags
+      b = {{n * n * 4, IN}, {(n + 1) * (n + 4) * 4, INOUT},
+           {2 * n * 8, SCR}};
       break;
     case GS_JOB_LUD:
       b = {{n * n * 4, INOUT}};
@@ -153,9 +154,22 @@ int job_grid(const gs_job_desc &j) {
   return j.kind == GS_JOB_KMEANS ? 3 * sm_count() : 2 * sm_count();
 }
 
-// needle: one warp per 32-row band in flight, at most the job's SM share
+// needle_bands8 (8 x 8 blocks, 256-row bands; n % 256 == 0) is opt-in
+// (GS_NEEDLE8=1): measured 6.76 vs 5.69 ms at 24576^2 — a lone warp per SM
+// issues its 414-instruction step at IPC ~0.2 (fixed-latency chains and the
+// band polls), so the 3072 fat steps cost more than the shorter chain saves
+// (profiles/r02_needle8.txt)
+static bool needle8(const gs_job_desc &j) {
+  static const bool on = [] {
+    const char *e = getenv("GS_NEEDLE8");
+    return e && e[0] == '1';
+  }();
+  return on && j.n % kN8Band == 0;
+}
+
+// needle: one warp per band in flight, at most the job's SM share
 int needle_grid(const gs_job_desc &j) {
-  const int bands = (int)(j.n / 64);
+  const int bands = (int)(needle8(j) ? j.n / kN8Band : j.n / 64);
   return std::min(bands, 4 * sm_count());
 }
 
@@ -195,8 +209,8 @@ static std::vector<Shape> job_kernels(const gs_job_desc &j) {
               {(const void *)bp_adjust, g, kThreads}};
     case GS_JOB_NEEDLE:
     {
-      Shape s{(const void *)needle_bands, needle_grid(j), 32};
-      s.dsmem = kNwSmem;
+      Shape s{needle8(j) ? (const void *)needle_bands8 : (const void *)needle_bands, needle_grid(j), 32};
+      s.dsmem = needle8(j) ? kN8Smem : kNwSmem;
       return {s};
     }
     case GS_JOB_LUD:
@@ -518,9 +532,14 @@ int run_kernels(const gs_job_desc &j, std::vector<void *> &buf, cudaStream_t st,
       break;
     }
     case GS_JOB_NEEDLE: {
-      CUW(cudaFuncSetAttribute(needle_bands, cudaFuncAttributeMaxDynamicSharedMemorySize, kNwSmem));
-      needle_bands<<<needle_grid(j), 32, kNwSmem, st>>>((int32_t *)buf[1], (const int32_t *)buf[0], (int)n, tk,
-                                                        (unsigned long long *)buf[2]);
+      if (needle8(j)) {  // 8 x 8 blocks per lane step, 256-row bands
+        needle_bands8<<<needle_grid(j), 32, kN8Smem, st>>>((int32_t *)buf[1], (const int32_t *)buf[0], (int)n, tk,
+                                                           (unsigned long long *)buf[2]);
+      } else {
+        CUW(cudaFuncSetAttribute(needle_bands, cudaFuncAttributeMaxDynamicSharedMemorySize, kNwSmem));
+        needle_bands<<<needle_grid(j), 32, kNwSmem, st>>>((int32_t *)buf[1], (const int32_t *)buf[0], (int)n, tk,
+                                                          (unsigned long long *)buf[2]);
+      }
       ++launches;
       *out_idx = 1;
       break;
