@@ -32,3 +32,12 @@ def test_hotspot_four_step_pass_matches_oracle(n, iters):
     got = _checksum("hotspot", {"GS_HOTSPOT_STEPS": "4"}, n=n, iters=iters, seed=5)
     want = K.run("hotspot", n=n, iters=iters, seed=5)
     assert got == K.digest("hotspot", want)
+
+
+@pytest.mark.parametrize("n", [256, 512, 1024])
+def test_needle_8x8_bands_match_oracle(n):
+    """needle_bands8 (GS_NEEDLE8=1: 8 x 8 blocks per lane step, 256-row
+    bands, tagged-word band handoff) — bit-exact scores."""
+    got = _checksum("needle", {"GS_NEEDLE8": "1"}, n=n, seed=9)
+    want = K.run("needle", n=n, seed=9)
+    assert got == K.digest("needle", want)
