@@ -327,15 +327,20 @@ def cfg2_block(W, C, devices, workers, jobs_n, seed):
 
     jobs = C.darknet_mix(jobs_n * len(devices), seed, C.CFG2_SIZES, C.CFG2_BATCHES, C.CFG2_RESNET)
     foot = sum(C.host_footprint(j) for j in jobs)
+    # one ledger size for every run (as cfg 1): a ledger re-read per run
+    # moves with what the previous run left mapped, and the job arena sized
+    # from it would be re-allocated inside a timed run
+    cap = min(W.ledger_capacity(d) for d in devices)
     out = {"workload": f"cfg2: {len(jobs)} Darknet jobs (YOLOv3-tiny / ResNet-50, batch 32-64) on "
-                       f"{len(devices)} GPU(s)", "sum_footprint_gib": round(foot / 2**30, 1)}
+                       f"{len(devices)} GPU(s)", "sum_footprint_gib": round(foot / 2**30, 1),
+           "ledger_bytes_per_gpu": cap}
     for policy in ("mgb-warps", "sa", "cg:8"):
-        W.run_jobs(jobs, policy=policy, devices=devices, workers=workers)
+        W.run_jobs(jobs, policy=policy, devices=devices, workers=workers, ledger_bytes=cap)
         for d in devices:
             torch.cuda.synchronize(d)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
-        res = W.run_jobs(jobs, policy=policy, devices=devices, workers=workers)
+        res = W.run_jobs(jobs, policy=policy, devices=devices, workers=workers, ledger_bytes=cap)
         e1.record()
         for d in devices:
             torch.cuda.synchronize(d)

@@ -264,9 +264,17 @@ int run_job(const gs_job_desc &j, const Staged *stg, int mode, cudaStream_t st, 
   // GPU are read in place: the job's kernels never write an IN buffer, so
   // copying 50 GB of them per cfg 1 step D2D was pure HBM traffic.  INOUT
   // buffers (modified in place) still get a private copy.
+  // An INOUT buffer whose first kernel reads a separate source
+  // (reads_source: hotspot T, srad J, backprop w1) gets its private buffer
+  // uninitialised and the resident input as that source: 36 GB less D2D
+  // copy traffic per cfg 1 step.
   std::vector<char> alias(bufs.size(), 0);
+  std::vector<const void *> src(bufs.size(), nullptr);
   if (stg && !stg->host && stg->device == device)
-    for (size_t i = 0; i < bufs.size(); ++i) alias[i] = bufs[i].role == IN && stg->ptr[i] != nullptr;
+    for (size_t i = 0; i < bufs.size(); ++i) {
+      alias[i] = bufs[i].role == IN && stg->ptr[i] != nullptr;
+      if (bufs[i].role == INOUT && stg->ptr[i] != nullptr && reads_source(j, i)) src[i] = stg->ptr[i];
+    }
   auto release = [&]() {
     if (arena) {
       cudaStreamSynchronize(st);
@@ -354,7 +362,7 @@ int run_job(const gs_job_desc &j, const Staged *stg, int mode, cudaStream_t st, 
   CUE(cudaMemsetAsync(dsum, 0, 32, st));
   // inputs in
   for (size_t i = 0; i < bufs.size(); ++i) {
-    if (alias[i]) continue;  // read in place
+    if (alias[i] || src[i]) continue;  // read in place
     if (bufs[i].role == IN || bufs[i].role == INOUT) {
       if (stg) {
         if (stg->host) {
@@ -378,7 +386,8 @@ int run_job(const gs_job_desc &j, const Staged *stg, int mode, cudaStream_t st, 
   CUE(cudaEventRecord(e0, st));
   int out_idx = 0;
   int64_t launches = 0;
-  int rc = run_kernels(j, buf, st, &out_idx, &launches, host_scalar, reinterpret_cast<unsigned *>(dsum + 1));
+  int rc = run_kernels(j, buf, st, &out_idx, &launches, host_scalar, reinterpret_cast<unsigned *>(dsum + 1),
+                       src.data());
   if (rc) return rc;
   CUE(cudaEventRecord(e1, st));
   rec.n_kernels = (int32_t)launches;

@@ -96,7 +96,7 @@ std::vector<Buf> job_buffers(const gs_job_desc &j) {
            {(int64_t)GS_KMEANS_K * j.m * 8, SCR}, {(int64_t)GS_KMEANS_K * 8, SCR}};
       break;
     case GS_JOB_BACKPROP:
-      b = {{(n + 1) * 4, IN}, {j.m * (n + 1) * 4, INOUT}, {j.m * (n + 1) * 4, SCR}, {80 * 4, INOUT},
+      b = {{(n + 1) * 4, IN}, {j.m * (n + 1) * 4, INOUT}, {j.m * (n + 1) * 4, PING}, {80 * 4, INOUT},
            {((n + 1 + kBpTile - 1) / kBpTile) * kMaxHid * 8, SCR}};  // one partial per tile
       break;
     case GS_JOB_NEEDLE:  // ref (n x n interior), score ((n+1) x (n+4) aligned), band edge rows / chunk flags
@@ -391,9 +391,27 @@ int generate_inputs(const gs_job_desc &j, const std::vector<void *> &dst, cudaSt
 // Run the kernels of a job whose buffers are ready in `buf`.  Returns the
 // index of the buffer holding the primary output in *out_idx (hotspot and
 // srad ping-pong).  `kernels` counts launches.
+// INOUT buffers whose first reader can take a separate read-only source:
+// every later pass reads only what an earlier pass of the job wrote, so the
+// executor can skip the private copy of a resident input (hotspot T and srad
+// J ping-pong from the first pass on; backprop's first adjust writes w1 from
+// the source weights).
+bool reads_source(const gs_job_desc &j, size_t i) {
+  switch (j.kind) {
+    case GS_JOB_HOTSPOT:
+    case GS_JOB_SRAD:
+      return i == 0;
+    case GS_JOB_BACKPROP:
+      return i == 1;
+    default:
+      return false;
+  }
+}
+
 int run_kernels(const gs_job_desc &j, std::vector<void *> &buf, cudaStream_t st, int *out_idx, int64_t *kernels,
-                int32_t *host_scalar, unsigned *tk) {
+                int32_t *host_scalar, unsigned *tk, const void *const *src) {
   const int g = job_grid(j);
+  auto source = [&](size_t i) -> const void * { return src && src[i] ? src[i] : buf[i]; };
   const int64_t n = j.n;
   int64_t launches = 0;
   switch (j.kind) {
@@ -441,10 +459,14 @@ int run_kernels(const gs_job_desc &j, std::vector<void *> &buf, cudaStream_t st,
       CUW(cudaFuncSetAttribute(hotspot_step2, cudaFuncAttributeMaxDynamicSharedMemorySize, kHs2Smem));
       // TMA descriptors of the two temperature buffers and the power map
       // (tile boxes of 136 columns x 36 / 34 rows)
-      CUtensorMap mt, mt2, mp;
+      // (the first pass reads the input from `source(0)`, then T and T2
+      // ping-pong)
+      const float *t0 = (const float *)source(0);
+      CUtensorMap mt, mt2, mp, ms;
       int rc = make_tmap_f32(&mt, t, n, n, kHs2W, kHs2TR);
       if (!rc) rc = make_tmap_f32(&mt2, t2, n, n, kHs2W, kHs2TR);
       if (!rc) rc = make_tmap_f32(&mp, p, n, n, kHs2W, kHs2UR);
+      if (!rc) rc = make_tmap_f32(&ms, t0, n, n, kHs2W, kHs2TR);
       if (rc) return rc;
       const CUtensorMap *min = &mt, *min2 = &mt2;
       int it = 0;
@@ -455,14 +477,15 @@ int run_kernels(const gs_job_desc &j, std::vector<void *> &buf, cudaStream_t st,
       // so it is issue bound above the two-step pass's HBM time
       if (hotspot_four_steps() && it + 3 < j.iters) {
         CUW(cudaFuncSetAttribute(hotspot_step4, cudaFuncAttributeMaxDynamicSharedMemorySize, kHs4Smem));
-        CUtensorMap m4, m42, mp4;
+        CUtensorMap m4, m42, mp4, ms4;
         rc = make_tmap_f32(&m4, t, n, n, kHs4W, kHs4H);
         if (!rc) rc = make_tmap_f32(&m42, t2, n, n, kHs4W, kHs4H);
         if (!rc) rc = make_tmap_f32(&mp4, p, n, n, kHs4W, kHs4H);
+        if (!rc) rc = make_tmap_f32(&ms4, t0, n, n, kHs4W, kHs4H);
         if (rc) return rc;
         const CUtensorMap *q = &m4, *q2 = &m42;
         for (; it + 3 < j.iters; it += 4) {
-          hotspot_step4<<<g, 256, kHs4Smem, st>>>(*q, mp4, t2, (int)n, cc, rx1, ry1, rz1, tk);
+          hotspot_step4<<<g, 256, kHs4Smem, st>>>(it ? *q : ms4, mp4, t2, (int)n, cc, rx1, ry1, rz1, tk);
           ++launches;
           std::swap(t, t2);
           std::swap(q, q2);
@@ -470,13 +493,13 @@ int run_kernels(const gs_job_desc &j, std::vector<void *> &buf, cudaStream_t st,
         }
       }
       for (; it + 1 < j.iters; it += 2) {
-        hotspot_step2<<<g, 256, kHs2Smem, st>>>(*min, mp, t2, (int)n, cc, rx1, ry1, rz1, tk);
+        hotspot_step2<<<g, 256, kHs2Smem, st>>>(it ? *min : ms, mp, t2, (int)n, cc, rx1, ry1, rz1, tk);
         ++launches;
         std::swap(t, t2);
         std::swap(min, min2);
       }
       if (it < j.iters) {
-        hotspot_step<<<g, dim3(32, 8), 0, st>>>(t, p, t2, (int)n, cc, rx1, ry1, rz1, tk);
+        hotspot_step<<<g, dim3(32, 8), 0, st>>>(it ? t : t0, p, t2, (int)n, cc, rx1, ry1, rz1, tk);
         ++launches;
         std::swap(t, t2);
       }
@@ -486,9 +509,10 @@ int run_kernels(const gs_job_desc &j, std::vector<void *> &buf, cudaStream_t st,
     case GS_JOB_SRAD: {
       float *J = (float *)buf[0], *J2 = (float *)buf[1], *q0 = (float *)buf[2];
       const int roi = n < 128 ? (int)n : 128;
+      const float *J0 = (const float *)source(0);  // the first iteration's input
       for (int it = 0; it < j.iters; ++it) {
-        srad_stats<<<1, kThreads, 0, st>>>(J, (int)n, roi, q0);
-        srad_fused<<<g, dim3(32, 8), 0, st>>>(J, J2, (int)n, q0, tk);
+        srad_stats<<<1, kThreads, 0, st>>>(it ? J : J0, (int)n, roi, q0);
+        srad_fused<<<g, dim3(32, 8), 0, st>>>(it ? J : J0, J2, (int)n, q0, tk);
         launches += 2;
         std::swap(J, J2);
       }
@@ -520,12 +544,15 @@ int run_kernels(const gs_job_desc &j, std::vector<void *> &buf, cudaStream_t st,
       float *w1 = (float *)buf[1], *ow1 = (float *)buf[2], *state = (float *)buf[3];
       double *partial = (double *)buf[4];
       const int nh = (int)j.m;
-      // ow1 (momentum) is a SCR buffer: the executor zeroed it with the job's buffers
+      // ow1 (momentum) starts at zero: the first adjust does not read it, so
+      // it is written before it is read (PING); the first iteration reads
+      // the weights from `source(1)` and writes w1
+      const float *w0 = (const float *)source(1);
       for (int it = 0; it < j.iters; ++it) {
         const int ntiles = (int)((n + 1 + kBpTile - 1) / kBpTile);
-        bp_forward<<<g, kThreads, 0, st>>>(x, w1, n + 1, nh, partial, tk);
+        bp_forward<<<g, kThreads, 0, st>>>(x, it ? w1 : w0, n + 1, nh, partial, tk);
         bp_output<<<1, 32 * kMaxHid, 0, st>>>(partial, ntiles, nh, state);
-        bp_adjust<<<g, kThreads, 0, st>>>(x, w1, ow1, n + 1, nh, state, tk);
+        bp_adjust<<<g, kThreads, 0, st>>>(x, it ? w1 : w0, w1, ow1, it == 0, n + 1, nh, state, tk);
         launches += 3;
       }
       *out_idx = 1;

@@ -43,9 +43,13 @@ int err(int code, const std::string &m);
 std::vector<Buf> job_buffers(const gs_job_desc &j);
 int validate(const gs_job_desc &j);
 int generate_inputs(const gs_job_desc &j, const std::vector<void *> &dst, cudaStream_t st);
-// tk: the job's two tile-ticket counters (zeroed before the first kernel)
+// tk: the job's two tile-ticket counters (zeroed before the first kernel).
+// src: per buffer, a read-only copy of an INOUT buffer's input that the
+// job's first kernel reads instead of the (then uninitialised) buffer, or
+// null — only where reads_source() says the kernels support it.
 int run_kernels(const gs_job_desc &j, std::vector<void *> &buf, cudaStream_t st, int *out_idx, int64_t *kernels,
-                int32_t *host_scalar, unsigned *tk);
+                int32_t *host_scalar, unsigned *tk, const void *const *src = nullptr);
+bool reads_source(const gs_job_desc &j, size_t buf);
 int digest(const void *p, int64_t bytes, unsigned long long *dsum, cudaStream_t st);
 int64_t round_granule(int64_t b);
 
