@@ -395,13 +395,15 @@ int generate_inputs(const gs_job_desc &j, const std::vector<void *> &dst, cudaSt
 // every later pass reads only what an earlier pass of the job wrote, so the
 // executor can skip the private copy of a resident input (hotspot T and srad
 // J ping-pong from the first pass on; backprop's first adjust writes w1 from
-// the source weights).
+// the source weights; needle writes every interior score cell, so only row 0
+// and the 16-byte pad + column 0 lead of each row are copied).
 bool reads_source(const gs_job_desc &j, size_t i) {
   switch (j.kind) {
     case GS_JOB_HOTSPOT:
     case GS_JOB_SRAD:
       return i == 0;
     case GS_JOB_BACKPROP:
+    case GS_JOB_NEEDLE:
       return i == 1;
     default:
       return false;
@@ -559,6 +561,12 @@ int run_kernels(const gs_job_desc &j, std::vector<void *> &buf, cudaStream_t st,
       break;
     }
     case GS_JOB_NEEDLE: {
+      if (src && src[1]) {  // the boundary of the score matrix from the source
+        const size_t pitch = (size_t)(n + 4) * 4;
+        CUW(cudaMemcpyAsync(buf[1], src[1], pitch, cudaMemcpyDeviceToDevice, st));
+        CUW(cudaMemcpy2DAsync((char *)buf[1] + pitch, pitch, (const char *)src[1] + pitch, pitch, 16, (size_t)n,
+                              cudaMemcpyDeviceToDevice, st));
+      }
       if (needle8(j)) {  // 8 x 8 blocks per lane step, 256-row bands
         needle_bands8<<<needle_grid(j), 32, kN8Smem, st>>>((int32_t *)buf[1], (const int32_t *)buf[0], (int)n, tk,
                                                            (unsigned long long *)buf[2]);
