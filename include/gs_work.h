@@ -202,6 +202,14 @@ int gs_exec_sm_parts_layout(int32_t cuda_device, int32_t parts, int32_t *sms_out
  * denominator of the FP32 CUDA-core kernels (lud). */
 int gs_measure_fp32_peak(int32_t cuda_device, double *tflops);
 
+/* Self-test of srad's branch-free IEEE division (gs_kernels.cuh,
+ * srad_coeff_fast): n random operand pairs across and beyond its proven
+ * domain against __fdiv_rn, and n random coefficient windows against
+ * srad_coeff_one with ROI statistic q0sqr.  out4 = {division mismatches
+ * inside the domain, in-domain pairs, coefficient mismatches where the fast
+ * path claimed its proof, such windows}; both mismatch counts must be 0. */
+int gs_selftest_division(int32_t cuda_device, int64_t n, uint64_t seed, float q0sqr, int64_t *out4);
+
 /* ---- placement log of the most recent executor run ---------------------
  * Every call the run made into the decision engine, in the order the single
  * decision authority serialized them (the linearization SPEC.md:419 asks

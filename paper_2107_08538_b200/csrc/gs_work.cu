@@ -147,10 +147,11 @@ int validate(const gs_job_desc &j) {
 // Grid of every workload kernel: the job's SM share (2 blocks of 256
 // threads per SM on all 148 SMs) — resident-sized, so a probe's
 // thread_blocks is a real placement demand for mgb-sm.
+int srad_grid();
 int job_grid(const gs_job_desc &j) {
-  // srad's fused kernel and kmeans' assignment are issue / latency bound:
-  // 3 CTAs per SM (<= 85 registers) hide more latency than 2
-  if (j.kind == GS_JOB_SRAD) return 4 * sm_count();
+  // srad's streaming kernel and kmeans' assignment are issue / latency
+  // bound: 3 CTAs per SM (<= 85 registers) hide more latency than 2
+  if (j.kind == GS_JOB_SRAD) return srad_grid();
   return j.kind == GS_JOB_KMEANS ? 3 * sm_count() : 2 * sm_count();
 }
 
@@ -171,6 +172,46 @@ static bool needle8(const gs_job_desc &j) {
 int needle_grid(const gs_job_desc &j) {
   const int bands = (int)(needle8(j) ? j.n / kN8Band : j.n / 64);
   return std::min(bands, 4 * sm_count());
+}
+
+// GS_SRAD=2: the v2 block-tile kernel (srad_fused) instead of the warp
+// strips (srad_stream), for A/B measurement
+bool srad_v2() {
+  static const bool v2 = [] {
+    const char *e = getenv("GS_SRAD");
+    return e && e[0] == '2';
+  }();
+  return v2;
+}
+
+
+// srad_stream variant and its grid (resident CTAs per SM x SMs).  Measured
+// at 24576^2 x 10 (profiles/r02_srad_stream.txt): the default, two rows per
+// unrolled step at 3 CTAs per SM (74 registers), 20.53 ms; GS_SRAD=1 one row
+// at 4 CTAs 21.28; a: 4 rows at 4 CTAs (spills) 20.67; b: 4 rows at 3 CTAs
+// 21.31; d: 8 rows 24.61; 3: IEEE divisions only (no srad_coeff_fast)
+// 22.65; 2: the v2 block-tile kernel 27.0
+using SradStreamFn = void (*)(const float *, float *, int, const float *, unsigned *);
+static int srad_variant() {
+  static const int v = [] {
+    const char *e = getenv("GS_SRAD");
+    return e ? (int)e[0] : 0;
+  }();
+  return v;
+}
+SradStreamFn srad_stream_kernel() {
+  switch (srad_variant()) {
+    case '3': return srad_stream<false, 1, 4>;
+    case '1': return srad_stream<true, 1, 4>;
+    case 'a': return srad_stream<true, 4, 4>;
+    case 'b': return srad_stream<true, 4, 3>;
+    case 'd': return srad_stream<true, 8, 3>;
+    default: return srad_stream<true, 2, 3>;
+  }
+}
+int srad_grid() {
+  const int v = srad_variant();
+  return (v == '3' || v == '1' || v == 'a' ? 4 : 3) * sm_count();
 }
 
 bool hotspot_four_steps() {
@@ -197,7 +238,8 @@ static std::vector<Shape> job_kernels(const gs_job_desc &j) {
       return {s4, s2, {(const void *)hotspot_step, g, kThreads}};
     }
     case GS_JOB_SRAD:
-      return {{(const void *)srad_stats, 1, kThreads}, {(const void *)srad_fused, g, kThreads}};
+      return {{(const void *)srad_stats, 1, kThreads},
+              {srad_v2() ? (const void *)srad_fused : (const void *)srad_stream_kernel(), srad_grid(), kThreads}};
     case GS_JOB_KMEANS:
     {
       Shape a{(const void *)kmeans_assign_fn((int)j.m), g, kThreads};
@@ -514,7 +556,10 @@ int run_kernels(const gs_job_desc &j, std::vector<void *> &buf, cudaStream_t st,
       const float *J0 = (const float *)source(0);  // the first iteration's input
       for (int it = 0; it < j.iters; ++it) {
         srad_stats<<<1, kThreads, 0, st>>>(it ? J : J0, (int)n, roi, q0);
-        srad_fused<<<g, dim3(32, 8), 0, st>>>(it ? J : J0, J2, (int)n, q0, tk);
+        if (srad_v2())
+          srad_fused<<<g, dim3(32, 8), 0, st>>>(it ? J : J0, J2, (int)n, q0, tk);
+        else
+          srad_stream_kernel()<<<srad_grid(), kThreads, 0, st>>>(it ? J : J0, J2, (int)n, q0, tk);
         launches += 2;
         std::swap(J, J2);
       }
@@ -658,6 +703,89 @@ __global__ void __launch_bounds__(256) fp32_peak_kernel(float *out, int iters, f
   if (s == 1234.5f) out[threadIdx.x] = s;  // keeps the chains live
 }
 }  // namespace
+
+namespace {
+// random float: sign, exponent uniform in [e_lo, e_hi], random mantissa;
+// 1 in 16 an exact +0
+__device__ float selftest_float(uint64_t h, int e_lo, int e_hi) {
+  if ((h & 15) == 0) return 0.0f;
+  const uint32_t e = (uint32_t)(e_lo + (int)((h >> 4) % (uint64_t)(e_hi - e_lo + 1)) + 127);
+  const uint32_t m = (uint32_t)(h >> 20) & 0x7fffffu;
+  const uint32_t sgn = (uint32_t)(h >> 43) & 1u;
+  return __uint_as_float(sgn << 31 | e << 23 | m);
+}
+
+// fdiv_q over operands drawn across (and beyond) its proven domain vs
+// __fdiv_rn: out[0] = mismatches inside the domain, out[1] = in-domain pairs
+__global__ void selftest_division(int64_t n, uint64_t seed, unsigned long long *out) {
+  unsigned long long bad = 0, in = 0;
+  for (int64_t i = gtid(); i < n; i += gstride()) {
+    const float a = selftest_float(gs_hash64(seed, 2 * (uint64_t)i), -66, 66);
+    const float b = selftest_float(gs_hash64(seed, 2 * (uint64_t)i + 1), -66, 66);
+    const float ab = fabsf(a), bb = fabsf(b);
+    const bool dom = bb >= kDivLo && bb <= kDivHi &&
+                     ((ab >= kDivLo && ab <= kDivHi) || (__float_as_uint(a) == 0u && b > 0.0f));
+    if (!dom) continue;
+    ++in;
+    if (__float_as_uint(fdiv_q(a, b, fdiv_y1(b))) != __float_as_uint(__fdiv_rn(a, b))) ++bad;
+  }
+  atomicAdd(&out[0], bad);
+  atomicAdd(&out[1], in);
+}
+
+// srad_coeff_fast vs srad_coeff_one on random 5-point windows in the J
+// range (independent values, near-flat windows, exactly flat ones):
+// out[0] = mismatches where the fast path claimed ok, out[1] = ok count
+__global__ void selftest_srad_coeff(int64_t n, uint64_t seed, float q0sqr, unsigned long long *out) {
+  const float c4 = __fmul_rn(q0sqr, __fadd_rn(1.0f, q0sqr));
+  const float yc4 = fdiv_y1(c4);
+  unsigned long long bad = 0, okc = 0;
+  for (int64_t i = gtid(); i < n; i += gstride()) {
+    const uint64_t h = gs_hash64(seed, (uint64_t)i);
+    float v[5];
+    const int mode = (int)(h & 3);
+    const float base = selftest_float(gs_hash64(seed ^ 0x5bd1e995u, (uint64_t)i) | 1u, -10, 9);
+    for (int k = 0; k < 5; ++k) {
+      const uint64_t hk = gs_hash64(seed + 1 + k, (uint64_t)i);
+      if (mode == 0) {  // independent values over the whole J range
+        v[k] = fabsf(selftest_float(hk | 1u, -10, 9));
+      } else if (mode == 1) {  // a few ulps around one value
+        v[k] = __uint_as_float(__float_as_uint(fabsf(base)) + (uint32_t)(hk % 9) - 4u);
+      } else if (mode == 2) {  // flat: some neighbours equal to the centre
+        v[k] = (hk & 1) ? fabsf(base) : fabsf(base) * (1.0f + 0x1p-12f * (float)(hk % 7));
+      } else {  // the srad input distribution: 1 + u, u in [0, 1)
+        v[k] = 1.0f + (float)(hk >> 40) * 0x1p-24f;
+      }
+      if (!(v[k] >= kSradJLo && v[k] <= kSradJHi)) v[k] = 1.0f;
+    }
+    bool ok;
+    const float f = srad_coeff_fast(v[0], v[1], v[2], v[3], v[4], q0sqr, c4, yc4, ok);
+    const bool c4_ok = fabsf(c4) >= kDivLo && fabsf(c4) <= kDivHi;
+    if (!(ok && c4_ok)) continue;
+    ++okc;
+    if (__float_as_uint(f) != __float_as_uint(srad_coeff_one(v[0], v[1], v[2], v[3], v[4], q0sqr))) ++bad;
+  }
+  atomicAdd(&out[0], bad);
+  atomicAdd(&out[1], okc);
+}
+}  // namespace
+
+extern "C" int gs_selftest_division(int32_t cuda_device, int64_t n, uint64_t seed, float q0sqr, int64_t *out4) {
+  CUW(cudaSetDevice(cuda_device));
+  unsigned long long *d;
+  CUW(cudaMalloc(&d, 32));
+  CUW(cudaMemset(d, 0, 32));
+  int sms = 0;
+  CUW(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, cuda_device));
+  selftest_division<<<4 * sms, 256>>>(n, seed, d);
+  selftest_srad_coeff<<<4 * sms, 256>>>(n, seed, q0sqr, d + 2);
+  CUW(cudaGetLastError());
+  unsigned long long h[4];
+  CUW(cudaMemcpy(h, d, 32, cudaMemcpyDeviceToHost));
+  cudaFree(d);
+  for (int k = 0; k < 4; ++k) out4[k] = (int64_t)h[k];
+  return GS_OK;
+}
 
 extern "C" int gs_measure_fp32_peak(int32_t cuda_device, double *tflops) {
   CUW(cudaSetDevice(cuda_device));

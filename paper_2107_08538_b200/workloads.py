@@ -74,6 +74,7 @@ WORK_SIGNATURES = {
     "gs_exec_ledger_capacity": (c_int32, [c_int32, POINTER(c_int64)]),
     "gs_exec_unstage": (None, []),
     "gs_measure_fp32_peak": (c_int32, [c_int32, POINTER(c_double)]),
+    "gs_selftest_division": (c_int32, [c_int32, c_int64, c_uint64, c_float, POINTER(c_int64)]),
     "gs_exec_set_sm_parts": (c_int32, [c_int32]),
     "gs_capture_begin": (c_int32, [c_int32, POINTER(c_void_p)]),
     "gs_capture_malloc": (c_int32, [c_void_p, c_int64, POINTER(c_void_p)]),
@@ -232,6 +233,13 @@ def fp32_peak_tflops(device: int = 0) -> float:
     t = c_double()
     nat.check(lib().gs_measure_fp32_peak(device, ctypes.byref(t)))
     return t.value
+
+
+def selftest_division(n: int, seed: int = 1, q0sqr: float = 0.05, device: int = 0) -> dict:
+    """srad's branch-free division against __fdiv_rn (gs_selftest_division)."""
+    out = (c_int64 * 4)()
+    nat.check(lib().gs_selftest_division(device, n, seed, q0sqr, out))
+    return {"div_mismatches": out[0], "div_checked": out[1], "coeff_mismatches": out[2], "coeff_checked": out[3]}
 
 
 def ledger_capacity(device: int = 0) -> int:

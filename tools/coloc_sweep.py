@@ -44,15 +44,17 @@ def main():
     for parts, workers, policy in runs:
         W.set_sm_parts(parts)
         W.run_jobs(jobs, policy=policy, workers=workers, ledger_bytes=cap)
-        ms, sl = [], []
+        ms, sl, ta = [], [], []
         for _ in range(args.reps):
             res = W.run_jobs(jobs, policy=policy, workers=workers, ledger_bytes=cap)
             ms.append(res.makespan_ms)
+            ta += [r["turnaround_ms"] for r in res.records if r["state"] == "done"]
             sl += [(r["compute_ms"] / solo[mix[i].template] - 1) * 100 for i, r in enumerate(res.records)
                    if r["state"] == "done"]
         mk = statistics.fmean(ms)
         print(json.dumps({"capture": args.capture, "parts": parts, "workers": workers, "policy": policy, "makespan_ms": round(mk, 1),
                           "jobs_per_s": round(len(jobs) / (mk / 1000), 2),
+                          "mean_turnaround_ms": round(statistics.fmean(ta), 1),
                           "slowdown_mean_pct": round(statistics.fmean(sl), 1),
                           "slowdown_median_pct": round(statistics.median(sl), 1),
                           "layout": W.sm_parts_layout(parts) if parts > 1 else None}), flush=True)

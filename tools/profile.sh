@@ -19,7 +19,7 @@ cap() {  # name regex skip cmd...
     || echo "capture $name failed/timeout" >> $OUT/prof_errors.log
 }
 cap hotspot hotspot_step2 2 python tools/debug_job.py hotspot 24576 8
-cap srad srad_fused 3 python tools/debug_job.py srad 24576 5
+cap srad srad_stream 3 python tools/debug_job.py srad 24576 5
 cap kmeans kmeans_assign 2 python tools/debug_job.py kmeans 32000000 4 34
 cap bfs bfs_expand 9 python tools/debug_job.py bfs 128000000
 cap needle needle_bands 0 python tools/debug_job.py needle 24576
