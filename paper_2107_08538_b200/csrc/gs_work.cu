@@ -187,7 +187,8 @@ bool srad_v2() {
 
 // srad_stream variant and its grid (resident CTAs per SM x SMs).  Measured
 // at 24576^2 x 10 (profiles/r02_srad_stream.txt): the default, two rows per
-// unrolled step at 3 CTAs per SM (74 registers), 20.53 ms; GS_SRAD=1 one row
+// unrolled step at 3 CTAs per SM (74 registers), 19.19 ms (20.53 with six
+// range checks per coefficient instead of srad_coeff_fast's one); GS_SRAD=1 one row
 // at 4 CTAs 21.28; a: 4 rows at 4 CTAs (spills) 20.67; b: 4 rows at 3 CTAs
 // 21.31; d: 8 rows 24.61; 3: IEEE divisions only (no srad_coeff_fast)
 // 22.65; 2: the v2 block-tile kernel 27.0
@@ -743,24 +744,29 @@ __global__ void selftest_srad_coeff(int64_t n, uint64_t seed, float q0sqr, unsig
   for (int64_t i = gtid(); i < n; i += gstride()) {
     const uint64_t h = gs_hash64(seed, (uint64_t)i);
     float v[5];
-    const int mode = (int)(h & 3);
-    const float base = selftest_float(gs_hash64(seed ^ 0x5bd1e995u, (uint64_t)i) | 1u, -10, 9);
+    const int mode = (int)(h % 6);
+    const float base = selftest_float(gs_hash64(seed ^ 0x5bd1e995u, (uint64_t)i) | 1u, -4, 3);
     for (int k = 0; k < 5; ++k) {
       const uint64_t hk = gs_hash64(seed + 1 + k, (uint64_t)i);
       if (mode == 0) {  // independent values over the whole J range
-        v[k] = fabsf(selftest_float(hk | 1u, -10, 9));
+        v[k] = fabsf(selftest_float(hk | 1u, -4, 3));
       } else if (mode == 1) {  // a few ulps around one value
         v[k] = __uint_as_float(__float_as_uint(fabsf(base)) + (uint32_t)(hk % 9) - 4u);
       } else if (mode == 2) {  // flat: some neighbours equal to the centre
         v[k] = (hk & 1) ? fabsf(base) : fabsf(base) * (1.0f + 0x1p-12f * (float)(hk % 7));
-      } else {  // the srad input distribution: 1 + u, u in [0, 1)
+      } else if (mode == 3) {  // the srad input distribution: 1 + u, u in [0, 1)
         v[k] = 1.0f + (float)(hk >> 40) * 0x1p-24f;
+      } else if (mode == 4) {  // centre near the top, neighbours near the bottom: den -> 2^-8
+        v[k] = k == 0 ? kSradJHi * (1.0f - 0x1p-20f * (float)(hk % 64))
+                      : kSradJLo * (1.0f + 0x1p-20f * (float)(hk % 64));
+      } else {  // centre near the bottom, neighbours anywhere above: |L| large
+        v[k] = k == 0 ? kSradJLo * (1.0f + 0x1p-22f * (float)(hk % 16)) : 1.0f + (float)(hk >> 40) * 0x1p-20f;
       }
       if (!(v[k] >= kSradJLo && v[k] <= kSradJHi)) v[k] = 1.0f;
     }
     bool ok;
     const float f = srad_coeff_fast(v[0], v[1], v[2], v[3], v[4], q0sqr, c4, yc4, ok);
-    const bool c4_ok = fabsf(c4) >= kDivLo && fabsf(c4) <= kDivHi;
+    const bool c4_ok = srad_c4_ok(c4);
     if (!(ok && c4_ok)) continue;
     ++okc;
     if (__float_as_uint(f) != __float_as_uint(srad_coeff_one(v[0], v[1], v[2], v[3], v[4], q0sqr))) ++bad;
