@@ -186,12 +186,11 @@ bool srad_v2() {
 
 
 // srad_stream variant and its grid (resident CTAs per SM x SMs).  Measured
-// at 24576^2 x 10 (profiles/r02_srad_stream.txt): the default, two rows per
-// unrolled step at 3 CTAs per SM (74 registers), 19.19 ms (20.53 with six
-// range checks per coefficient instead of srad_coeff_fast's one); GS_SRAD=1 one row
-// at 4 CTAs 21.28; a: 4 rows at 4 CTAs (spills) 20.67; b: 4 rows at 3 CTAs
-// 21.31; d: 8 rows 24.61; 3: IEEE divisions only (no srad_coeff_fast)
-// 22.65; 2: the v2 block-tile kernel 27.0
+// at 24576^2 x 10 with the packed coefficient / update (profiles/
+// r02_srad_stream.txt): the default, four rows per unrolled step at 3 CTAs
+// per SM, 16.31 ms; c: two rows 16.54; 1: one row at 4 CTAs 16.61; a: four
+// rows at 4 CTAs (spills) 16.30; 3: IEEE divisions only, scalar, 22.65;
+// 2: the v2 block-tile kernel 27.0
 using SradStreamFn = void (*)(const float *, float *, int, const float *, unsigned *);
 static int srad_variant() {
   static const int v = [] {
@@ -205,9 +204,9 @@ SradStreamFn srad_stream_kernel() {
     case '3': return srad_stream<false, 1, 4>;
     case '1': return srad_stream<true, 1, 4>;
     case 'a': return srad_stream<true, 4, 4>;
-    case 'b': return srad_stream<true, 4, 3>;
+    case 'c': return srad_stream<true, 2, 3>;
     case 'd': return srad_stream<true, 8, 3>;
-    default: return srad_stream<true, 2, 3>;
+    default: return srad_stream<true, 4, 3>;
   }
 }
 int srad_grid() {
@@ -764,12 +763,21 @@ __global__ void selftest_srad_coeff(int64_t n, uint64_t seed, float q0sqr, unsig
       }
       if (!(v[k] >= kSradJLo && v[k] <= kSradJHi)) v[k] = 1.0f;
     }
-    bool ok;
+    bool ok, ok2;
     const float f = srad_coeff_fast(v[0], v[1], v[2], v[3], v[4], q0sqr, c4, yc4, ok);
+    // the packed form on (this window, the window rotated by one), both halves
+    const float2 f2 = srad_coeff_fast2(make_float2(v[0], v[1]), make_float2(v[1], v[2]), make_float2(v[2], v[3]),
+                                       make_float2(v[3], v[4]), make_float2(v[4], v[0]), q0sqr, c4, yc4, ok2);
     const bool c4_ok = srad_c4_ok(c4);
     if (!(ok && c4_ok)) continue;
     ++okc;
-    if (__float_as_uint(f) != __float_as_uint(srad_coeff_one(v[0], v[1], v[2], v[3], v[4], q0sqr))) ++bad;
+    const uint32_t want = __float_as_uint(srad_coeff_one(v[0], v[1], v[2], v[3], v[4], q0sqr));
+    if (__float_as_uint(f) != want) ++bad;
+    if (ok2) {
+      if (__float_as_uint(f2.x) != want ||
+          __float_as_uint(f2.y) != __float_as_uint(srad_coeff_one(v[1], v[2], v[3], v[4], v[0], q0sqr)))
+        ++bad;
+    }
   }
   atomicAdd(&out[0], bad);
   atomicAdd(&out[1], okc);
