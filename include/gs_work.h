@@ -106,7 +106,10 @@ int gs_request_from_launches(const gs_launch_desc *launches, int32_t n, const in
  * granule, plus the 8 MiB device heap the reference counts per task
  * (task_builder.py:264-268). */
 int gs_job_probe(const gs_job_desc *job, gs_probe *out);
-/* Bytes of the job's host inputs / outputs (for the e2e accounting). */
+/* Bytes a job moves host -> device / device -> host in e2e mode: its
+ * inputs less what it rebuilds on the device (bfs's transposed CSR) and,
+ * for needle's score matrix, only the boundary (row 0 and the pad + column
+ * 0 lead of every row); its outputs. */
 int gs_job_io_bytes(const gs_job_desc *job, int64_t *in_bytes, int64_t *out_bytes);
 
 /* Run one job to completion on `cuda_device` (isolated), for tests and the

@@ -268,12 +268,24 @@ int run_job(const gs_job_desc &j, const Staged *stg, int mode, cudaStream_t st, 
   // (reads_source: hotspot T, srad J, backprop w1) gets its private buffer
   // uninitialised and the resident input as that source: 36 GB less D2D
   // copy traffic per cfg 1 step.
-  std::vector<char> alias(bufs.size(), 0);
+  // From pinned host memory (e2e) a job moves only real inputs over PCIe:
+  // derived inputs (bfs's transposed CSR) are rebuilt on the device, and
+  // needle copies only its score matrix's boundary (reads_source_host).
+  std::vector<char> alias(bufs.size(), 0), derive(bufs.size(), 0);
   std::vector<const void *> src(bufs.size(), nullptr);
   if (stg && !stg->host && stg->device == device)
     for (size_t i = 0; i < bufs.size(); ++i) {
       alias[i] = bufs[i].role == IN && stg->ptr[i] != nullptr;
       if (bufs[i].role == INOUT && stg->ptr[i] != nullptr && reads_source(j, i)) src[i] = stg->ptr[i];
+    }
+  bool need_derive = false;
+  if (stg && stg->host)
+    for (size_t i = 0; i < bufs.size(); ++i) {
+      if (derived_input(j, i)) derive[i] = need_derive = true;
+      if (bufs[i].role == INOUT && stg->ptr[i] != nullptr && reads_source_host(j, i)) {
+        src[i] = stg->ptr[i];
+        rec.h2d_bytes += source_host_bytes(j, i);  // copied by the job's first step
+      }
     }
   auto release = [&]() {
     if (arena) {
@@ -362,7 +374,7 @@ int run_job(const gs_job_desc &j, const Staged *stg, int mode, cudaStream_t st, 
   CUE(cudaMemsetAsync(dsum, 0, 32, st));
   // inputs in
   for (size_t i = 0; i < bufs.size(); ++i) {
-    if (alias[i] || src[i]) continue;  // read in place
+    if (alias[i] || src[i] || derive[i]) continue;  // read in place / rebuilt below
     if (bufs[i].role == IN || bufs[i].role == INOUT) {
       if (stg) {
         if (stg->host) {
@@ -380,6 +392,9 @@ int run_job(const gs_job_desc &j, const Staged *stg, int mode, cudaStream_t st, 
   }
   if (!stg) {  // unstaged: synthesize the inputs in place
     int rc = generate_inputs(j, buf, st);
+    if (rc) return rc;
+  } else if (need_derive) {
+    int rc = derive_inputs(j, buf, st);
     if (rc) return rc;
   }
   rec.setup_ms = ms_since(t_admit);

@@ -365,9 +365,17 @@ extern "C" int gs_job_io_bytes(const gs_job_desc *job, int64_t *in_bytes, int64_
   int rc = validate(*job);
   if (rc) return rc;
   int64_t i = 0, o = 0;
-  for (const Buf &b : job_buffers(*job)) {
-    if (b.role == IN || b.role == INOUT) i += b.bytes;
+  const std::vector<Buf> bufs = job_buffers(*job);
+  for (size_t k = 0; k < bufs.size(); ++k) {
+    const Buf &b = bufs[k];
     if (b.role == OUT || b.role == INOUT) o += b.bytes;
+    if (b.role != IN && b.role != INOUT) continue;
+    if (derived_input(*job, k)) continue;  // rebuilt on the device
+    if (reads_source_host(*job, k)) {  // needle: row 0 + the 16-byte lead of rows 1..n
+      i += source_host_bytes(*job, k);
+      continue;
+    }
+    i += b.bytes;
   }
   if (in_bytes) *in_bytes = i;
   if (out_bytes) *out_bytes = o;
@@ -375,6 +383,37 @@ extern "C" int gs_job_io_bytes(const gs_job_desc *job, int64_t *in_bytes, int64_
 }
 
 namespace gsw {
+
+// Inputs a job can derive on the device from its other inputs: bfs's
+// transposed CSR (in_row, in_col; the bottom-up levels' view of the graph).
+// A job whose inputs come from host memory builds them with
+// derive_inputs instead of moving them over PCIe (3 GB per 128 M-vertex
+// graph).
+bool derived_input(const gs_job_desc &j, size_t i) { return j.kind == GS_JOB_BFS && (i == 7 || i == 8); }
+
+// bfs: in-degree histogram, inclusive scan, scatter.  Scratch comes from the
+// job's own buffers (no allocation outside its probe): the level array
+// (n x 4 B, written by the first kernel) holds the scatter cursors and the
+// V bitmap the scan's temporary storage (re-zeroed after).
+int derive_inputs(const gs_job_desc &j, std::vector<void *> &buf, cudaStream_t st) {
+  if (j.kind != GS_JOB_BFS) return GS_OK;
+  const int g = 4 * sm_count();
+  const int64_t n = j.n;
+  const int32_t *row = (const int32_t *)buf[0], *col = (const int32_t *)buf[1];
+  int32_t *in_row = (int32_t *)buf[7], *cursor = (int32_t *)buf[2];
+  const size_t v_bytes = (size_t)bfs_words4(n) * 16;
+  CUW(cudaMemsetAsync(in_row, 0, (n + 1) * 4, st));
+  bfs_indeg<<<g, kThreads, 0, st>>>(col, n * GS_BFS_DEGREE, in_row + 1);
+  size_t tmp_bytes = 0;
+  CUW(cub::DeviceScan::InclusiveSum(nullptr, tmp_bytes, in_row + 1, in_row + 1, (int)n, st));
+  if (tmp_bytes > v_bytes) return err(GS_ERR_CONFIG, "bfs: scan scratch exceeds the visited bitmap");
+  CUW(cub::DeviceScan::InclusiveSum(buf[4], tmp_bytes, in_row + 1, in_row + 1, (int)n, st));
+  CUW(cudaMemcpyAsync(cursor, in_row, n * 4, cudaMemcpyDeviceToDevice, st));
+  bfs_scatter<<<g, kThreads, 0, st>>>(row, col, n, cursor, (int32_t *)buf[8]);
+  CUW(cudaMemsetAsync(buf[4], 0, v_bytes, st));
+  CUW(cudaGetLastError());
+  return GS_OK;
+}
 
 // Generate a job's IN/INOUT buffers into `dst` (device pointers, one per
 // buffer; nullptr for other roles).
@@ -439,6 +478,15 @@ int generate_inputs(const gs_job_desc &j, const std::vector<void *> &dst, cudaSt
 // J ping-pong from the first pass on; backprop's first adjust writes w1 from
 // the source weights; needle writes every interior score cell, so only row 0
 // and the 16-byte pad + column 0 lead of each row are copied).
+// (from pinned host memory only needle's boundary copy applies: the stencil
+// and backprop kernels read their source in bulk, which stays an H2D copy)
+bool reads_source_host(const gs_job_desc &j, size_t i) { return j.kind == GS_JOB_NEEDLE && i == 1; }
+// bytes such a buffer moves from its source: needle's row 0 + the 16-byte
+// lead (pad + column 0) of rows 1..n
+int64_t source_host_bytes(const gs_job_desc &j, size_t i) {
+  return reads_source_host(j, i) ? (j.n + 4) * 4 + 16 * j.n : 0;
+}
+
 bool reads_source(const gs_job_desc &j, size_t i) {
   switch (j.kind) {
     case GS_JOB_HOTSPOT:
@@ -606,11 +654,11 @@ int run_kernels(const gs_job_desc &j, std::vector<void *> &buf, cudaStream_t st,
       break;
     }
     case GS_JOB_NEEDLE: {
-      if (src && src[1]) {  // the boundary of the score matrix from the source
+      if (src && src[1]) {  // the boundary of the score matrix from the source (HBM or pinned host)
         const size_t pitch = (size_t)(n + 4) * 4;
-        CUW(cudaMemcpyAsync(buf[1], src[1], pitch, cudaMemcpyDeviceToDevice, st));
+        CUW(cudaMemcpyAsync(buf[1], src[1], pitch, cudaMemcpyDefault, st));
         CUW(cudaMemcpy2DAsync((char *)buf[1] + pitch, pitch, (const char *)src[1] + pitch, pitch, 16, (size_t)n,
-                              cudaMemcpyDeviceToDevice, st));
+                              cudaMemcpyDefault, st));
       }
       if (needle8(j)) {  // 8 x 8 blocks per lane step, 256-row bands
         needle_bands8<<<needle_grid(j), 32, kN8Smem, st>>>((int32_t *)buf[1], (const int32_t *)buf[0], (int)n, tk,

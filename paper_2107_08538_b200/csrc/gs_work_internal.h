@@ -50,6 +50,10 @@ int generate_inputs(const gs_job_desc &j, const std::vector<void *> &dst, cudaSt
 int run_kernels(const gs_job_desc &j, std::vector<void *> &buf, cudaStream_t st, int *out_idx, int64_t *kernels,
                 int32_t *host_scalar, unsigned *tk, const void *const *src = nullptr);
 bool reads_source(const gs_job_desc &j, size_t buf);
+bool reads_source_host(const gs_job_desc &j, size_t buf);
+int64_t source_host_bytes(const gs_job_desc &j, size_t buf);
+bool derived_input(const gs_job_desc &j, size_t buf);
+int derive_inputs(const gs_job_desc &j, std::vector<void *> &buf, cudaStream_t st);
 int digest(const void *p, int64_t bytes, unsigned long long *dsum, cudaStream_t st);
 int64_t round_granule(int64_t b);
 

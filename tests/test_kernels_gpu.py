@@ -181,3 +181,28 @@ def test_executor_resident_inputs_match_solo():
         W.unstage()
     assert res.completed == 2 * len(jobs) and res.oom == 0
     assert [r["checksum"] for r in res.records] == solo + solo
+
+
+def test_executor_e2e_rebuilds_derived_inputs():
+    """Inputs in pinned host memory: bfs rebuilds its transposed CSR on the
+    device instead of copying it, needle copies only its score matrix's
+    boundary; outputs still equal the solo runs and the bytes moved equal
+    gs_job_io_bytes (less than the jobs' whole input buffers)."""
+    jobs = [W.Job("bfs", n=300_000, seed=41), W.Job("needle", n=1024, seed=42), W.Job("bfs", n=1_000_003, seed=43),
+            W.Job("needle", n=512, seed=44), W.Job("hotspot", n=512, iters=3, seed=45)]
+    solo = [W.run_solo(j)[1].checksum for j in jobs]
+    W.stage(jobs, [0], W.MODE_E2E)
+    try:
+        res = W.run_jobs(jobs, policy="mgb-warps", workers=3, mode=W.MODE_E2E)
+    finally:
+        W.unstage()
+    assert res.completed == len(jobs) and res.oom == 0
+    assert [r["checksum"] for r in res.records] == solo
+    for r, j in zip(res.records, jobs):
+        i, _ = W.io_bytes(j)
+        assert r["h2d_bytes"] == i
+        n = j.n
+        if j.kind == "bfs":  # row_ptr + col only (not the transposed pair)
+            assert i == (n + 1) * 4 + n * 6 * 4
+        if j.kind == "needle":  # the reference matrix + the score boundary
+            assert i == n * n * 4 + (n + 4) * 4 + 16 * n
