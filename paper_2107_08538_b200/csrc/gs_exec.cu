@@ -401,15 +401,19 @@ int run_job(const gs_job_desc &j, const Staged *stg, int mode, cudaStream_t st, 
   CUE(cudaEventRecord(e0, st));
   int out_idx = 0;
   int64_t launches = 0;
+  bool digested = false;
   int rc = run_kernels(j, buf, st, &out_idx, &launches, host_scalar, reinterpret_cast<unsigned *>(dsum + 1),
-                       src.data());
+                       src.data(), &digested);
   if (rc) return rc;
   CUE(cudaEventRecord(e1, st));
   rec.n_kernels = (int32_t)launches;
-  kernel_count->fetch_add(launches + 1);
-  // outputs: the primary output buffer (and every OUT buffer in e2e)
-  rc = digest(buf[out_idx], bufs[out_idx].bytes, dsum, st);
-  if (rc) return rc;
+  kernel_count->fetch_add(launches + (digested ? 0 : 1));
+  // outputs: the primary output buffer (and every OUT buffer in e2e); its
+  // digest unless the last kernel already summed it
+  if (!digested) {
+    rc = digest(buf[out_idx], bufs[out_idx].bytes, dsum, st);
+    if (rc) return rc;
+  }
   if (mode == GS_MODE_E2E) {
     if (stg && stg->host_out) {
       host_out = stg->host_out;
@@ -439,7 +443,7 @@ int run_job(const gs_job_desc &j, const Staged *stg, int mode, cudaStream_t st, 
   rec.gen_ms = ms;
   CUE(cudaEventElapsedTime(&ms, e1, ed));
   rec.tail_ms = ms;
-  rec.checksum = *host_sum;
+  rec.checksum = *host_sum + (digested ? digest_tail(bufs[out_idx].bytes) : 0ull);
   return GS_OK;
 }
 

@@ -191,7 +191,7 @@ bool srad_v2() {
 // per SM, 16.31 ms; c: two rows 16.54; 1: one row at 4 CTAs 16.61; a: four
 // rows at 4 CTAs (spills) 16.30; 3: IEEE divisions only, scalar, 22.65;
 // 2: the v2 block-tile kernel 27.0
-using SradStreamFn = void (*)(const float *, float *, int, const float *, unsigned *);
+using SradStreamFn = void (*)(const float *, float *, int, const float *, unsigned *, unsigned long long *);
 static int srad_variant() {
   static const int v = [] {
     const char *e = getenv("GS_SRAD");
@@ -501,8 +501,12 @@ bool reads_source(const gs_job_desc &j, size_t i) {
 }
 
 int run_kernels(const gs_job_desc &j, std::vector<void *> &buf, cudaStream_t st, int *out_idx, int64_t *kernels,
-                int32_t *host_scalar, unsigned *tk, const void *const *src) {
+                int32_t *host_scalar, unsigned *tk, const void *const *src, bool *digested) {
   const int g = job_grid(j);
+  // the job's output digest accumulator (tk's control block word 0, zeroed
+  // with it) when the caller lets the last kernel compute the digest
+  unsigned long long *dg = digested ? reinterpret_cast<unsigned long long *>(tk) - 1 : nullptr;
+  if (digested) *digested = false;
   auto source = [&](size_t i) -> const void * { return src && src[i] ? src[i] : buf[i]; };
   const int64_t n = j.n;
   int64_t launches = 0;
@@ -585,13 +589,17 @@ int run_kernels(const gs_job_desc &j, std::vector<void *> &buf, cudaStream_t st,
         }
       }
       for (; it + 1 < j.iters; it += 2) {
-        hotspot_step2<<<g, 256, kHs2Smem, st>>>(it ? *min : ms, mp, t2, (int)n, cc, rx1, ry1, rz1, tk);
+        const bool last = dg && it + 2 == j.iters;
+        hotspot_step2<<<g, 256, kHs2Smem, st>>>(it ? *min : ms, mp, t2, (int)n, cc, rx1, ry1, rz1, tk,
+                                                 last ? dg : nullptr);
+        if (last) *digested = true;
         ++launches;
         std::swap(t, t2);
         std::swap(min, min2);
       }
       if (it < j.iters) {
-        hotspot_step<<<g, dim3(32, 8), 0, st>>>(it ? t : t0, p, t2, (int)n, cc, rx1, ry1, rz1, tk);
+        hotspot_step<<<g, dim3(32, 8), 0, st>>>(it ? t : t0, p, t2, (int)n, cc, rx1, ry1, rz1, tk, dg);
+        if (dg) *digested = true;
         ++launches;
         std::swap(t, t2);
       }
@@ -607,7 +615,9 @@ int run_kernels(const gs_job_desc &j, std::vector<void *> &buf, cudaStream_t st,
         if (srad_v2())
           srad_fused<<<g, dim3(32, 8), 0, st>>>(it ? J : J0, J2, (int)n, q0, tk);
         else
-          srad_stream_kernel()<<<srad_grid(), kThreads, 0, st>>>(it ? J : J0, J2, (int)n, q0, tk);
+          srad_stream_kernel()<<<srad_grid(), kThreads, 0, st>>>(it ? J : J0, J2, (int)n, q0, tk,
+                                                                 it + 1 == j.iters ? dg : nullptr);
+        if (!srad_v2() && dg && it + 1 == j.iters) *digested = true;
         launches += 2;
         std::swap(J, J2);
       }
@@ -647,7 +657,9 @@ int run_kernels(const gs_job_desc &j, std::vector<void *> &buf, cudaStream_t st,
         const int ntiles = (int)((n + 1 + kBpTile - 1) / kBpTile);
         bp_forward<<<g, kThreads, 0, st>>>(x, it ? w1 : w0, n + 1, nh, partial, tk);
         bp_output<<<1, 32 * kMaxHid, 0, st>>>(partial, ntiles, nh, state);
-        bp_adjust<<<g, kThreads, 0, st>>>(x, it ? w1 : w0, w1, ow1, it == 0, n + 1, nh, state, tk);
+        bp_adjust<<<g, kThreads, 0, st>>>(x, it ? w1 : w0, w1, ow1, it == 0, n + 1, nh, state, tk,
+                                          it + 1 == j.iters ? dg : nullptr);
+        if (dg && it + 1 == j.iters) *digested = true;
         launches += 3;
       }
       *out_idx = 1;
@@ -666,7 +678,8 @@ int run_kernels(const gs_job_desc &j, std::vector<void *> &buf, cudaStream_t st,
       } else {
         CUW(cudaFuncSetAttribute(needle_bands, cudaFuncAttributeMaxDynamicSharedMemorySize, kNwSmem));
         needle_bands<<<needle_grid(j), 32, kNwSmem, st>>>((int32_t *)buf[1], (const int32_t *)buf[0], (int)n, tk,
-                                                          (unsigned long long *)buf[2]);
+                                                          (unsigned long long *)buf[2], dg);
+        if (dg) *digested = true;
       }
       ++launches;
       *out_idx = 1;
@@ -720,6 +733,12 @@ int run_kernels(const gs_job_desc &j, std::vector<void *> &buf, cudaStream_t st,
   CUW(cudaGetLastError());
   *kernels += launches;
   return GS_OK;
+}
+
+// the n(n-1)/2 term of a digest whose word sum a kernel accumulated
+unsigned long long digest_tail(int64_t bytes) {
+  const unsigned long long nw = (unsigned long long)(bytes / 4);
+  return (nw & 1) ? nw * ((nw - 1) / 2) : (nw / 2) * (nw - 1);
 }
 
 int digest(const void *p, int64_t bytes, unsigned long long *dsum, cudaStream_t st) {

@@ -47,8 +47,12 @@ int generate_inputs(const gs_job_desc &j, const std::vector<void *> &dst, cudaSt
 // src: per buffer, a read-only copy of an INOUT buffer's input that the
 // job's first kernel reads instead of the (then uninitialised) buffer, or
 // null — only where reads_source() says the kernels support it.
+// digested: non-null lets the job's last kernel accumulate the output digest
+// (C * word sum) into tk's control word 0; *digested then says whether it did
+// (the caller skips digest() and adds digest_tail to the read-back).
 int run_kernels(const gs_job_desc &j, std::vector<void *> &buf, cudaStream_t st, int *out_idx, int64_t *kernels,
-                int32_t *host_scalar, unsigned *tk, const void *const *src = nullptr);
+                int32_t *host_scalar, unsigned *tk, const void *const *src = nullptr, bool *digested = nullptr);
+unsigned long long digest_tail(int64_t bytes);
 bool reads_source(const gs_job_desc &j, size_t buf);
 bool reads_source_host(const gs_job_desc &j, size_t buf);
 int64_t source_host_bytes(const gs_job_desc &j, size_t buf);
