@@ -230,12 +230,13 @@ static std::vector<Shape> job_kernels(const gs_job_desc &j) {
       return {{(const void *)bfs_expand, g, kBfsThreads}, {(const void *)bfs_commit, g, kBfsThreads}};
     case GS_JOB_HOTSPOT:
     {
-      Shape s2{(const void *)hotspot_step2, g, kThreads};
-      s2.dsmem = kHs2Smem;
-      if (j.iters < 4 || !hotspot_four_steps()) return {s2, {(const void *)hotspot_step, g, kThreads}};
+      // (the last two-step pass is the digesting instance)
+      Shape s2{(const void *)hotspot_step2<false>, g, kThreads}, s2d{(const void *)hotspot_step2<true>, g, kThreads};
+      s2.dsmem = s2d.dsmem = kHs2Smem;
+      if (j.iters < 4 || !hotspot_four_steps()) return {s2, s2d, {(const void *)hotspot_step, g, kThreads}};
       Shape s4{(const void *)hotspot_step4, g, kThreads};
       s4.dsmem = kHs4Smem;
-      return {s4, s2, {(const void *)hotspot_step, g, kThreads}};
+      return {s4, s2, s2d, {(const void *)hotspot_step, g, kThreads}};
     }
     case GS_JOB_SRAD:
       return {{(const void *)srad_stats, 1, kThreads},
@@ -552,7 +553,8 @@ int run_kernels(const gs_job_desc &j, std::vector<void *> &buf, cudaStream_t st,
       // two time steps per pass through shared memory (~6.5 B/cell-step);
       // an odd step count ends with one single-step pass.  (A register-only
       // two-step variant was FP32-issue bound: 2.5 updates per output.)
-      CUW(cudaFuncSetAttribute(hotspot_step2, cudaFuncAttributeMaxDynamicSharedMemorySize, kHs2Smem));
+      CUW(cudaFuncSetAttribute(hotspot_step2<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kHs2Smem));
+      CUW(cudaFuncSetAttribute(hotspot_step2<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kHs2Smem));
       // TMA descriptors of the two temperature buffers and the power map
       // (tile boxes of 136 columns x 36 / 34 rows)
       // (the first pass reads the input from `source(0)`, then T and T2
@@ -590,8 +592,10 @@ int run_kernels(const gs_job_desc &j, std::vector<void *> &buf, cudaStream_t st,
       }
       for (; it + 1 < j.iters; it += 2) {
         const bool last = dg && it + 2 == j.iters;
-        hotspot_step2<<<g, 256, kHs2Smem, st>>>(it ? *min : ms, mp, t2, (int)n, cc, rx1, ry1, rz1, tk,
-                                                 last ? dg : nullptr);
+        if (last)
+          hotspot_step2<true><<<g, 256, kHs2Smem, st>>>(it ? *min : ms, mp, t2, (int)n, cc, rx1, ry1, rz1, tk, dg);
+        else
+          hotspot_step2<false><<<g, 256, kHs2Smem, st>>>(it ? *min : ms, mp, t2, (int)n, cc, rx1, ry1, rz1, tk);
         if (last) *digested = true;
         ++launches;
         std::swap(t, t2);
