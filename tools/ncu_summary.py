@@ -1,54 +1,62 @@
-"""One line per ncu report: DRAM bytes, duration, achieved DRAM GB/s,
-occupancy and pipe utilisation (the numbers profiles/ cites).
+"""One line per ncu capture of tools/profile.sh (run where the .ncu-rep files are).
 
-    python tools/ncu_summary.py gpurun_out/prof_*.ncu-rep
+    python tools/ncu_summary.py gpurun_out > profiles/<tag>_ncu_current_kernels.txt
+    python tools/ncu_summary.py gpurun_out/prof_srad.ncu-rep ...
+
+Per capture: kernel, device time, DRAM bytes and rate, issue-active and
+SM-throughput %, warps-active %, registers, grid, the top stall reasons.
 """
 
+from __future__ import annotations
+
 import csv
+import glob
 import io
+import os
 import subprocess
 import sys
 
-METRICS = ["dram__bytes_read.sum", "dram__bytes_write.sum", "gpu__time_duration.sum", "launch__registers_per_thread",
-           "launch__grid_size", "launch__block_size", "sm__warps_active.avg.pct_of_peak_sustained_active",
-           "dram__throughput.avg.pct_of_peak_sustained_elapsed", "sm__throughput.avg.pct_of_peak_sustained_elapsed",
-           "sm__pipe_tensor_op_hmma_cycles_active.avg.pct_of_peak_sustained_active",
-           "sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active"]
-SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "ns": 1e-9, "us": 1e-6, "usecond": 1e-6,
-         "ms": 1e-3, "msecond": 1e-3, "nsecond": 1e-9}
+SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "ns": 1e-9, "us": 1e-6, "ms": 1e-3, "s": 1.0,
+         "nsecond": 1e-9, "usecond": 1e-6, "msecond": 1e-3, "second": 1.0}
 
 
-def summarize(path: str) -> str:
-    out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv", "--metrics", ",".join(METRICS)],
-                         capture_output=True, text=True).stdout
-    rows = list(csv.reader(io.StringIO(out)))
-    if len(rows) < 3:
-        return f"{path}: no data"
-    h, u, v = rows[0], rows[1], rows[2]
-    d = {h[i]: (v[i], u[i]) for i in range(len(h))}
+def main() -> int:
+    args = sys.argv[1:] or ["gpurun_out"]
+    reps = [a for a in args if a.endswith(".ncu-rep")]
+    for a in args:
+        if os.path.isdir(a):
+            reps += sorted(glob.glob(os.path.join(a, "prof_*.ncu-rep")))
+    for rep in reps:
+        out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+        rows = list(csv.reader(io.StringIO(out)))
+        if len(rows) < 3:
+            print(f"{os.path.basename(rep)}: no data")
+            continue
+        h, u, v = rows[0], rows[1], rows[2]
+        d = dict(zip(h, v))
+        units = dict(zip(h, u))
 
-    def num(k):
-        if k not in d or d[k][0] in ("", "n/a"):
-            return None
-        return float(d[k][0].replace(",", "")) * SCALE.get(d[k][1], 1.0)
+        def num(k):
+            try:
+                return float(d[k].replace(",", "")) * SCALE.get(units.get(k, ""), 1.0)
+            except (KeyError, ValueError):
+                return float("nan")
 
-    rd, wr, t = num("dram__bytes_read.sum"), num("dram__bytes_write.sum"), num("gpu__time_duration.sum")
-    name = d["Kernel Name"][0].split("(")[0].replace("gsw::", "")
-    parts = [f"{name:28s}", f"time={t * 1e6:10.1f}us" if t else "time=?"]
-    if rd is not None and wr is not None:
-        parts.append(f"dram={(rd + wr) / 1e6:10.1f}MB")
-        if t:
-            parts.append(f"dram_GBps={(rd + wr) / t / 1e9:7.1f}")
-    for k, lab in [("dram__throughput.avg.pct_of_peak_sustained_elapsed", "dram%"),
-                   ("sm__throughput.avg.pct_of_peak_sustained_elapsed", "sm%"),
-                   ("sm__warps_active.avg.pct_of_peak_sustained_active", "warps%"),
-                   ("sm__pipe_tensor_op_hmma_cycles_active.avg.pct_of_peak_sustained_active", "tensor%"),
-                   ("launch__registers_per_thread", "regs"), ("launch__grid_size", "grid")]:
-        if k in d and d[k][0] not in ("", "n/a"):
-            parts.append(f"{lab}={d[k][0]}")
-    return " ".join(parts)
+        t = num("gpu__time_duration.sum")
+        dram = num("dram__bytes_read.sum") + num("dram__bytes_write.sum")
+        stalls = sorted(((num(k), k) for k in h if "issue_stalled" in k and k.endswith("per_issue_active.ratio")),
+                        reverse=True)[:4]
+        st = ", ".join(f"{k.split('issue_stalled_')[1].split('_per')[0]} {x:.2f}" for x, k in stalls)
+        name = d.get("Kernel Name", "?").split("(")[0]
+        print(f"{os.path.basename(rep)[5:-8]:8s} {name:40s} time={t * 1e6:10.1f}us dram={dram / 1e6:9.1f}MB "
+              f"dram_GBps={dram / t / 1e9 if t > 0 else 0:7.1f} "
+              f"issue%={num('sm__issue_active.avg.pct_of_peak_sustained_elapsed'):5.1f} "
+              f"sm%={num('sm__throughput.avg.pct_of_peak_sustained_elapsed'):5.1f} "
+              f"warps%={num('sm__warps_active.avg.pct_of_peak_sustained_active'):5.1f} "
+              f"regs={d.get('launch__registers_per_thread', '?')} grid={d.get('launch__grid_size', '?')} "
+              f"stalls: {st}")
+    return 0
 
 
 if __name__ == "__main__":
-    for p in sys.argv[1:]:
-        print(summarize(p))
+    sys.exit(main())
