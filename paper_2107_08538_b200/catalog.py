@@ -16,6 +16,7 @@ staged copy of each template's inputs, not one per job.
 from __future__ import annotations
 
 import math
+import os
 import random
 from dataclasses import dataclass
 
@@ -220,8 +221,15 @@ def algorithmic_work(job: Job) -> tuple[float, str]:
     """(work, unit) per job run — SURVEY.md §8d's per-unit figures times the
     units a run processes: bytes for HBM-bound kernels, flops for lud."""
     n, it, m = job.n, max(job.iters, 1), job.m
-    if job.kind == "hotspot":  # two steps per pass: read T and P, write T once per pass
-        return 12.0 * n * n * (it // 2 + it % 2), "B"
+    if job.kind == "hotspot":
+        # read T and P, write T once per pass; passes of four steps
+        # (hotspot_pass4) while four remain, then two-step passes, then an
+        # odd single step (csrc/gs_work.cu run_kernels; GS_HOTSPOT_STEPS=2
+        # runs two-step passes only)
+        passes = it // 4 + (it % 4) // 2 + it % 2
+        if os.environ.get("GS_HOTSPOT_STEPS", "")[:1] == "2":
+            passes = it // 2 + it % 2
+        return 12.0 * n * n * passes, "B"
     if job.kind == "srad":  # fused coefficient + update: read J, write J
         return 8.0 * n * n * it, "B"
     if job.kind == "bfs":

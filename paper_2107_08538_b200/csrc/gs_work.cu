@@ -214,12 +214,16 @@ int srad_grid() {
   return (v == '3' || v == '1' || v == 'a' ? 4 : 3) * sm_count();
 }
 
-bool hotspot_four_steps() {
-  static const bool four = [] {
+// hotspot pass kernel: 4 = hotspot_pass4 (default), 2 = two-step passes
+// only (GS_HOTSPOT_STEPS=2), 5 = the first four-step kernel (=s)
+int hotspot_pass_mode() {
+  static const int m = [] {
     const char *e = getenv("GS_HOTSPOT_STEPS");
-    return e && e[0] == '4';
+    if (e && e[0] == '2') return 2;
+    if (e && e[0] == 's') return 5;
+    return 4;
   }();
-  return four;
+  return m;
 }
 
 // The job's kernels, in the order its host code first launches them.
@@ -230,13 +234,19 @@ static std::vector<Shape> job_kernels(const gs_job_desc &j) {
       return {{(const void *)bfs_expand, g, kBfsThreads}, {(const void *)bfs_commit, g, kBfsThreads}};
     case GS_JOB_HOTSPOT:
     {
-      // (the last two-step pass is the digesting instance)
+      // (the last pass is a digesting instance)
       Shape s2{(const void *)hotspot_step2<false>, g, kThreads}, s2d{(const void *)hotspot_step2<true>, g, kThreads};
       s2.dsmem = s2d.dsmem = kHs2Smem;
-      if (j.iters < 4 || !hotspot_four_steps()) return {s2, s2d, {(const void *)hotspot_step, g, kThreads}};
-      Shape s4{(const void *)hotspot_step4, g, kThreads};
-      s4.dsmem = kHs4Smem;
-      return {s4, s2, s2d, {(const void *)hotspot_step, g, kThreads}};
+      const int mode = hotspot_pass_mode();
+      if (j.iters < 4 || mode == 2) return {s2, s2d, {(const void *)hotspot_step, g, kThreads}};
+      if (mode == 5) {
+        Shape s4{(const void *)hotspot_step4, g, kThreads};
+        s4.dsmem = kHs4Smem;
+        return {s4, s2, s2d, {(const void *)hotspot_step, g, kThreads}};
+      }
+      Shape p4{(const void *)hotspot_pass4<false>, g, kThreads}, p4d{(const void *)hotspot_pass4<true>, g, kThreads};
+      p4.dsmem = p4d.dsmem = kP4Smem;
+      return {p4, p4d, s2, s2d, {(const void *)hotspot_step, g, kThreads}};
     }
     case GS_JOB_SRAD:
       return {{(const void *)srad_stats, 1, kThreads},
@@ -568,12 +578,37 @@ int run_kernels(const gs_job_desc &j, std::vector<void *> &buf, cudaStream_t st,
       if (rc) return rc;
       const CUtensorMap *min = &mt, *min2 = &mt2;
       int it = 0;
-      // GS_HOTSPOT_STEPS=4: four steps per pass while four remain (~3 B per
-      // cell-step).  Opt-in: measured 28.7 vs 23.7 ms at 24576^2 x 40 — the
-      // four barrier-separated steps at 16 warps per SM issue at 53 % and
-      // ~20 instructions per cell update (ncu, profiles/r02_hotspot_step4.txt),
-      // so it is issue bound above the two-step pass's HBM time
-      if (hotspot_four_steps() && it + 3 < j.iters) {
+      // Four steps per pass while four remain (hotspot_pass4: 120 x 32 tiles
+      // in 128-wide boxes, ~3.2 B per cell-step), then two-step passes and
+      // an odd last step.  GS_HOTSPOT_STEPS=2: two-step passes only (the
+      // round-1 / early round-2 path); =s: the first four-step kernel
+      // (hotspot_step4: 136-wide boxes with a separate halo-column phase,
+      // issue bound: 28.7 ms at 24576^2 x 40, profiles/r02_hotspot_step4.txt)
+      const int mode = hotspot_pass_mode();
+      if (mode == 4 && it + 3 < j.iters) {
+        CUW(cudaFuncSetAttribute(hotspot_pass4<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kP4Smem));
+        CUW(cudaFuncSetAttribute(hotspot_pass4<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kP4Smem));
+        CUtensorMap m4, m42, mp4, ms4;
+        rc = make_tmap_f32(&m4, t, n, n, kP4W, kP4H);
+        if (!rc) rc = make_tmap_f32(&m42, t2, n, n, kP4W, kP4H);
+        if (!rc) rc = make_tmap_f32(&mp4, p, n, n, kP4W, kP4H);
+        if (!rc) rc = make_tmap_f32(&ms4, t0, n, n, kP4W, kP4H);
+        if (rc) return rc;
+        const CUtensorMap *q = &m4, *q2 = &m42;
+        for (; it + 3 < j.iters; it += 4) {
+          const bool last = dg && it + 4 == j.iters;
+          if (last)
+            hotspot_pass4<true><<<g, 256, kP4Smem, st>>>(it ? *q : ms4, mp4, t2, (int)n, cc, rx1, ry1, rz1, tk, dg);
+          else
+            hotspot_pass4<false><<<g, 256, kP4Smem, st>>>(it ? *q : ms4, mp4, t2, (int)n, cc, rx1, ry1, rz1, tk,
+                                                          nullptr);
+          if (last) *digested = true;
+          ++launches;
+          std::swap(t, t2);
+          std::swap(q, q2);
+          std::swap(min, min2);  // the two-step maps follow the buffers
+        }
+      } else if (mode == 5 && it + 3 < j.iters) {
         CUW(cudaFuncSetAttribute(hotspot_step4, cudaFuncAttributeMaxDynamicSharedMemorySize, kHs4Smem));
         CUtensorMap m4, m42, mp4, ms4;
         rc = make_tmap_f32(&m4, t, n, n, kHs4W, kHs4H);
@@ -587,7 +622,7 @@ int run_kernels(const gs_job_desc &j, std::vector<void *> &buf, cudaStream_t st,
           ++launches;
           std::swap(t, t2);
           std::swap(q, q2);
-          std::swap(min, min2);  // the two-step maps follow the buffers
+          std::swap(min, min2);
         }
       }
       for (; it + 1 < j.iters; it += 2) {
