@@ -18,7 +18,7 @@ cap() {  # name regex skip cmd...
   timeout 300 $NCU -k regex:$rx -s $skip -c 1 -o $OUT/prof_$name -f "$@" > $OUT/prof_$name.log 2>&1 \
     || echo "capture $name failed/timeout" >> $OUT/prof_errors.log
 }
-cap hotspot hotspot_step2 2 python tools/debug_job.py hotspot 24576 8
+cap hotspot hotspot_pass4 1 python tools/debug_job.py hotspot 24576 16
 cap srad srad_stream 3 python tools/debug_job.py srad 24576 5
 cap kmeans kmeans_assign 2 python tools/debug_job.py kmeans 32000000 4 34
 cap bfs bfs_expand 9 python tools/debug_job.py bfs 128000000

@@ -14,7 +14,7 @@ import sys
 
 # kind -> (capture name, kernel, size note, algorithmic bytes of ONE launch)
 KINDS = {
-    "hotspot": ("hotspot", "hotspot_step2", "24576^2, one two-step pass", 12.0 * 24576 ** 2),
+    "hotspot": ("hotspot", "hotspot_pass4", "24576^2, one four-step pass", 12.0 * 24576 ** 2),
     "srad": ("srad", "srad_stream", "24576^2, one iteration", 8.0 * 24576 ** 2),
     "kmeans": ("kmeans", "kmeans_assign<34>", "32M x 34, one iteration", 4.0 * 32e6 * 34 + 4.0 * 32e6),
     "backprop": ("bpadj", "bp_adjust", "48M x 16", None),
