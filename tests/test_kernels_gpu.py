@@ -20,6 +20,13 @@ CASES = [
     ("hotspot", dict(n=1024, iters=3, seed=5), "exact"),   # one two-step pass + one single step
     ("hotspot", dict(n=128, iters=2, seed=6), "exact"),    # grid edges on every side of one tile column
     ("hotspot", dict(n=256, iters=5, seed=7), "exact"),
+    # four-step passes (120 x 32 tiles in 128-wide boxes): an east edge that
+    # falls exactly on a tile boundary (1920 = 16 x 120), one inside the last
+    # tile (640), and pass4 + two-step + single-step remainders
+    ("hotspot", dict(n=1920, iters=8, seed=11), "exact"),
+    ("hotspot", dict(n=640, iters=4, seed=12), "exact"),
+    ("hotspot", dict(n=640, iters=7, seed=13), "exact"),
+    ("hotspot", dict(n=384, iters=6, seed=14), "exact"),
     ("srad", dict(n=512, iters=5, seed=4), "exact"),
     ("srad", dict(n=128, iters=3, seed=8), "exact"),     # one tile: every halo is a grid edge
     ("srad", dict(n=384, iters=2, seed=9), "exact"),
