@@ -255,7 +255,7 @@ static std::vector<Shape> job_kernels(const gs_job_desc &j) {
     {
       Shape a{(const void *)kmeans_assign_fn((int)j.m), g, kThreads};
       a.dsmem = kKmSmem;
-      return {a, {(const void *)kmeans_recenter, 1, kThreads}};
+      return {{(const void *)kmeans_init, 1, kThreads}, a, {(const void *)kmeans_recenter, 1, kThreads}};
     }
     case GS_JOB_BACKPROP:
       return {{(const void *)bp_forward, g, kThreads}, {(const void *)bp_output, 1, 32 * kMaxHid},
@@ -669,11 +669,8 @@ int run_kernels(const gs_job_desc &j, std::vector<void *> &buf, cudaStream_t st,
       float *cent = (float *)buf[2];
       auto *sumq = (unsigned long long *)buf[3], *cnt = (unsigned long long *)buf[4];
       const int nf = (int)j.m;
-      CUW(cudaMemsetAsync(sumq, 0, (size_t)GS_KMEANS_K * nf * 8, st));
-      CUW(cudaMemsetAsync(cnt, 0, GS_KMEANS_K * 8, st));
-      for (int f = 0; f < nf; ++f)  // initial centroids: the first K points
-        CUW(cudaMemcpy2DAsync(cent + f, nf * 4, x + (int64_t)f * n, 4, 4, GS_KMEANS_K, cudaMemcpyDeviceToDevice,
-                              st));
+      kmeans_init<<<1, kThreads, 0, st>>>(x, n, nf, cent, sumq, cnt);  // the first K points, zeroed sums
+      ++launches;
       CUW(cudaFuncSetAttribute(kmeans_assign_fn(nf), cudaFuncAttributeMaxDynamicSharedMemorySize, kKmSmem));
       for (int it = 0; it < j.iters; ++it) {
         kmeans_assign_fn(nf)<<<g, kThreads, kKmSmem, st>>>(x, n, nf, cent, mem, sumq, cnt, tk);
