@@ -570,6 +570,12 @@ def drive(args, devices, torch, barrier):
     for k in ("survey_8d_bytes", "frac_survey_8d"):
         if k in kd:
             roof[k] = kd[k]
+    if dom == "hotspot":
+        roof["note"] = ("four time steps per TMA-fed pass (hotspot_pass4): 12 B per cell per pass = 3 B per "
+                        "cell-step, ncu DRAM per launch = the algorithmic bytes; the pass is issue / barrier bound "
+                        "(ncu: 47 % issue-active, profiles/r02j_ncu_current_kernels.txt), 25 % faster than the "
+                        "two-step pass that ran at 0.95 of HBM; frac_survey_8d restates on SURVEY §8(d)'s 12 B per "
+                        "cell-step")
     # aggregate HBM roofline fraction of the whole mix
     mix_bytes = sum(C.algorithmic_work(j)[0] for j in jobs if C.algorithmic_work(j)[1] == "B")
     mix_frac = mix_bytes / (ours["ms_per_step"] / 1000.0) / 1e9 / (pk["hbm_gbs"] * len(devices))
