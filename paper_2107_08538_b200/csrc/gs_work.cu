@@ -259,7 +259,7 @@ static std::vector<Shape> job_kernels(const gs_job_desc &j) {
     }
     case GS_JOB_BACKPROP:
       return {{(const void *)bp_forward, g, kThreads}, {(const void *)bp_output, 1, 32 * kMaxHid},
-              {(const void *)bp_adjust, g, kThreads}};
+              {(const void *)bp_adjust<false>, g, kThreads}, {(const void *)bp_adjust<true>, g, kThreads}};
     case GS_JOB_NEEDLE:
     {
       Shape s{needle8(j) ? (const void *)needle_bands8 : (const void *)needle_bands, needle_grid(j), 32};
@@ -689,14 +689,21 @@ int run_kernels(const gs_job_desc &j, std::vector<void *> &buf, cudaStream_t st,
       // it is written before it is read (PING); the first iteration reads
       // the weights from `source(1)` and writes w1
       const float *w0 = (const float *)source(1);
+      // the first forward pass alone; every later one is fused into the
+      // previous iteration's weight update (bp_adjust<true>)
+      const int ntiles = (int)((n + 1 + kBpTile - 1) / kBpTile);
+      bp_forward<<<g, kThreads, 0, st>>>(x, w0, n + 1, nh, partial, tk);
+      ++launches;
       for (int it = 0; it < j.iters; ++it) {
-        const int ntiles = (int)((n + 1 + kBpTile - 1) / kBpTile);
-        bp_forward<<<g, kThreads, 0, st>>>(x, it ? w1 : w0, n + 1, nh, partial, tk);
         bp_output<<<1, 32 * kMaxHid, 0, st>>>(partial, ntiles, nh, state);
-        bp_adjust<<<g, kThreads, 0, st>>>(x, it ? w1 : w0, w1, ow1, it == 0, n + 1, nh, state, tk,
-                                          it + 1 == j.iters ? dg : nullptr);
+        if (it + 1 < j.iters)
+          bp_adjust<true><<<g, kThreads, 0, st>>>(x, it ? w1 : w0, w1, ow1, it == 0, n + 1, nh, state, tk, nullptr,
+                                                  partial);
+        else
+          bp_adjust<false><<<g, kThreads, 0, st>>>(x, it ? w1 : w0, w1, ow1, it == 0, n + 1, nh, state, tk, dg,
+                                                   nullptr);
         if (dg && it + 1 == j.iters) *digested = true;
-        launches += 3;
+        launches += 2;
       }
       *out_idx = 1;
       break;
