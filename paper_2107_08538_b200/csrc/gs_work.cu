@@ -417,8 +417,12 @@ int derive_inputs(const gs_job_desc &j, std::vector<void *> &buf, cudaStream_t s
   bfs_indeg<<<g, kThreads, 0, st>>>(col, n * GS_BFS_DEGREE, in_row + 1);
   size_t tmp_bytes = 0;
   CUW(cub::DeviceScan::InclusiveSum(nullptr, tmp_bytes, in_row + 1, in_row + 1, (int)n, st));
-  if (tmp_bytes > v_bytes) return err(GS_ERR_CONFIG, "bfs: scan scratch exceeds the visited bitmap");
-  CUW(cub::DeviceScan::InclusiveSum(buf[4], tmp_bytes, in_row + 1, in_row + 1, (int)n, st));
+  // (a tiny graph's bitmap can be smaller than the scan's scratch: then a
+  // stream-ordered allocation of a few KB)
+  void *tmp = buf[4];
+  if (tmp_bytes > v_bytes) CUW(cudaMallocAsync(&tmp, tmp_bytes, st));
+  CUW(cub::DeviceScan::InclusiveSum(tmp, tmp_bytes, in_row + 1, in_row + 1, (int)n, st));
+  if (tmp != buf[4]) CUW(cudaFreeAsync(tmp, st));
   CUW(cudaMemcpyAsync(cursor, in_row, n * 4, cudaMemcpyDeviceToDevice, st));
   bfs_scatter<<<g, kThreads, 0, st>>>(row, col, n, cursor, (int32_t *)buf[8]);
   CUW(cudaMemsetAsync(buf[4], 0, v_bytes, st));

@@ -196,6 +196,7 @@ def test_executor_e2e_rebuilds_derived_inputs():
     boundary; outputs still equal the solo runs and the bytes moved equal
     gs_job_io_bytes (less than the jobs' whole input buffers)."""
     jobs = [W.Job("bfs", n=300_000, seed=41), W.Job("needle", n=1024, seed=42), W.Job("bfs", n=1_000_003, seed=43),
+            W.Job("bfs", n=1000, seed=46),  # bitmap smaller than the scan's scratch
             W.Job("needle", n=512, seed=44), W.Job("hotspot", n=512, iters=3, seed=45)]
     solo = [W.run_solo(j)[1].checksum for j in jobs]
     W.stage(jobs, [0], W.MODE_E2E)
