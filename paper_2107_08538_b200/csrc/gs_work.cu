@@ -244,7 +244,8 @@ static std::vector<Shape> job_kernels(const gs_job_desc &j) {
         s4.dsmem = kHs4Smem;
         return {s4, s2, s2d, {(const void *)hotspot_step, g, kThreads}};
       }
-      Shape p4{(const void *)hotspot_pass4<false>, g, kThreads}, p4d{(const void *)hotspot_pass4<true>, g, kThreads};
+      Shape p4{(const void *)hotspot_pass4<false, kP4Warps>, g, 32 * kP4Warps},
+          p4d{(const void *)hotspot_pass4<true, kP4Warps>, g, 32 * kP4Warps};
       p4.dsmem = p4d.dsmem = kP4Smem;
       return {p4, p4d, s2, s2d, {(const void *)hotspot_step, g, kThreads}};
     }
@@ -590,8 +591,8 @@ int run_kernels(const gs_job_desc &j, std::vector<void *> &buf, cudaStream_t st,
       // issue bound: 28.7 ms at 24576^2 x 40, profiles/r02_hotspot_step4.txt)
       const int mode = hotspot_pass_mode();
       if (mode == 4 && it + 3 < j.iters) {
-        CUW(cudaFuncSetAttribute(hotspot_pass4<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kP4Smem));
-        CUW(cudaFuncSetAttribute(hotspot_pass4<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kP4Smem));
+        CUW(cudaFuncSetAttribute(hotspot_pass4<false, kP4Warps>, cudaFuncAttributeMaxDynamicSharedMemorySize, kP4Smem));
+        CUW(cudaFuncSetAttribute(hotspot_pass4<true, kP4Warps>, cudaFuncAttributeMaxDynamicSharedMemorySize, kP4Smem));
         CUtensorMap m4, m42, mp4, ms4;
         rc = make_tmap_f32(&m4, t, n, n, kP4W, kP4H);
         if (!rc) rc = make_tmap_f32(&m42, t2, n, n, kP4W, kP4H);
@@ -602,10 +603,11 @@ int run_kernels(const gs_job_desc &j, std::vector<void *> &buf, cudaStream_t st,
         for (; it + 3 < j.iters; it += 4) {
           const bool last = dg && it + 4 == j.iters;
           if (last)
-            hotspot_pass4<true><<<g, 256, kP4Smem, st>>>(it ? *q : ms4, mp4, t2, (int)n, cc, rx1, ry1, rz1, tk, dg);
+            hotspot_pass4<true, kP4Warps><<<g, 32 * kP4Warps, kP4Smem, st>>>(it ? *q : ms4, mp4, t2, (int)n, cc, rx1,
+                                                                              ry1, rz1, tk, dg);
           else
-            hotspot_pass4<false><<<g, 256, kP4Smem, st>>>(it ? *q : ms4, mp4, t2, (int)n, cc, rx1, ry1, rz1, tk,
-                                                          nullptr);
+            hotspot_pass4<false, kP4Warps><<<g, 32 * kP4Warps, kP4Smem, st>>>(it ? *q : ms4, mp4, t2, (int)n, cc, rx1,
+                                                                               ry1, rz1, tk, nullptr);
           if (last) *digested = true;
           ++launches;
           std::swap(t, t2);
