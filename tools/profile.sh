@@ -25,7 +25,7 @@ cap bfs bfs_expand 9 python tools/debug_job.py bfs 128000000
 cap needle needle_bands 0 python tools/debug_job.py needle 24576
 cap lud lud_internal 20 python tools/debug_job.py lud 6144
 cap ludp lud_panel 20 python tools/debug_job.py lud 6144
-cap bpfwd bp_forward 1 python tools/debug_job.py backprop 48000000 2 16
+cap bpfwd bp_forward 0 python tools/debug_job.py backprop 48000000 2 16
 cap bpadj bp_adjust 1 python tools/debug_job.py backprop 48000000 2 16
 cap gemm gemm_bf16_tc 4 python tools/debug_job.py yolo 608 1 32
 cap decide gs_interp 0 python -c "import __graft_entry__ as g; g.smoke()"
